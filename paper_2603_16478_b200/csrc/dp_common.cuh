@@ -1,0 +1,82 @@
+// Deterministic block / grid reductions used by every reducing kernel.
+// Grid-wide results use the "last block finishes" pattern: each block writes
+// its partial, the last block to arrive (atomic ticket) folds the partials in
+// block order, so results are bitwise run-to-run reproducible (no float
+// atomics anywhere in the library).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace dp {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// sum over the block; result valid in thread 0.  `sh` >= 32 doubles.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (NT > 32) {
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    v = (threadIdx.x < NT / 32) ? sh[threadIdx.x] : 0.0;
+    if (wid == 0) v = warp_sum(v);
+    __syncthreads();
+  }
+  return v;
+}
+template <int NT>
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  v = warp_max(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (NT > 32) {
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    v = (threadIdx.x < NT / 32) ? sh[threadIdx.x] : 0.0;
+    if (wid == 0) v = warp_max(v);
+    __syncthreads();
+  }
+  return v;
+}
+
+// Call from all threads after the block's partials are stored by thread 0.
+// Returns true in every thread of the last block to arrive.
+__device__ __forceinline__ bool last_block(unsigned int* counter) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t = atomicAdd(counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  return s_last;
+}
+
+// In the last block: fold W partial columns (partial[b*W + k]) over blocks
+// b in [0, nb) in a fixed order; result[k] in thread 0 returned via out[k]
+// (shared memory, visible to all threads after the call).
+template <int NT, int W>
+__device__ __forceinline__ void fold_partials(const double* partial, int nb, double* out, double* sh, bool is_max = false) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    double v = is_max ? 0.0 : 0.0;
+    for (int b = threadIdx.x; b < nb; b += NT) {
+      double p = __ldcg(partial + (size_t)b * W + k);
+      v = is_max ? fmax(v, p) : v + p;
+    }
+    v = is_max ? block_max<NT>(v, sh) : block_sum<NT>(v, sh);
+    if (threadIdx.x == 0) out[k] = v;
+    __syncthreads();
+  }
+}
+
+}  // namespace dp

@@ -1,0 +1,243 @@
+// Internal declarations shared by the CUDA translation units of
+// libdiffproj_b200.so.  Not part of the ABI (see include/diffproj_b200.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/diffproj_b200.h"
+
+namespace dp {
+
+constexpr int kSlice = 32;          // SELL slice height (rows per warp)
+constexpr int kMaxColliders = 64;
+
+// Status word written by kernels (bit-or of ST_* codes, dp_math.cuh).
+// Reduction scalars of the Newton loop live in one struct so one D2H copy
+// returns everything the host needs per evaluation.
+struct EvalScalars {
+  double rmax;          // max |r|
+  double rnorm2;        // |r|_2^2
+  double scale_max;     // max |m * q_hat|  (forward.py:169-171)
+  int status;           // OR of element / contact status bits
+  int penetrating;      // any gap <= 0 (forward.py:86-93)
+  int n_contacts;
+  int asym;             // any active contact with mu != 0
+};
+
+// Krylov scalars (device resident; the host only polls `done`).
+struct KrylovScalars {
+  double alpha, beta, gamma, delta, rho;   // CG recurrences
+  double bnorm2, tol2;                      // |b|^2, (tol*|b|)^2
+  int done;                                 // 1 converged, 2 breakdown
+  int iters;
+  double pad[2];
+};
+
+constexpr int kMaxRestart = 50;
+struct GmresScalars {
+  double H[kMaxRestart * (kMaxRestart + 1)];   // column j at H[j*(m+1) + i]
+  double cs[kMaxRestart], sn[kMaxRestart], g[kMaxRestart + 1];
+  double coef[kMaxRestart + 1];                 // coefficients of the current pass
+  double wn2_before;                            // |w|^2 before orthogonalisation
+  double hn;                                    // H[j+1, j] before rotation
+  double beta;                                  // |M^-1 r0|
+  double nmb;                                   // |M^-1 b|
+  double thr;                                   // stop when |g[j+1]| <= thr
+  double est;                                   // |g[j+1]| / nmb
+  int done;                                     // 1 inner stop, 2 lucky breakdown
+  int reorth;
+  int used;
+  int pad;
+};
+
+struct ColliderSet {
+  int n;
+  int kind[kMaxColliders];
+  double vec[kMaxColliders][3];
+  double scalar[kMaxColliders];
+  double mu[kMaxColliders];
+};
+
+// reduction scratch: partial sums per block + a completion counter
+struct Reduce {
+  double* partial = nullptr;     // [nblocks * width]
+  unsigned int* counter = nullptr;
+  int cap_blocks = 0;
+  int width = 0;
+};
+
+template <class T>
+struct DArr {
+  T* p = nullptr;
+  size_t n = 0;
+};
+
+}  // namespace dp
+
+struct dp_cache {
+  dp_scene* scene = nullptr;
+  int V = 0;
+  int valid = 0;
+  double *q_bar = nullptr, *v_bar = nullptr, *q_hat = nullptr, *q_new = nullptr, *q_eval = nullptr;
+  // contact records of the final evaluation
+  int n_contacts = 0;
+  int cap_contacts = 0;
+  int* c_vertex = nullptr;
+  int* c_collider = nullptr;
+  double* c_frame = nullptr;   // C*9
+  double* c_dn = nullptr;
+  double* c_mu = nullptr;
+  double* c_delta = nullptr;   // C*3 (lam/s/capped/Kc are functions of delta)
+  int asym = 0;
+  // colliders / bindings used by the step (bindings are needed by backprop)
+  dp::ColliderSet colliders;
+};
+
+struct dp_scene {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int V = 0, E = 0, NV = 4, D = 3, NP = 10;
+  double h = 0.01, eps_fb = 1e-6, act = 1e-3, grav[3] = {0, 0, -9.8};
+  int64_t nnzb = 0;
+  int64_t NS = 0;            // SELL slots
+  int S = 0;                 // slices
+  size_t bytes = 0;
+
+  // host mirrors
+  std::vector<double> h_vol, h_w, h_mass;
+  std::vector<int> h_model;
+  std::vector<double> h_E, h_nu;
+  std::vector<int> h_rowptr, h_colidx;   // CSR block pattern
+  std::vector<int64_t> h_block_slot;     // CSR block -> SELL slot
+  std::vector<int> h_orig;               // element order on device -> original index (identity)
+
+  // device element data (SoA)
+  int4* ev = nullptr;
+  double* B = nullptr;       // [9][E] (tets) or [4][E] (tris)
+  double *w = nullptr, *vol = nullptr, *mu = nullptr, *lam = nullptr;
+  int* model = nullptr;
+  int any_nh = 0;
+
+  // per-vertex
+  double* mass = nullptr;
+  int *inc_ptr = nullptr, *inc = nullptr;
+
+  // SELL-32 BSR
+  int *slice_base = nullptr, *slice_width = nullptr, *col = nullptr, *diag_slot = nullptr;
+  int *row_slot_ptr = nullptr;     // unused padding helper
+  double* val_fwd = nullptr;       // forward Newton matrix
+  double* val_adj = nullptr;       // adjoint operator (transposed contact blocks)
+  double* val_A = nullptr;         // constant A (lazy, export only)
+  int *contrib_ptr = nullptr, *contrib = nullptr;
+  double* minv = nullptr;          // block-Jacobi inverses [9][V]
+
+  // element outputs
+  double* fe = nullptr;            // E*NV*3
+  double* H = nullptr;             // E*NP*9
+  double* Pst = nullptr;           // E*27 (P, dP/dmu, dP/dlam) for backprop
+
+  // colliders / bindings / fext
+  dp::ColliderSet colliders;
+  dp::ColliderSet* d_colliders = nullptr;
+  int nb = 0;
+  std::vector<int> hb_vertex;
+  std::vector<double> hb_target, hb_comp;
+  int *b_ptr = nullptr, *b_idx = nullptr;   // per-vertex CSR of binding ids
+  double *b_target = nullptr, *b_comp = nullptr;
+  int* b_vertex = nullptr;
+  double* fext = nullptr;   // 3V, zero when unset
+  int has_fext = 0;
+
+  // contacts (capacity V * n_colliders)
+  int ccap = 0;
+  int *c_count = nullptr, *c_off = nullptr, *c_vertex = nullptr, *c_collider = nullptr;
+  double *c_frame = nullptr, *c_dn = nullptr, *c_mu = nullptr, *c_delta = nullptr;
+  double *c_blk = nullptr, *c_force = nullptr, *c_kmu = nullptr, *c_kc = nullptr;
+  void* scan_tmp = nullptr;
+  size_t scan_tmp_bytes = 0;
+
+  // vectors (3V each)
+  double *q = nullptr, *q_hat = nullptr, *q_bar = nullptr, *v_bar = nullptr, *r = nullptr, *dq = nullptr;
+  double *q_try = nullptr, *rhs = nullptr, *z = nullptr, *tmp = nullptr, *q_ev = nullptr, *r_try = nullptr;
+  // Krylov workspace
+  double *kx = nullptr, *kr = nullptr, *ku = nullptr, *kw = nullptr, *kp = nullptr, *ks = nullptr;
+  double* gm_V = nullptr;          // (restart+1) * 3V basis
+  int gm_cap = 0;
+  dp::KrylovScalars* ksc = nullptr;
+  dp::GmresScalars* gsc = nullptr;
+  dp::EvalScalars* esc = nullptr;
+  dp::EvalScalars* h_esc = nullptr;     // pinned
+  dp::KrylovScalars* h_ksc = nullptr;   // pinned
+  dp::GmresScalars* h_gsc = nullptr;    // pinned
+  dp::Reduce red;
+
+  // gradient accumulators
+  double* g_dw = nullptr;       // E
+  double* g_scal = nullptr;     // [mu_fric, stiffness, dmu_lame, dlam_lame]
+  double* g_dEb = nullptr;      // nb
+  double* g_ddb = nullptr;      // nb*3
+  int g_nb_cap = 0;
+
+  // timing
+  int timing = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  dp_kernel_times times{};
+  int64_t launches = 0;
+
+  // last assembled operator: symmetric flag
+  int last_sym_fwd = 1, last_sym_adj = 1;
+};
+
+namespace dp {
+
+// error helpers -------------------------------------------------------------
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+#define DP_CUDA(call)                                         \
+  do {                                                        \
+    cudaError_t _e = (call);                                  \
+    if (_e != cudaSuccess) return dp::cuda_fail(_e, #call);   \
+  } while (0)
+
+int grid_for(int64_t n, int threads);
+
+// launchers (dp_kernels.cu) -----------------------------------------------
+// element evaluation: mode bit 1 = jacobian blocks, bit 2 = store P/dP for
+// backprop, bit 4 = zero jacobian (A-matrix assembly).
+enum { EV_JAC = 1, EV_STOREP = 2, EV_AMAT = 4 };
+void launch_elements(dp_scene* s, const double* q, int mode, int* status);
+// residual gather r = M(q - q_hat) + sum_e f_e - h^2 J_b^T lam_b + contact forces; max|r| into esc
+void launch_residual(dp_scene* s, const double* q, const double* q_hat, double* r, dp::EvalScalars* esc);
+// BSR gather: val = M + sum_e H_e + K_b + (K_c or K_c^T); plus block-Jacobi inverses
+void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat);
+void launch_spmv(dp_scene* s, const double* val, const double* x, double* y);
+// Krylov
+int cg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
+             int* iters, double* relres, int* breakdown);
+int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
+                int restart, int* iters, double* relres);
+double device_norm2(dp_scene* s, const double* x);   // sum of squares, synchronous
+// vector ops
+void launch_axpy_to(dp_scene* s, double* out, const double* a, double t, const double* b);   // out = a + t*b
+void launch_predict(dp_scene* s);   // q_hat, q (pre-pullback copy), scale
+void launch_velocity(dp_scene* s, const double* q, const double* q_bar, double* v);
+void launch_reset_eval(dp_scene* s, dp::EvalScalars* esc);
+// backprop
+void launch_backprop(dp_scene* s, const dp_cache* c, const double* z, const double* dL_dv,
+                     double* dqbar, double* dvbar, double* dfext);
+
+// launchers (dp_contact.cu) ------------------------------------------------
+void launch_pullback(dp_scene* s, double* q, const double* q_bar, double margin);
+void launch_penetration(dp_scene* s, const double* q, dp::EvalScalars* esc);
+void launch_detect(dp_scene* s, const double* q);   // fills contact records + esc->n_contacts
+// per-contact condensation; writes c_delta, c_blk (h^2 fr^T Kc fr, or ^T if
+// transpose), c_force; status/asym bits into esc
+void launch_contacts(dp_scene* s, const double* q, const double* q_bar, int n_contacts,
+                     const int* vtx, const double* frame, const double* dn, const double* mu,
+                     double* delta_out, int from_delta, int transpose, dp::EvalScalars* esc);
+int contact_scan_setup(dp_scene* s);
+
+}  // namespace dp

@@ -1,0 +1,1460 @@
+// Element, assembly, SpMV, Krylov and backprop kernels of libdiffproj_b200.
+//
+// Data layout:
+//  * vectors: flat FP64, xyz-interleaved per vertex (the reference layout);
+//  * element inputs: SoA (Dm^-1 as [9][E], w/mu/lam/model as [E]) and the
+//    four vertex ids as one int4 per element (one 16-byte load);
+//  * element outputs: residual contributions fe[E][NV][3] and the NP
+//    unique 3x3 blocks of the symmetric element Hessian H[E][NP][9];
+//  * system matrix: SELL-32 block-sparse (3x3 FP64 blocks), slices of 32
+//    block rows, block k of lane l at slot base_s + 32k + l; block values
+//    component-major inside a slice so each warp load is 32 consecutive
+//    doubles (256 B).
+// Assembly is a deterministic gather (no atomics): every SELL slot owns a
+// list of (element, local block, transposed?) contributions.
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include "dp_common.cuh"
+#include "dp_internal.h"
+#include "dp_math.cuh"
+
+namespace dp {
+
+// ---------------------------------------------------------------------------
+// element kernel
+
+// Gt_a J G_b in the singular basis: U~ C U~^T with C built from W, the
+// (M, N) pair coefficients and (triangles) the out-of-plane term.
+template <int D>
+struct ElemJac {
+  double U3[3][3];      // [U | u3] for triangles, U for tets
+  double W[D][D];
+  double m[3], n[3];    // pairs (0,1), (0,2), (1,2) (tets) / (0,1) (tris)
+  double oop[2];        // theta/sigma (triangles)
+};
+
+template <int D>
+__device__ __forceinline__ void jac_block(const ElemJac<D>& J, const double aa[D], const double ab[D], double out[3][3]) {
+  double C[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+#pragma unroll
+    for (int l = 0; l < D; ++l) C[k][l] = aa[k] * J.W[k][l] * ab[l];
+  if (D == 3) {
+    const int pk[3] = {0, 0, 1}, pl[3] = {1, 2, 2};
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      const int k = pk[p], l = pl[p];
+      C[l][l] += J.m[p] * aa[k] * ab[k];
+      C[k][k] += J.m[p] * aa[l] * ab[l];
+      C[l][k] += J.n[p] * aa[k] * ab[l];
+      C[k][l] += J.n[p] * aa[l] * ab[k];
+    }
+  } else {
+    C[1][1] += J.m[0] * aa[0] * ab[0];
+    C[0][0] += J.m[0] * aa[1] * ab[1];
+    C[1][0] += J.n[0] * aa[0] * ab[1];
+    C[0][1] += J.n[0] * aa[1] * ab[0];
+    C[2][2] = J.oop[0] * aa[0] * ab[0] + J.oop[1] * aa[1] * ab[1];
+  }
+  // out = U C U^T
+  double T[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int l = 0; l < 3; ++l) T[i][l] = J.U3[i][0] * C[0][l] + J.U3[i][1] * C[1][l] + J.U3[i][2] * C[2][l];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) out[i][j] = T[i][0] * J.U3[j][0] + T[i][1] * J.U3[j][1] + T[i][2] * J.U3[j][2];
+}
+
+// Full per-element projection: F -> SVD -> theta, W -> P (+ jacobian data).
+// F is 3 x D.  Returns status.
+template <int D>
+__device__ __forceinline__ int project_full(const double F[3][D], int model, double mu, double lam, double tau_rel,
+                                            double U[3][D], double sig[D], double V[D][D], double th[D],
+                                            double W[D][D]) {
+  int st;
+  if (D == 3) st = svd3((const double(*)[3])F, (double(*)[3])U, sig, (double(*)[3])V);
+  else st = svd32((const double(*)[2])F, (double(*)[2])U, sig, (double(*)[2])V);
+  if (st) return st;
+  if (model == DP_MODEL_NEOHOOKEAN) {
+    st = nh_project<D>(sig, mu, lam, th, W);
+    if (st) return st;
+  } else {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      th[i] = 1.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) W[i][j] = 0.0;
+    }
+  }
+  return ST_OK;
+}
+
+template <int D>
+__device__ __forceinline__ void make_jac(const double U[3][D], const double sig[D], const double th[D],
+                                         const double W[D][D], double tau_rel, ElemJac<D>& J) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < D; ++k) J.U3[i][k] = U[i][k];
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) J.W[i][j] = W[i][j];
+  const double tau = tau_rel * sig[0];
+  if (D == 3) {
+    mn_pair(sig[0], sig[1], th[0], th[1], W[0][0], W[1][1], W[0][1], tau, J.m[0], J.n[0]);
+    mn_pair(sig[0], sig[2], th[0], th[2], W[0][0], W[2][2], W[0][2], tau, J.m[1], J.n[1]);
+    mn_pair(sig[1], sig[2], th[1], th[2], W[1][1], W[2][2], W[1][2], tau, J.m[2], J.n[2]);
+  } else {
+    mn_pair(sig[0], sig[1], th[0], th[1], W[0][0], W[1][1], W[0][1], tau, J.m[0], J.n[0]);
+    J.m[1] = J.m[2] = J.n[1] = J.n[2] = 0.0;
+    // u3 = u1 x u2 completes the basis (elasticity.py:302-305)
+    J.U3[0][2] = U[1][0] * U[2][1] - U[2][0] * U[1][1];
+    J.U3[1][2] = U[2][0] * U[0][1] - U[0][0] * U[2][1];
+    J.U3[2][2] = U[0][0] * U[1][1] - U[1][0] * U[0][1];
+    J.oop[0] = th[0] / sig[0];
+    J.oop[1] = th[1] / sig[1];
+  }
+}
+
+// One thread per element.  NV = vertices per element (4 tet, 3 tri).
+template <int NV>
+__global__ void __launch_bounds__(128) k_elements(const int4* __restrict__ ev, const double* __restrict__ Bm,
+                                                  const double* __restrict__ w, const double* __restrict__ mu,
+                                                  const double* __restrict__ lam, const int* __restrict__ model, int E,
+                                                  const double* __restrict__ q, double h2, double tau_rel, int mode,
+                                                  double* __restrict__ fe, double* __restrict__ H,
+                                                  double* __restrict__ Pst, int* __restrict__ status) {
+  constexpr int D = NV - 1;
+  constexpr int NP = NV * (NV + 1) / 2;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int4 vv = ev[e];
+  const int vid[4] = {vv.x, vv.y, vv.z, vv.w};
+  double beta[NV][D];
+#pragma unroll
+  for (int k = 1; k < NV; ++k)
+#pragma unroll
+    for (int c = 0; c < D; ++c) beta[k][c] = __ldg(Bm + (size_t)((k - 1) * D + c) * E + e);
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 1; k < NV; ++k) s += beta[k][c];
+    beta[0][c] = -s;
+  }
+  double x[NV][3];
+#pragma unroll
+  for (int a = 0; a < NV; ++a)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) x[a][i] = q[3 * (size_t)vid[a] + i];
+  double F[3][D];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < NV; ++a) s += x[a][i] * beta[a][c];
+      F[i][c] = s;
+    }
+  const double hw = h2 * w[e];
+  const int mdl = model[e];
+  const double emu = mu[e], elam = lam[e];
+
+  double U[3][D], sig[D], V[D][D], th[D], W[D][D];
+  int st = ST_OK;
+  if (mode & EV_AMAT) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) { sig[i] = 1.0; th[i] = 1.0; }
+  } else {
+    st = project_full<D>(F, mdl, emu, elam, tau_rel, U, sig, V, th, W);
+  }
+  if (st) {
+    atomicOr(status, st);
+#pragma unroll
+    for (int a = 0; a < NV; ++a)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) fe[((size_t)e * NV + a) * 3 + i] = 0.0;
+    return;
+  }
+  if (!(mode & EV_AMAT)) {
+    // P = U diag(theta) V^T ; fe_a = h^2 w (F - P) beta_a  (internal_force_and_rhs, elasticity.py:386-396)
+    double P[3][D];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) s += U[i][k] * th[k] * V[c][k];
+        P[i][c] = s;
+      }
+#pragma unroll
+    for (int a = 0; a < NV; ++a)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) s += (F[i][c] - P[i][c]) * beta[a][c];
+        fe[((size_t)e * NV + a) * 3 + i] = hw * s;
+      }
+    if (mode & EV_STOREP) {
+      double* o = Pst + (size_t)e * 27;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int c = 0; c < D; ++c) o[i * 3 + c] = P[i][c];
+      double dmu[D], dlm[D];
+      if (mdl == DP_MODEL_NEOHOOKEAN) {
+        nh_dtheta_dlame<D>(th, sig, emu, elam, dmu, dlm);
+      } else {
+#pragma unroll
+        for (int k = 0; k < D; ++k) dmu[k] = dlm[k] = 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) { s1 += U[i][k] * dmu[k] * V[c][k]; s2 += U[i][k] * dlm[k] * V[c][k]; }
+          o[9 + i * 3 + c] = s1;
+          o[18 + i * 3 + c] = s2;
+        }
+    }
+  }
+  if (mode & EV_JAC) {
+    ElemJac<D> J;
+    double alpha[NV][D];
+    const bool amat = (mode & EV_AMAT) != 0;
+    if (!amat) {
+      make_jac<D>(U, sig, th, W, tau_rel, J);
+#pragma unroll
+      for (int a = 0; a < NV; ++a)
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < D; ++c) s += V[c][k] * beta[a][c];
+          alpha[a][k] = s;
+        }
+    }
+    double* Ho = H + (size_t)e * NP * 9;
+    int p = 0;
+#pragma unroll
+    for (int a = 0; a < NV; ++a)
+#pragma unroll
+      for (int b = a; b < NV; ++b, ++p) {
+        double bb = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) bb += beta[a][c] * beta[b][c];
+        double blk[3][3];
+        if (amat) {
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) blk[i][j] = 0.0;
+        } else {
+          jac_block<D>(J, alpha[a], alpha[b], blk);
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) Ho[p * 9 + i * 3 + j] = hw * (((i == j) ? bb : 0.0) - blk[i][j]);
+      }
+  }
+}
+
+void launch_elements(dp_scene* s, const double* q, int mode, int* status) {
+  if (s->E == 0) return;
+  const int nt = 128;
+  const int nb = grid_for(s->E, nt);
+  const double h2 = s->h * s->h;
+  if (s->NV == 4)
+    k_elements<4><<<nb, nt, 0, s->stream>>>(s->ev, s->B, s->w, s->mu, s->lam, s->model, s->E, q, h2, 1e-6, mode,
+                                            s->fe, s->H, s->Pst, status);
+  else
+    k_elements<3><<<nb, nt, 0, s->stream>>>(s->ev, s->B, s->w, s->mu, s->lam, s->model, s->E, q, h2, 1e-6, mode,
+                                            s->fe, s->H, s->Pst, status);
+  s->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// residual gather: r = M (q - q_hat) + sum_e fe - h^2 J_b^T lam_b - h^2 J_c^T lam_c
+// (momentum_residual, forward.py:101-110), plus max|r| (forward.py:202).
+
+constexpr int kVT = 256;
+
+__global__ void __launch_bounds__(kVT) k_residual(int V, const double* __restrict__ mass, const double* __restrict__ q,
+                                                  const double* __restrict__ q_hat, const int* __restrict__ inc_ptr,
+                                                  const int* __restrict__ inc, const double* __restrict__ fe,
+                                                  const int* __restrict__ b_ptr, const int* __restrict__ b_idx,
+                                                  const double* __restrict__ b_target, const double* __restrict__ b_comp,
+                                                  const int* __restrict__ c_count, const int* __restrict__ c_off,
+                                                  const double* __restrict__ c_force, int has_contacts, double h2,
+                                                  double* __restrict__ r, double* partial, unsigned int* counter,
+                                                  EvalScalars* esc) {
+  __shared__ double sh[32];
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  double amax = 0.0, sq = 0.0;
+  if (i < V) {
+    const double m = mass[i];
+    double r0 = m * (q[3 * i] - q_hat[3 * i]);
+    double r1 = m * (q[3 * i + 1] - q_hat[3 * i + 1]);
+    double r2 = m * (q[3 * i + 2] - q_hat[3 * i + 2]);
+    for (int k = inc_ptr[i]; k < inc_ptr[i + 1]; ++k) {
+      const double* f = fe + (size_t)inc[k] * 3;
+      r0 += f[0]; r1 += f[1]; r2 += f[2];
+    }
+    if (b_ptr) {
+      for (int k = b_ptr[i]; k < b_ptr[i + 1]; ++k) {
+        const int b = b_idx[k];
+        const double c = h2 / b_comp[b];
+        r0 += c * (q[3 * i] - b_target[3 * b]);
+        r1 += c * (q[3 * i + 1] - b_target[3 * b + 1]);
+        r2 += c * (q[3 * i + 2] - b_target[3 * b + 2]);
+      }
+    }
+    if (has_contacts) {
+      const int c0 = c_off[i], cn = c_count[i];
+      for (int c = c0; c < c0 + cn; ++c) {
+        r0 += c_force[3 * c]; r1 += c_force[3 * c + 1]; r2 += c_force[3 * c + 2];
+      }
+    }
+    r[3 * i] = r0; r[3 * i + 1] = r1; r[3 * i + 2] = r2;
+    amax = fmax(fabs(r0), fmax(fabs(r1), fabs(r2)));
+    if (!(amax == amax)) amax = INFINITY;   // NaN propagates as +inf
+    sq = r0 * r0 + r1 * r1 + r2 * r2;
+  }
+  double bm = block_max<kVT>(amax, sh);
+  double bs = block_sum<kVT>(sq, sh);
+  if (threadIdx.x == 0) { partial[2 * blockIdx.x] = bm; partial[2 * blockIdx.x + 1] = bs; }
+  if (last_block(counter)) {
+    __shared__ double out[2];
+    double m = 0.0, t = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kVT) {
+      m = fmax(m, __ldcg(partial + 2 * b));
+      t += __ldcg(partial + 2 * b + 1);
+    }
+    m = block_max<kVT>(m, sh);
+    t = block_sum<kVT>(t, sh);
+    if (threadIdx.x == 0) { esc->rmax = m; esc->rnorm2 = t; *counter = 0; }
+  }
+}
+
+void launch_residual(dp_scene* s, const double* q, const double* q_hat, double* r, EvalScalars* esc) {
+  const int nb = grid_for(s->V, kVT);
+  const int has_c = s->colliders.n > 0;
+  k_residual<<<nb, kVT, 0, s->stream>>>(s->V, s->mass, q, q_hat, s->inc_ptr, s->inc, s->fe, s->nb ? s->b_ptr : nullptr,
+                                        s->b_idx, s->b_target, s->b_comp, s->c_count, s->c_off, s->c_force, has_c,
+                                        s->h * s->h, r, s->red.partial, s->red.counter, esc);
+  s->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// assembly gather into SELL-32 + block-Jacobi inverses
+// (fill_pattern core.py:367-376 / assemble_system_jacobian forward.py:113-149
+//  / assemble_adjoint_operator adjoint.py:93-120)
+
+__device__ __forceinline__ void inv3_guarded(const double a[9], double o[9]) {
+  double c00 = a[4] * a[8] - a[5] * a[7];
+  double c01 = a[5] * a[6] - a[3] * a[8];
+  double c02 = a[3] * a[7] - a[4] * a[6];
+  double det = a[0] * c00 + a[1] * c01 + a[2] * c02;
+  double scale = fabs(a[0]) + fabs(a[4]) + fabs(a[8]);
+  if (!(fabs(det) > 1e-14 * scale * scale * scale) || !isfinite(det)) {
+    // fall back to the scalar Jacobi of the reference (linsolve.py:216-227)
+#pragma unroll
+    for (int k = 0; k < 9; ++k) o[k] = 0.0;
+    o[0] = 1.0 / a[0]; o[4] = 1.0 / a[4]; o[8] = 1.0 / a[8];
+    return;
+  }
+  double id = 1.0 / det;
+  o[0] = c00 * id;
+  o[1] = (a[2] * a[7] - a[1] * a[8]) * id;
+  o[2] = (a[1] * a[5] - a[2] * a[4]) * id;
+  o[3] = c01 * id;
+  o[4] = (a[0] * a[8] - a[2] * a[6]) * id;
+  o[5] = (a[2] * a[3] - a[0] * a[5]) * id;
+  o[6] = c02 * id;
+  o[7] = (a[1] * a[6] - a[0] * a[7]) * id;
+  o[8] = (a[0] * a[4] - a[1] * a[3]) * id;
+}
+
+__global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __restrict__ slice_base,
+                                                  const int* __restrict__ slice_width, const int* __restrict__ diag_slot,
+                                                  const int* __restrict__ contrib_ptr, const int* __restrict__ contrib,
+                                                  const double* __restrict__ H, const double* __restrict__ mass,
+                                                  const int* __restrict__ b_ptr, const int* __restrict__ b_idx,
+                                                  const double* __restrict__ b_comp, const int* __restrict__ c_count,
+                                                  const int* __restrict__ c_off, const double* __restrict__ c_blk,
+                                                  int use_extras, double h2, double* __restrict__ val,
+                                                  double* __restrict__ minv) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= S) return;
+  const int row = gw * kSlice + lane;
+  const int base = slice_base[gw];
+  const int K = slice_width[gw];
+  const int dslot = (row < V) ? diag_slot[row] : -1;
+  double* vs = val + (size_t)base * 9;
+  for (int k = 0; k < K; ++k) {
+    const int slot = base + k * kSlice + lane;
+    double b[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) b[c] = 0.0;
+    const int t0 = contrib_ptr[slot], t1 = contrib_ptr[slot + 1];
+    for (int t = t0; t < t1; ++t) {
+      const int cid = contrib[t];
+      if (cid >= 0) {
+        const double* src = H + (size_t)cid * 9;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) b[c] += src[c];
+      } else {
+        const double* src = H + (size_t)(~cid) * 9;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) b[i * 3 + j] += src[j * 3 + i];
+      }
+    }
+    if (slot == dslot) {
+      const double m = mass[row];
+      b[0] += m; b[4] += m; b[8] += m;
+      if (use_extras) {
+        if (b_ptr) {
+          for (int t = b_ptr[row]; t < b_ptr[row + 1]; ++t) {
+            const double kb = h2 / b_comp[b_idx[t]];
+            b[0] += kb; b[4] += kb; b[8] += kb;
+          }
+        }
+        if (c_count) {
+          const int c0 = c_off[row], cn = c_count[row];
+          for (int c = c0; c < c0 + cn; ++c)
+#pragma unroll
+            for (int u = 0; u < 9; ++u) b[u] += c_blk[(size_t)c * 9 + u];
+        }
+      }
+      double o[9];
+      inv3_guarded(b, o);
+#pragma unroll
+      for (int u = 0; u < 9; ++u) minv[(size_t)u * V + row] = o[u];
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) vs[(k * 9 + c) * kSlice + lane] = b[c];
+  }
+}
+
+void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat) {
+  (void)transpose_contacts;   // contact blocks are already stored transposed by the contact kernel
+  const int nt = 256;
+  const int nb = grid_for((int64_t)s->S * 32, nt);
+  const int has_c = (s->colliders.n > 0) && !amat;
+  k_assemble<<<nb, nt, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->diag_slot, s->contrib_ptr,
+                                       s->contrib, s->H, s->mass, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_comp,
+                                       has_c ? s->c_count : nullptr, s->c_off, s->c_blk, amat ? 0 : 1,
+                                       s->h * s->h, val, s->minv);
+  s->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// SELL-32 BSR SpMV: one warp per slice of 32 block rows, one lane per row.
+
+template <bool PRECOND>
+__device__ __forceinline__ void spmv_row(int V, int slice, int lane, const int* __restrict__ slice_base,
+                                         const int* __restrict__ slice_width, const int* __restrict__ col,
+                                         const double* __restrict__ val, const double* __restrict__ x, double y[3]) {
+  const int base = slice_base[slice];
+  const int K = slice_width[slice];
+  const double* vs = val + (size_t)base * 9 + lane;
+  const int* cs = col + base + lane;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < K; ++k) {
+    const int j = __ldg(cs + k * kSlice);
+    const double* v = vs + k * 9 * kSlice;
+    const double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
+    a0 += __ldcs(v + 0 * kSlice) * x0 + __ldcs(v + 1 * kSlice) * x1 + __ldcs(v + 2 * kSlice) * x2;
+    a1 += __ldcs(v + 3 * kSlice) * x0 + __ldcs(v + 4 * kSlice) * x1 + __ldcs(v + 5 * kSlice) * x2;
+    a2 += __ldcs(v + 6 * kSlice) * x0 + __ldcs(v + 7 * kSlice) * x1 + __ldcs(v + 8 * kSlice) * x2;
+  }
+  y[0] = a0; y[1] = a1; y[2] = a2;
+}
+
+__global__ void __launch_bounds__(256) k_spmv(int V, int S, const int* __restrict__ slice_base,
+                                              const int* __restrict__ slice_width, const int* __restrict__ col,
+                                              const double* __restrict__ val, const double* __restrict__ x,
+                                              double* __restrict__ y) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= S) return;
+  double a[3];
+  spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, x, a);
+  const int row = gw * kSlice + lane;
+  if (row < V) { y[3 * row] = a[0]; y[3 * row + 1] = a[1]; y[3 * row + 2] = a[2]; }
+}
+
+void launch_spmv(dp_scene* s, const double* val, const double* x, double* y) {
+  const int nb = grid_for((int64_t)s->S * 32, 256);
+  if (s->timing) cudaEventRecord(s->ev0, s->stream);
+  k_spmv<<<nb, 256, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->col, val, x, y);
+  s->launches++;
+  if (s->timing) {
+    cudaEventRecord(s->ev1, s->stream);
+    cudaEventSynchronize(s->ev1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->ev0, s->ev1);
+    s->times.spmv_ms += ms;
+    s->times.spmv_calls++;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Chronopoulos-Gear PCG (one grid reduction phase per iteration) with
+// 3x3 block-Jacobi preconditioning.  Two kernels per iteration:
+//   KA: p = u + b p; s = w + b s; x += a p; r -= a s; u = Minv r; (r,u), (r,r)
+//   KB: w = A u; (w,u); last block updates alpha/beta and the done flag.
+
+__device__ __forceinline__ void minv_apply(const double* __restrict__ minv, int V, int i, const double r[3], double u[3]) {
+  const double m0 = minv[0 * (size_t)V + i], m1 = minv[1 * (size_t)V + i], m2 = minv[2 * (size_t)V + i];
+  const double m3 = minv[3 * (size_t)V + i], m4 = minv[4 * (size_t)V + i], m5 = minv[5 * (size_t)V + i];
+  const double m6 = minv[6 * (size_t)V + i], m7 = minv[7 * (size_t)V + i], m8 = minv[8 * (size_t)V + i];
+  u[0] = m0 * r[0] + m1 * r[1] + m2 * r[2];
+  u[1] = m3 * r[0] + m4 * r[1] + m5 * r[2];
+  u[2] = m6 * r[0] + m7 * r[1] + m8 * r[2];
+}
+
+__device__ __forceinline__ int ldflag(const int* p) { return *(volatile const int*)p; }
+
+// init: x = 0, p = s = 0, r = b, u = Minv r; gamma = (r,u), rho = (r,r)
+__global__ void __launch_bounds__(kVT) k_cg_init(int V, const double* __restrict__ b, const double* __restrict__ minv,
+                                                 double* x, double* r, double* u, double* p, double* s, double rtol,
+                                                 double* partial, unsigned int* counter, KrylovScalars* ks) {
+  __shared__ double sh[32];
+  __shared__ double out[2];
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  double ru = 0.0, rr = 0.0;
+  if (i < V) {
+    double rv[3] = {b[3 * i], b[3 * i + 1], b[3 * i + 2]};
+    double uv[3];
+    minv_apply(minv, V, i, rv, uv);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      x[3 * i + c] = 0.0; p[3 * i + c] = 0.0; s[3 * i + c] = 0.0;
+      r[3 * i + c] = rv[c]; u[3 * i + c] = uv[c];
+      ru += rv[c] * uv[c]; rr += rv[c] * rv[c];
+    }
+  }
+  double t0 = block_sum<kVT>(ru, sh);
+  double t1 = block_sum<kVT>(rr, sh);
+  if (threadIdx.x == 0) { partial[2 * blockIdx.x] = t0; partial[2 * blockIdx.x + 1] = t1; }
+  if (last_block(counter)) {
+    fold_partials<kVT, 2>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) {
+      ks->gamma = out[0];
+      ks->rho = out[1];
+      ks->bnorm2 = out[1];
+      ks->tol2 = rtol * rtol * out[1];
+      ks->alpha = 0.0; ks->beta = 0.0; ks->delta = 0.0;
+      ks->iters = 0;
+      ks->done = (out[1] == 0.0) ? 1 : 0;
+      ks->pad[0] = out[0];   // gamma_new
+      *counter = 0;
+    }
+  }
+}
+
+// KB: w = A u; delta = (w, u); last block computes alpha, beta
+__global__ void __launch_bounds__(256) k_cg_spmv(int V, int S, const int* __restrict__ slice_base,
+                                                 const int* __restrict__ slice_width, const int* __restrict__ col,
+                                                 const double* __restrict__ val, const double* __restrict__ u,
+                                                 double* __restrict__ w, double* partial, unsigned int* counter,
+                                                 KrylovScalars* ks, int first) {
+  __shared__ double sh[32];
+  __shared__ double out[1];
+  if (ldflag(&ks->done)) return;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  double wu = 0.0;
+  if (gw < S) {
+    double a[3];
+    spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, u, a);
+    const int row = gw * kSlice + lane;
+    if (row < V) {
+      w[3 * row] = a[0]; w[3 * row + 1] = a[1]; w[3 * row + 2] = a[2];
+      wu = a[0] * u[3 * row] + a[1] * u[3 * row + 1] + a[2] * u[3 * row + 2];
+    }
+  }
+  double t = block_sum<256>(wu, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    fold_partials<256, 1>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) {
+      const double delta = out[0];
+      const double gnew = ks->pad[0];
+      if (first) {
+        ks->beta = 0.0;
+        if (!(delta > 0.0)) ks->done = 2;
+        else ks->alpha = gnew / delta;
+      } else {
+        const double beta = gnew / ks->gamma;
+        const double den = delta - beta * gnew / ks->alpha;
+        ks->beta = beta;
+        if (!(den > 0.0)) ks->done = 2;     // p^T A p <= 0: breakdown (linsolve.py:89-91)
+        else ks->alpha = gnew / den;
+      }
+      ks->gamma = gnew;
+      ks->delta = delta;
+      *counter = 0;
+    }
+  }
+}
+
+// KA: vector updates + preconditioner + (r,u), (r,r)
+__global__ void __launch_bounds__(kVT) k_cg_update(int V, const double* __restrict__ minv, double* x, double* r,
+                                                   double* u, const double* __restrict__ w, double* p, double* s,
+                                                   double* partial, unsigned int* counter, KrylovScalars* ks) {
+  __shared__ double sh[32];
+  __shared__ double out[2];
+  if (ldflag(&ks->done)) return;
+  const double alpha = ks->alpha, beta = ks->beta;
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  double ru = 0.0, rr = 0.0;
+  if (i < V) {
+    double rv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int k = 3 * i + c;
+      const double pk = u[k] + beta * p[k];
+      const double sk = w[k] + beta * s[k];
+      p[k] = pk; s[k] = sk;
+      x[k] += alpha * pk;
+      rv[c] = r[k] - alpha * sk;
+      r[k] = rv[c];
+    }
+    double uv[3];
+    minv_apply(minv, V, i, rv, uv);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      u[3 * i + c] = uv[c];
+      ru += rv[c] * uv[c];
+      rr += rv[c] * rv[c];
+    }
+  }
+  double t0 = block_sum<kVT>(ru, sh);
+  double t1 = block_sum<kVT>(rr, sh);
+  if (threadIdx.x == 0) { partial[2 * blockIdx.x] = t0; partial[2 * blockIdx.x + 1] = t1; }
+  if (last_block(counter)) {
+    fold_partials<kVT, 2>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) {
+      ks->pad[0] = out[0];
+      ks->rho = out[1];
+      ks->iters += 1;
+      if (out[1] <= ks->tol2) ks->done = 1;
+      *counter = 0;
+    }
+  }
+}
+
+// r = b - A x ; returns partial |r|^2 -> scalar (used for true residuals)
+__global__ void __launch_bounds__(256) k_resid_true(int V, int S, const int* __restrict__ slice_base,
+                                                    const int* __restrict__ slice_width, const int* __restrict__ col,
+                                                    const double* __restrict__ val, const double* __restrict__ x,
+                                                    const double* __restrict__ b, double* __restrict__ r,
+                                                    double* partial, unsigned int* counter, double* result) {
+  __shared__ double sh[32];
+  __shared__ double out[1];
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  if (gw < S) {
+    double a[3];
+    spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, x, a);
+    const int row = gw * kSlice + lane;
+    if (row < V) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double v = b[3 * row + c] - a[c];
+        r[3 * row + c] = v;
+        acc += v * v;
+      }
+    }
+  }
+  double t = block_sum<256>(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    fold_partials<256, 1>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) { *result = out[0]; *counter = 0; }
+  }
+}
+
+__global__ void __launch_bounds__(kVT) k_norm2(int n, const double* __restrict__ x, double* partial,
+                                               unsigned int* counter, double* result) {
+  __shared__ double sh[32];
+  __shared__ double out[1];
+  double acc = 0.0;
+  for (int i = blockIdx.x * kVT + threadIdx.x; i < n; i += gridDim.x * kVT) acc += x[i] * x[i];
+  double t = block_sum<kVT>(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    fold_partials<kVT, 1>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) { *result = out[0]; *counter = 0; }
+  }
+}
+
+__global__ void k_axpy_to(int n, double* out, const double* a, double t, const double* b) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] + t * b[i];
+}
+
+void launch_axpy_to(dp_scene* s, double* out, const double* a, double t, const double* b) {
+  const int n = 3 * s->V;
+  k_axpy_to<<<grid_for(n, 256), 256, 0, s->stream>>>(n, out, a, t, b);
+  s->launches++;
+}
+
+double device_norm2(dp_scene* s, const double* x) {
+  const int n = 3 * s->V;
+  int nb = grid_for(n, kVT);
+  if (nb > 1024) nb = 1024;
+  double* res = s->red.partial + s->red.cap_blocks * s->red.width - 1;
+  k_norm2<<<nb, kVT, 0, s->stream>>>(n, x, s->red.partial, s->red.counter, res);
+  s->launches++;
+  double h = 0.0;
+  cudaMemcpyAsync(&s->h_ksc->pad[1], res, sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+  cudaStreamSynchronize(s->stream);
+  h = s->h_ksc->pad[1];
+  return h;
+}
+
+// true relative residual |b - A x| / |b| (synchronous)
+static double true_relres(dp_scene* s, const double* val, const double* b, const double* x, double* r, double bnorm) {
+  const int nb = grid_for((int64_t)s->S * 32, 256);
+  double* res = s->red.partial + s->red.cap_blocks * s->red.width - 1;
+  k_resid_true<<<nb, 256, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->col, val, x, b, r,
+                                          s->red.partial, s->red.counter, res);
+  s->launches++;
+  cudaMemcpyAsync(&s->h_ksc->pad[1], res, sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+  cudaStreamSynchronize(s->stream);
+  return sqrt(s->h_ksc->pad[1]) / bnorm;
+}
+
+static void read_ksc(dp_scene* s) {
+  cudaMemcpyAsync(s->h_ksc, s->ksc, sizeof(KrylovScalars), cudaMemcpyDeviceToHost, s->stream);
+  cudaStreamSynchronize(s->stream);
+}
+
+// Solve A x = b to rtol (true relative residual).  Returns 0 ok, 1 not
+// converged, 2 breakdown (A not SPD).  x is overwritten.
+int cg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int* iters,
+             double* relres, int* breakdown) {
+  const int V = s->V;
+  const int nbv = grid_for(V, kVT);
+  const int nbs = grid_for((int64_t)s->S * 32, 256);
+  *iters = 0;
+  *breakdown = 0;
+  double bnorm = sqrt(device_norm2(s, b));
+  if (bnorm == 0.0) {
+    cudaMemsetAsync(x, 0, sizeof(double) * 3 * V, s->stream);
+    *relres = 0.0;
+    return 0;
+  }
+  // restarts on the true residual: x = x0 + d, A d = b - A x0
+  double* bb = s->tmp;   // current rhs of the correction solve
+  double* xc = s->kx;
+  cudaMemsetAsync(x, 0, sizeof(double) * 3 * V, s->stream);
+  cudaMemcpyAsync(bb, b, sizeof(double) * 3 * V, cudaMemcpyDeviceToDevice, s->stream);
+  double rel = 1.0;
+  for (int restart = 0; restart < 4; ++restart) {
+    double inner_rtol = rtol / rel * 0.5;
+    if (inner_rtol > 0.5) inner_rtol = 0.5;
+    if (inner_rtol < 1e-15) inner_rtol = 1e-15;
+    k_cg_init<<<nbv, kVT, 0, s->stream>>>(V, bb, s->minv, xc, s->kr, s->ku, s->kp, s->ks, inner_rtol, s->red.partial,
+                                          s->red.counter, s->ksc);
+    k_cg_spmv<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, s->ku, s->kw,
+                                          s->red.partial, s->red.counter, s->ksc, 1);
+    s->launches += 2;
+    int done = 0, launched = 0;
+    int chunk = 8;
+    while (!done && *iters + launched < max_iter) {
+      int n = chunk;
+      if (*iters + launched + n > max_iter) n = max_iter - *iters - launched;
+      for (int k = 0; k < n; ++k) {
+        k_cg_update<<<nbv, kVT, 0, s->stream>>>(V, s->minv, xc, s->kr, s->ku, s->kw, s->kp, s->ks, s->red.partial,
+                                                s->red.counter, s->ksc);
+        k_cg_spmv<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, s->ku, s->kw,
+                                              s->red.partial, s->red.counter, s->ksc, 0);
+      }
+      s->launches += 2 * n;
+      launched += n;
+      read_ksc(s);
+      done = s->h_ksc->done;
+      if (chunk < 64) chunk *= 2;
+    }
+    *iters += s->h_ksc->iters;
+    if (s->h_ksc->done == 2) {
+      *breakdown = 1;
+      // keep the progress so far
+      launch_axpy_to(s, x, x, 1.0, xc);
+      *relres = true_relres(s, val, b, x, s->tmp, bnorm);
+      return 2;
+    }
+    launch_axpy_to(s, x, x, 1.0, xc);
+    rel = true_relres(s, val, b, x, bb, bnorm);   // bb <- b - A x
+    if (rel <= rtol || *iters >= max_iter) break;
+  }
+  *relres = rel;
+  return rel <= rtol ? 0 : 1;
+}
+
+// ---------------------------------------------------------------------------
+// GMRES(m), left block-Jacobi preconditioning, classical Gram-Schmidt with a
+// conditional second pass (re-orthogonalise when |w| drops by more than 2x),
+// Givens rotations on device (gmres, linsolve.py:108-197).  The host drives
+// the column index j; kernels exit early once `done` is set.
+
+constexpr int kGT = 256;
+constexpr int kGM1 = kMaxRestart + 1;
+
+// w = Minv (A v)
+__global__ void __launch_bounds__(256) k_gm_apply(int V, int S, const int* __restrict__ slice_base,
+                                                  const int* __restrict__ slice_width, const int* __restrict__ col,
+                                                  const double* __restrict__ val, const double* __restrict__ minv,
+                                                  const double* __restrict__ v, double* __restrict__ w,
+                                                  const GmresScalars* gs) {
+  if (ldflag(&gs->done)) return;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= S) return;
+  double a[3];
+  spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, v, a);
+  const int row = gw * kSlice + lane;
+  if (row < V) {
+    double u[3];
+    minv_apply(minv, V, row, a, u);
+    w[3 * row] = u[0]; w[3 * row + 1] = u[1]; w[3 * row + 2] = u[2];
+  }
+}
+
+// coef_i = (w, v_i) for i <= j; pass 0 also |w|^2 -> wn2_before.
+__global__ void __launch_bounds__(kGT) k_gm_dots(int n, int j, int pass, const double* __restrict__ Vb, size_t ld,
+                                                 const double* __restrict__ w, double* partial, unsigned int* counter,
+                                                 GmresScalars* gs) {
+  __shared__ double sh[32];
+  if (ldflag(&gs->done)) return;
+  if (pass == 1 && !ldflag(&gs->reorth)) return;
+  const int nd = (pass == 0) ? j + 2 : j + 1;
+  for (int i = 0; i < nd; ++i) {
+    const double* vi = (i <= j) ? Vb + (size_t)i * ld : w;
+    double acc = 0.0;
+    for (int k = blockIdx.x * kGT + threadIdx.x; k < n; k += gridDim.x * kGT) acc += w[k] * vi[k];
+    double t = block_sum<kGT>(acc, sh);
+    if (threadIdx.x == 0) partial[(size_t)blockIdx.x * (kGM1 + 1) + i] = t;
+  }
+  if (last_block(counter)) {
+    for (int i = 0; i < nd; ++i) {
+      double acc = 0.0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += kGT) acc += __ldcg(partial + (size_t)b * (kGM1 + 1) + i);
+      double t = block_sum<kGT>(acc, sh);
+      if (threadIdx.x == 0) {
+        if (i <= j) {
+          gs->coef[i] = t;
+          double* Hc = gs->H + (size_t)j * kGM1;
+          Hc[i] = (pass == 0) ? t : Hc[i] + t;
+        } else {
+          gs->wn2_before = t;
+        }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+__device__ void gm_finish_column(GmresScalars* gs, int j, double wn2) {
+  double* Hc = gs->H + (size_t)j * kGM1;
+  const double hn = sqrt(wn2);
+  gs->hn = hn;
+  Hc[j + 1] = hn;
+  for (int i = 0; i < j; ++i) {
+    const double t = gs->cs[i] * Hc[i] + gs->sn[i] * Hc[i + 1];
+    Hc[i + 1] = -gs->sn[i] * Hc[i] + gs->cs[i] * Hc[i + 1];
+    Hc[i] = t;
+  }
+  const double den = hypot(Hc[j], Hc[j + 1]);
+  gs->cs[j] = den != 0.0 ? Hc[j] / den : 1.0;
+  gs->sn[j] = den != 0.0 ? Hc[j + 1] / den : 0.0;
+  Hc[j] = den;
+  Hc[j + 1] = 0.0;
+  gs->g[j + 1] = -gs->sn[j] * gs->g[j];
+  gs->g[j] = gs->cs[j] * gs->g[j];
+  gs->used = j + 1;
+  gs->est = fabs(gs->g[j + 1]) / gs->nmb;
+  if (fabs(gs->g[j + 1]) <= gs->thr) gs->done = 1;
+  else if (!(hn > 1e-300)) gs->done = 2;
+}
+
+// w -= sum_i coef_i v_i ; |w|^2 ; the last block finishes column j unless a
+// second orthogonalisation pass is needed.
+__global__ void __launch_bounds__(kGT) k_gm_update(int n, int j, int pass, const double* __restrict__ Vb, size_t ld,
+                                                   double* w, double* partial, unsigned int* counter,
+                                                   GmresScalars* gs) {
+  __shared__ double sh[32];
+  __shared__ double coef[kGM1];
+  __shared__ double out[1];
+  if (ldflag(&gs->done)) return;
+  if (pass == 1 && !ldflag(&gs->reorth)) return;
+  for (int i = threadIdx.x; i <= j; i += kGT) coef[i] = gs->coef[i];
+  __syncthreads();
+  double acc = 0.0;
+  for (int k = blockIdx.x * kGT + threadIdx.x; k < n; k += gridDim.x * kGT) {
+    double v = w[k];
+    for (int i = 0; i <= j; ++i) v -= coef[i] * Vb[(size_t)i * ld + k];
+    w[k] = v;
+    acc += v * v;
+  }
+  double t = block_sum<kGT>(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    fold_partials<kGT, 1>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) {
+      *counter = 0;
+      const double wn2 = out[0];
+      if (pass == 0 && wn2 < 0.25 * gs->wn2_before) {
+        gs->reorth = 1;
+      } else {
+        gs->reorth = 0;
+        gm_finish_column(gs, j, wn2);
+      }
+    }
+  }
+}
+
+// v_{j+1} = w / hn
+__global__ void k_gm_normalize(int n, const double* __restrict__ w, double* __restrict__ vnext, const GmresScalars* gs) {
+  if (ldflag(&gs->done)) return;
+  const double inv = 1.0 / gs->hn;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) vnext[k] = w[k] * inv;
+}
+
+// cycle start: v0 = Minv r (unnormalised) and |v0|^2 -> beta, g, thresholds
+__global__ void __launch_bounds__(kVT) k_gm_start(int V, const double* __restrict__ minv, const double* __restrict__ r,
+                                                  double* __restrict__ v0, double* partial, unsigned int* counter,
+                                                  GmresScalars* gs, double tol, int set_nmb) {
+  __shared__ double sh[32];
+  __shared__ double out[1];
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  double acc = 0.0;
+  if (i < V) {
+    double rv[3] = {r[3 * i], r[3 * i + 1], r[3 * i + 2]}, u[3];
+    minv_apply(minv, V, i, rv, u);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { v0[3 * i + c] = u[c]; acc += u[c] * u[c]; }
+  }
+  double t = block_sum<kVT>(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    fold_partials<kVT, 1>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) {
+      *counter = 0;
+      const double beta = sqrt(out[0]);
+      if (set_nmb) {
+        gs->nmb = beta != 0.0 ? beta : 1.0;   // |M^-1 b| (linsolve.py:180)
+      } else {
+        gs->beta = beta;
+        for (int k = 0; k <= kMaxRestart; ++k) gs->g[k] = 0.0;
+        gs->g[0] = beta;
+        gs->hn = beta;
+        gs->thr = 0.1 * tol * gs->nmb;
+        gs->done = (beta == 0.0) ? 2 : 0;
+        gs->reorth = 0;
+        gs->used = 0;
+        gs->est = beta / gs->nmb;
+      }
+    }
+  }
+}
+
+// x += sum_i y_i v_i
+__global__ void k_gm_combine(int n, int used, const double* __restrict__ y, const double* __restrict__ Vb, size_t ld,
+                             double* __restrict__ x) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < used; ++i) acc += y[i] * Vb[(size_t)i * ld + k];
+    x[k] += acc;
+  }
+}
+
+static int gm_grid(int n) {
+  int nb = grid_for(n, kGT);
+  return nb > 4 * 148 ? 4 * 148 : nb;
+}
+
+// Restarted GMRES on A x = b (true relative residual <= rtol).  x is
+// overwritten (zero initial guess).  Returns 0 converged, 1 not converged.
+int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int restart,
+                int* iters, double* relres) {
+  const int V = s->V, n = 3 * V;
+  if (restart > kMaxRestart) restart = kMaxRestart;
+  if (restart > n) restart = n;
+  if (restart < 1) restart = 1;
+  const size_t ld = (size_t)n;
+  const int nbv = grid_for(V, kVT);
+  const int nbs = grid_for((int64_t)s->S * 32, 256);
+  const int nbg = gm_grid(n);
+  double* Vb = s->gm_V;
+  double* w = s->kw;
+  double* r = s->kr;
+  double* y_dev = s->ks;   // scratch (>= restart doubles)
+  *iters = 0;
+  cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+  const double bnorm = sqrt(device_norm2(s, b));
+  if (bnorm == 0.0) { *relres = 0.0; return 0; }
+  // |M^-1 b|
+  k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, b, w, s->red.partial, s->red.counter, s->gsc, rtol, 1);
+  s->launches++;
+  int total = 0;
+  double rel = 1.0;
+  while (total < max_iter) {
+    rel = true_relres(s, val, b, x, r, bnorm);
+    if (rel <= rtol) break;
+    const double cycle_start = rel;
+    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, r, Vb, s->red.partial, s->red.counter, s->gsc, rtol, 0);
+    k_gm_normalize<<<nbg, kGT, 0, s->stream>>>(n, Vb, Vb, s->gsc);
+    s->launches += 2;
+    int j = 0;
+    bool stop = false;
+    while (j < restart && total < max_iter && !stop) {
+      int chunk = 8;
+      if (j + chunk > restart) chunk = restart - j;
+      if (total + chunk > max_iter) chunk = max_iter - total;
+      for (int c = 0; c < chunk; ++c, ++j) {
+        k_gm_apply<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, s->minv,
+                                               Vb + (size_t)j * ld, w, s->gsc);
+        k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, 0, Vb, ld, w, s->red.partial, s->red.counter, s->gsc);
+        k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, j, 0, Vb, ld, w, s->red.partial, s->red.counter, s->gsc);
+        k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, 1, Vb, ld, w, s->red.partial, s->red.counter, s->gsc);
+        k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, j, 1, Vb, ld, w, s->red.partial, s->red.counter, s->gsc);
+        if (j + 1 < restart)
+          k_gm_normalize<<<nbg, kGT, 0, s->stream>>>(n, w, Vb + (size_t)(j + 1) * ld, s->gsc);
+        s->launches += 6;
+      }
+      cudaMemcpyAsync(s->h_gsc, s->gsc, sizeof(GmresScalars), cudaMemcpyDeviceToHost, s->stream);
+      cudaStreamSynchronize(s->stream);
+      if (s->h_gsc->done) stop = true;
+      total = *iters + s->h_gsc->used;
+    }
+    const GmresScalars* hg = s->h_gsc;
+    const int used = hg->used;
+    *iters += used;
+    total = *iters;
+    if (used > 0) {
+      // back substitution H[:used,:used] y = g[:used]
+      double y[kMaxRestart];
+      for (int i = used - 1; i >= 0; --i) {
+        double acc = hg->g[i];
+        for (int k = i + 1; k < used; ++k) acc -= hg->H[(size_t)k * kGM1 + i] * y[k];
+        y[i] = acc / hg->H[(size_t)i * kGM1 + i];
+      }
+      cudaMemcpyAsync(y_dev, y, sizeof(double) * used, cudaMemcpyHostToDevice, s->stream);
+      k_gm_combine<<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, Vb, ld, x);
+      s->launches++;
+    }
+    rel = true_relres(s, val, b, x, r, bnorm);
+    if (rel <= rtol) break;
+    if (rel >= cycle_start * (1.0 - 1e-12)) break;   // stagnation (linsolve.py:187-188)
+    if (used == 0) break;
+  }
+  *relres = rel;
+  return rel <= rtol ? 0 : 1;
+}
+
+// ---------------------------------------------------------------------------
+// step prologue (core.predict core.py:392-397, _residual_scale
+// forward.py:169-171) and epilogue (v = (q - q_bar)/h, forward.py:241)
+
+__global__ void __launch_bounds__(kVT) k_predict(int V, const double* __restrict__ q_bar, const double* __restrict__ v_bar,
+                                                 const double* __restrict__ mass, const double* __restrict__ fext,
+                                                 int has_fext, double h, double g0, double g1, double g2,
+                                                 double* __restrict__ q_hat, double* __restrict__ q,
+                                                 double* partial, unsigned int* counter, EvalScalars* esc) {
+  __shared__ double sh[32];
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  double amax = 0.0;
+  if (i < V) {
+    const double m = mass[i];
+    const double hh_minv = __dmul_rn(__dmul_rn(h, h), 1.0 / m);
+    const double g[3] = {g0, g1, g2};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int k = 3 * i + c;
+      const double f = __dadd_rn(has_fext ? fext[k] : 0.0, __dmul_rn(m, g[c]));
+      const double qh = __dadd_rn(__dadd_rn(q_bar[k], __dmul_rn(h, v_bar[k])), __dmul_rn(hh_minv, f));
+      q_hat[k] = qh;
+      q[k] = qh;
+      amax = fmax(amax, fabs(m * qh));
+    }
+  }
+  double bm = block_max<kVT>(amax, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = bm;
+  if (last_block(counter)) {
+    __shared__ double out[1];
+    fold_partials<kVT, 1>(partial, gridDim.x, out, sh, true);
+    if (threadIdx.x == 0) { esc->scale_max = out[0]; *counter = 0; }
+  }
+}
+
+void launch_predict(dp_scene* s) {
+  k_predict<<<grid_for(s->V, kVT), kVT, 0, s->stream>>>(s->V, s->q_bar, s->v_bar, s->mass, s->fext, s->has_fext,
+                                                         s->h, s->grav[0], s->grav[1], s->grav[2], s->q_hat, s->q,
+                                                         s->red.partial, s->red.counter, s->esc);
+  s->launches++;
+}
+
+__global__ void k_velocity(int n, const double* q, const double* q_bar, double h, double* v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = (q[i] - q_bar[i]) / h;
+}
+
+void launch_velocity(dp_scene* s, const double* q, const double* q_bar, double* v) {
+  const int n = 3 * s->V;
+  k_velocity<<<grid_for(n, 256), 256, 0, s->stream>>>(n, q, q_bar, s->h, v);
+  s->launches++;
+}
+
+__global__ void k_reset_eval(EvalScalars* esc) {
+  esc->rmax = 0.0;
+  esc->status = 0;
+  esc->penetrating = 0;
+  esc->asym = 0;
+}
+
+void launch_reset_eval(dp_scene* s, EvalScalars* esc) {
+  k_reset_eval<<<1, 1, 0, s->stream>>>(esc);
+  s->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// backprop_step (adjoint.py:154-219)
+
+// per vertex: dqbar = m z - dL_dv / h + contact q_bar term; dvbar = h m z;
+// dfext = h^2 z (adjoint.py:166-176, _contact_qbar_term :142-151)
+__global__ void __launch_bounds__(kVT) k_bp_vertex(int V, const double* __restrict__ mass, const double* __restrict__ z,
+                                                   const double* __restrict__ dL_dv, double h,
+                                                   const int* __restrict__ c_count, const int* __restrict__ c_off,
+                                                   const double* __restrict__ c_frame, const double* __restrict__ c_kc,
+                                                   int has_contacts, double* __restrict__ dqbar,
+                                                   double* __restrict__ dvbar, double* __restrict__ dfext) {
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  if (i >= V) return;
+  const double m = mass[i], h2 = h * h;
+  const double zi[3] = {z[3 * i], z[3 * i + 1], z[3 * i + 2]};
+  double out[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) out[c] = m * zi[c] - dL_dv[3 * i + c] / h;
+  if (has_contacts) {
+    const int c0 = c_off[i], cn = c_count[i];
+    for (int c = c0; c < c0 + cn; ++c) {
+      const double* fr = c_frame + (size_t)c * 9;
+      const double* K = c_kc + (size_t)c * 9;
+      double zc[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) zc[a] = fr[a * 3] * zi[0] + fr[a * 3 + 1] * zi[1] + fr[a * 3 + 2] * zi[2];
+      // t = P_f^T Kc^T zc, P_f = diag(0, 1, 1)
+      double t1 = K[0 * 3 + 1] * zc[0] + K[1 * 3 + 1] * zc[1] + K[2 * 3 + 1] * zc[2];
+      double t2 = K[0 * 3 + 2] * zc[0] + K[1 * 3 + 2] * zc[1] + K[2 * 3 + 2] * zc[2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) out[a] += h2 * (fr[1 * 3 + a] * t1 + fr[2 * 3 + a] * t2);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    dqbar[3 * i + c] = out[c];
+    dvbar[3 * i + c] = h * (m * zi[c]);
+    dfext[3 * i + c] = h2 * zi[c];
+  }
+}
+
+// per contact: dL/dmu_friction += -h^2 k_mu . (frame z)  (adjoint.py:187-191)
+__global__ void __launch_bounds__(kVT) k_bp_contacts(int C, const int* __restrict__ vtx, const double* __restrict__ frame,
+                                                     const double* __restrict__ kmu, const double* __restrict__ z,
+                                                     double h2, double* partial, unsigned int* counter, double* acc) {
+  __shared__ double sh[32];
+  __shared__ double out[1];
+  const int c = blockIdx.x * kVT + threadIdx.x;
+  double v = 0.0;
+  if (c < C) {
+    const int i = vtx[c];
+    const double* fr = frame + (size_t)c * 9;
+    double zc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) zc[a] = fr[a * 3] * z[3 * i] + fr[a * 3 + 1] * z[3 * i + 1] + fr[a * 3 + 2] * z[3 * i + 2];
+    v = -h2 * (kmu[3 * c] * zc[0] + kmu[3 * c + 1] * zc[1] + kmu[3 * c + 2] * zc[2]);
+  }
+  double t = block_sum<kVT>(v, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    fold_partials<kVT, 1>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) { acc[0] += out[0]; *counter = 0; }
+  }
+}
+
+// per binding (adjoint.py:178-184)
+__global__ void k_bp_bindings(int nb, const int* __restrict__ vtx, const double* __restrict__ target,
+                              const double* __restrict__ comp, const double* __restrict__ q,
+                              const double* __restrict__ z, double h2, double* dEb, double* ddb) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const int i = vtx[b];
+  const double Eb = comp[b];
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double lam_b = -(q[3 * i + c] - target[3 * b + c]) / Eb;
+    const double zb = z[3 * i + c];
+    acc += zb * (-h2 * lam_b / Eb);
+    ddb[3 * b + c] += h2 / Eb * zb;
+  }
+  dEb[b] += acc;
+}
+
+// per element (adjoint.py:193-210): base = (G z).(p - G q_new); ARAP dL/dw,
+// dL/dstiffness; NH dmu, dlambda partials.
+template <int NV>
+__global__ void __launch_bounds__(128) k_bp_elements(const int4* __restrict__ ev, const double* __restrict__ Bm,
+                                                     const double* __restrict__ w, const double* __restrict__ vol,
+                                                     const int* __restrict__ model, int E, const double* __restrict__ q,
+                                                     const double* __restrict__ z, const double* __restrict__ Pst,
+                                                     double h2, double* __restrict__ dw, double* partial,
+                                                     unsigned int* counter, double* acc) {
+  constexpr int D = NV - 1;
+  __shared__ double sh[32];
+  __shared__ double out[3];
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  double s_stiff = 0.0, s_mu = 0.0, s_lam = 0.0;
+  if (e < E) {
+    const int4 vv = ev[e];
+    const int vid[4] = {vv.x, vv.y, vv.z, vv.w};
+    double beta[NV][D];
+#pragma unroll
+    for (int k = 1; k < NV; ++k)
+#pragma unroll
+      for (int c = 0; c < D; ++c) beta[k][c] = Bm[(size_t)((k - 1) * D + c) * E + e];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 1; k < NV; ++k) s += beta[k][c];
+      beta[0][c] = -s;
+    }
+    const double* P = Pst + (size_t)e * 27;
+    double base = 0.0, gzmu = 0.0, gzlam = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        double gz = 0.0, gq = 0.0;
+#pragma unroll
+        for (int a = 0; a < NV; ++a) {
+          gz += z[3 * (size_t)vid[a] + i] * beta[a][c];
+          gq += q[3 * (size_t)vid[a] + i] * beta[a][c];
+        }
+        base += gz * (P[i * 3 + c] - gq);
+        gzmu += gz * P[9 + i * 3 + c];
+        gzlam += gz * P[18 + i * 3 + c];
+      }
+    if (model[e] == DP_MODEL_ARAP) {
+      dw[e] += h2 * base;
+      s_stiff = h2 * base * vol[e];
+    } else {
+      s_mu = h2 * (2.0 * vol[e] * base + w[e] * gzmu);
+      s_lam = h2 * w[e] * gzlam;
+    }
+  }
+  double t0 = block_sum<128>(s_stiff, sh);
+  double t1 = block_sum<128>(s_mu, sh);
+  double t2 = block_sum<128>(s_lam, sh);
+  if (threadIdx.x == 0) {
+    partial[3 * blockIdx.x] = t0;
+    partial[3 * blockIdx.x + 1] = t1;
+    partial[3 * blockIdx.x + 2] = t2;
+  }
+  if (last_block(counter)) {
+    fold_partials<128, 3>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) {
+      acc[1] += out[0];
+      acc[2] += out[1];
+      acc[3] += out[2];
+      *counter = 0;
+    }
+  }
+}
+
+void launch_backprop(dp_scene* s, const dp_cache* c, const double* z, const double* dL_dv, double* dqbar, double* dvbar,
+                     double* dfext) {
+  const int has_c = c->n_contacts > 0;
+  k_bp_vertex<<<grid_for(s->V, kVT), kVT, 0, s->stream>>>(s->V, s->mass, z, dL_dv, s->h, s->c_count, s->c_off,
+                                                          s->c_frame, s->c_kc, has_c, dqbar, dvbar, dfext);
+  s->launches++;
+  const double h2 = s->h * s->h;
+  if (has_c) {
+    k_bp_contacts<<<grid_for(c->n_contacts, kVT), kVT, 0, s->stream>>>(
+        c->n_contacts, s->c_vertex, s->c_frame, s->c_kmu, z, h2, s->red.partial, s->red.counter, s->g_scal);
+    s->launches++;
+  }
+  if (s->nb) {
+    k_bp_bindings<<<grid_for(s->nb, 128), 128, 0, s->stream>>>(s->nb, s->b_vertex, s->b_target, s->b_comp, c->q_new,
+                                                               z, h2, s->g_dEb, s->g_ddb);
+    s->launches++;
+  }
+  if (s->E) {
+    const int nb = grid_for(s->E, 128);
+    if (s->NV == 4)
+      k_bp_elements<4><<<nb, 128, 0, s->stream>>>(s->ev, s->B, s->w, s->vol, s->model, s->E, c->q_new, z, s->Pst, h2,
+                                                  s->g_dw, s->red.partial, s->red.counter, s->g_scal);
+    else
+      k_bp_elements<3><<<nb, 128, 0, s->stream>>>(s->ev, s->B, s->w, s->vol, s->model, s->E, c->q_new, z, s->Pst, h2,
+                                                  s->g_dw, s->red.partial, s->red.counter, s->g_scal);
+    s->launches++;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// batched unit kernels (dp_project_batch): project_element + proj_jacobian +
+// dP_dlame for a list of F (elasticity.py:137-324)
+
+template <int D>
+__global__ void k_project_batch(int n, const double* __restrict__ F, const int* __restrict__ model,
+                                const double* __restrict__ mu, const double* __restrict__ lam, double tau_rel,
+                                double* sigma, double* theta, double* Wout, double* Pout, double* J, double* dPmu,
+                                double* dPlam, int* status) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double Fm[3][D];
+  // input F is (3, D) row-major per item
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int c = 0; c < D; ++c) Fm[i][c] = F[(size_t)e * 3 * D + i * D + c];
+  double U[3][D], sig[D], V[D][D], th[D], W[D][D];
+  int st = project_full<D>(Fm, model[e], mu[e], lam[e], tau_rel, U, sig, V, th, W);
+  status[e] = st;
+  if (st) return;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    sigma[(size_t)e * D + k] = sig[k];
+    theta[(size_t)e * D + k] = th[k];
+#pragma unroll
+    for (int l = 0; l < D; ++l) Wout[(size_t)e * D * D + k * D + l] = W[k][l];
+  }
+  double dmu[D], dlm[D];
+  if (model[e] == DP_MODEL_NEOHOOKEAN) nh_dtheta_dlame<D>(th, sig, mu[e], lam[e], dmu, dlm);
+  else {
+#pragma unroll
+    for (int k = 0; k < D; ++k) dmu[k] = dlm[k] = 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double p = 0.0, pm = 0.0, pl = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        p += U[i][k] * th[k] * V[c][k];
+        pm += U[i][k] * dmu[k] * V[c][k];
+        pl += U[i][k] * dlm[k] * V[c][k];
+      }
+      Pout[(size_t)e * 3 * D + i * D + c] = p;
+      dPmu[(size_t)e * 3 * D + i * D + c] = pm;
+      dPlam[(size_t)e * 3 * D + i * D + c] = pl;
+    }
+  // dP/dF in the column-stacked basis: J[(c,i),(c',j)] = [Gt_a J G_b]_{ij}
+  // with beta_a = e_c, beta_b = e_c'  ->  alpha = row c of V.
+  ElemJac<D> Jm;
+  make_jac<D>(U, sig, th, W, tau_rel, Jm);
+  const int N = 3 * D;
+#pragma unroll
+  for (int c = 0; c < D; ++c)
+#pragma unroll
+    for (int c2 = 0; c2 < D; ++c2) {
+      double aa[D], ab[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) { aa[k] = V[c][k]; ab[k] = V[c2][k]; }
+      double blk[3][3];
+      jac_block<D>(Jm, aa, ab, blk);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) J[(size_t)e * N * N + (c * 3 + i) * N + (c2 * 3 + j)] = blk[i][j];
+    }
+}
+
+void launch_project_batch(int n, int d, const double* F, const int* model, const double* mu, const double* lam,
+                          double tau_rel, double* sigma, double* theta, double* W, double* P, double* J, double* dPmu,
+                          double* dPlam, int* status) {
+  if (d == 3)
+    k_project_batch<3><<<grid_for(n, 64), 64>>>(n, F, model, mu, lam, tau_rel, sigma, theta, W, P, J, dPmu, dPlam,
+                                               status);
+  else
+    k_project_batch<2><<<grid_for(n, 64), 64>>>(n, F, model, mu, lam, tau_rel, sigma, theta, W, P, J, dPmu, dPlam,
+                                               status);
+}
+
+// per-element projection export (dp_cache_get_projections)
+template <int NV>
+__global__ void k_export_proj(const int4* __restrict__ ev, const double* __restrict__ Bm,
+                              const double* __restrict__ mu, const double* __restrict__ lam,
+                              const int* __restrict__ model, int E, const double* __restrict__ q, double* sigma,
+                              double* theta, double* Pout, double* energy) {
+  constexpr int D = NV - 1;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int4 vv = ev[e];
+  const int vid[4] = {vv.x, vv.y, vv.z, vv.w};
+  double beta[NV][D];
+  for (int k = 1; k < NV; ++k)
+    for (int c = 0; c < D; ++c) beta[k][c] = Bm[(size_t)((k - 1) * D + c) * E + e];
+  for (int c = 0; c < D; ++c) {
+    double s = 0.0;
+    for (int k = 1; k < NV; ++k) s += beta[k][c];
+    beta[0][c] = -s;
+  }
+  double F[3][D];
+  for (int i = 0; i < 3; ++i)
+    for (int c = 0; c < D; ++c) {
+      double s = 0.0;
+      for (int a = 0; a < NV; ++a) s += q[3 * (size_t)vid[a] + i] * beta[a][c];
+      F[i][c] = s;
+    }
+  double U[3][D], sig[D], V[D][D], th[D], W[D][D];
+  int st = project_full<D>(F, model[e], mu[e], lam[e], 1e-6, U, sig, V, th, W);
+  if (st) {
+    for (int k = 0; k < D; ++k) sigma[(size_t)e * D + k] = theta[(size_t)e * D + k] = NAN;
+    return;
+  }
+  for (int k = 0; k < D; ++k) { sigma[(size_t)e * D + k] = sig[k]; theta[(size_t)e * D + k] = th[k]; }
+  for (int i = 0; i < 3; ++i)
+    for (int c = 0; c < D; ++c) {
+      double p = 0.0;
+      for (int k = 0; k < D; ++k) p += U[i][k] * th[k] * V[c][k];
+      Pout[(size_t)e * 3 * D + i * D + c] = p;
+    }
+  energy[e] = (model[e] == DP_MODEL_NEOHOOKEAN) ? nh_energy<D>(th, mu[e], lam[e]) : 0.0;
+}
+
+void launch_export_proj(dp_scene* s, const double* q, double* sigma, double* theta, double* P, double* energy) {
+  if (!s->E) return;
+  if (s->NV == 4)
+    k_export_proj<4><<<grid_for(s->E, 128), 128, 0, s->stream>>>(s->ev, s->B, s->mu, s->lam, s->model, s->E, q,
+                                                                  sigma, theta, P, energy);
+  else
+    k_export_proj<3><<<grid_for(s->E, 128), 128, 0, s->stream>>>(s->ev, s->B, s->mu, s->lam, s->model, s->E, q,
+                                                                  sigma, theta, P, energy);
+  s->launches++;
+}
+
+}  // namespace dp

@@ -1,0 +1,244 @@
+"""Callers of the hot path: procedural meshes, the identification loss and
+its finite-difference check (the parts of diffproj.ident that drive
+``rollout``/``backprop_rollout``; reference ident.py:81-216, :320-453).
+
+Kept on the host; only used to build synthetic workloads and to exercise
+the drop-in API the way the reference's own harness does.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import adjoint as aj
+from . import core
+from . import forward as fw
+
+# cube split into six tetrahedra along the main diagonal, one per axis order
+_AXIS_ORDERS = ((0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0))
+
+
+def box_tet_mesh(nx, ny, nz, size=1.0, origin=(0.0, 0.0, 0.0)):
+    """Grid of nx*ny*nz cubes, 6 positively oriented tets each (same vertex
+    and element order as the reference generator, ident.py:320-352)."""
+    n1 = np.array([nx + 1, ny + 1, nz + 1])
+    idx = np.stack(np.meshgrid(np.arange(n1[0]), np.arange(n1[1]), np.arange(n1[2]),
+                               indexing="ij"), axis=-1).reshape(-1, 3)
+    verts = np.asarray(origin, dtype=np.float64) + idx * float(size)
+    cubes = np.stack(np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"),
+                     axis=-1).reshape(-1, 3)
+
+    def vid(p):
+        return (p[..., 0] * n1[1] + p[..., 1]) * n1[2] + p[..., 2]
+
+    tets = np.empty((cubes.shape[0], 6, 4), dtype=np.int64)
+    for t, order in enumerate(_AXIS_ORDERS):
+        cur = cubes.copy()
+        tets[:, t, 0] = vid(cur)
+        for k, ax in enumerate(order):
+            cur = cur.copy()
+            cur[:, ax] += 1
+            tets[:, t, k + 1] = vid(cur)
+    tets = tets.reshape(-1, 4)
+    x = verts[tets]
+    det = np.linalg.det(np.stack([x[:, 1] - x[:, 0], x[:, 2] - x[:, 0], x[:, 3] - x[:, 0]], axis=2))
+    neg = det < 0
+    tets[neg, 2], tets[neg, 3] = tets[neg, 3].copy(), tets[neg, 2].copy()
+    return verts, tets
+
+
+def triangle_sheet(nx, nz, size=0.2, origin=(0.0, 0.0, 0.0)):
+    """Vertical sheet in the x-z plane (ident.py:355-369)."""
+    j, i = np.meshgrid(np.arange(nz + 1), np.arange(nx + 1), indexing="ij")
+    verts = np.stack([origin[0] + i.ravel() * size, np.full(i.size, origin[1]),
+                      origin[2] - j.ravel() * size], axis=1)
+    jj, ii = np.meshgrid(np.arange(nz), np.arange(nx), indexing="ij")
+    a = (jj * (nx + 1) + ii).ravel()
+    b, c = a + 1, a + nx + 1
+    d = c + 1
+    tris = np.stack([np.stack([a, b, c], 1), np.stack([b, d, c], 1)], axis=1).reshape(-1, 3)
+    return verts, tris
+
+
+def horizontal_sheet(nx, ny, size, origin=(0.0, 0.0, 0.0)):
+    """Triangle sheet in the x-y plane (C2 cloth)."""
+    j, i = np.meshgrid(np.arange(ny + 1), np.arange(nx + 1), indexing="ij")
+    verts = np.stack([origin[0] + i.ravel() * size, origin[1] + j.ravel() * size,
+                      np.full(i.size, origin[2])], axis=1)
+    jj, ii = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+    a = (jj * (nx + 1) + ii).ravel()
+    b, c = a + 1, a + nx + 1
+    d = c + 1
+    tris = np.stack([np.stack([a, b, c], 1), np.stack([b, d, c], 1)], axis=1).reshape(-1, 3)
+    return verts, tris
+
+
+def _mats(n, **kw):
+    return [core.MaterialParams(**kw) for _ in range(n)]
+
+
+def scene_library():
+    """Desk-scale scenes of the reference test-suite (ident.py:376-453)."""
+    out = {}
+    v, t = box_tet_mesh(2, 1, 1, size=0.5)
+    left = np.nonzero(v[:, 0] == 0.0)[0]
+    m = core.lumped_masses(v, t, 1000.0)
+    out["bar_arap"] = core.Scene(v, t, m, _mats(len(t), model="arap", stiffness=2e4),
+                                 bindings=[core.BindingSpec(i, v[i], 1e-6) for i in left], h=0.01)
+    out["bar_neohookean"] = core.Scene(v.copy(), t.copy(), m.copy(),
+                                       _mats(len(t), model="neohookean", E=5e4, nu=0.3),
+                                       bindings=[core.BindingSpec(i, v[i], 1e-6) for i in left], h=0.01)
+    vs, ts = triangle_sheet(3, 3, size=0.2, origin=(0.0, 0.0, 1.0))
+    out["hanging_sheet"] = core.Scene(vs, ts, core.lumped_masses(vs, ts, 0.3),
+                                      _mats(len(ts), model="arap", stiffness=50.0),
+                                      bindings=[core.BindingSpec(i, vs[i], 1e-6) for i in range(4)],
+                                      h=0.01)
+    vb, tb = box_tet_mesh(1, 1, 1, size=0.4, origin=(0.0, 0.0, 0.001))
+    out["block_on_plane"] = core.Scene(vb, tb, core.lumped_masses(vb, tb, 1000.0),
+                                       _mats(len(tb), model="arap", stiffness=5e4),
+                                       colliders=[core.HalfSpace([0, 0, 1], 0.0, mu=0.0)], h=0.01)
+    for tag, mu in (("high", 0.101), ("low", 0.099)):
+        out[f"friction_{tag}"] = core.Scene(
+            np.array([[0.0, 0.0, 1e-6]]), np.zeros((0, 4), np.int64), np.array([1000.0]), [],
+            colliders=[core.HalfSpace([0, 0, 1], 0.0, mu=mu)], eps_fb=1e-6,
+            fext=np.array([0.1 * 1000.0 * 9.8, 0.0, 0.0]), h=0.01)
+    out["friction_ident"] = core.Scene(
+        np.array([[0.0, 0.0, 1e-6]]), np.zeros((0, 4), np.int64), np.array([1.0]), [],
+        colliders=[core.HalfSpace([0, 0, 1], 0.0, mu=0.55)], eps_fb=2e-6,
+        fext=np.array([6.0, 0.0, 0.0]), h=0.01)
+    out["block_lift"] = core.Scene(
+        np.array([[0.0, 0.0, 1e-5]]), np.zeros((0, 4), np.int64), np.array([1.0]), [],
+        colliders=[core.HalfSpace([0, 0, 1], 0.0, mu=0.0)], eps_fb=2e-1,
+        contact_activation=10.0, h=0.01)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# identification problem (ident.py:81-216)
+
+
+def _setter_material(attr, model):
+    def f(scene, state0, x):
+        for m in scene.materials:
+            if m.model == model:
+                setattr(m, attr, float(x))
+    return f
+
+
+def _set_mu(scene, state0, x):
+    for c in scene.colliders:
+        c.mu = float(x)
+
+
+def _set_fext(axis):
+    def f(scene, state0, x):
+        g = np.zeros(scene.ndof)
+        g[axis::3] = float(x) / scene.n_verts
+        scene.fext = g
+    return f
+
+
+def _set_v0(axis):
+    def f(scene, state0, x):
+        state0.v[axis::3] = float(x)
+    return f
+
+
+def _set_eb(scene, state0, x):
+    for b in scene.bindings:
+        b.compliance = float(x)
+
+
+def _set_db_z(scene, state0, x):
+    for b in scene.bindings:
+        b.target[2] += float(x)
+
+
+def _get_fext(axis):
+    return lambda g, s: sum(float(np.sum(f[axis::3])) for f in g.dL_dfext) / s.n_verts
+
+
+VARIABLES = {
+    "stiffness": (_setter_material("stiffness", "arap"), lambda g, s: g.dL_dstiffness),
+    "E": (_setter_material("E", "neohookean"), lambda g, s: g.dL_dE),
+    "nu": (_setter_material("nu", "neohookean"), lambda g, s: g.dL_dnu),
+    "mu": (_set_mu, lambda g, s: g.dL_dmu_friction),
+    "fext_x": (_set_fext(0), _get_fext(0)),
+    "fext_y": (_set_fext(1), _get_fext(1)),
+    "fext_z": (_set_fext(2), _get_fext(2)),
+    "v0_x": (_set_v0(0), lambda g, s: float(np.sum(g.dL_dvbar[0::3]))),
+    "v0_z": (_set_v0(2), lambda g, s: float(np.sum(g.dL_dvbar[2::3]))),
+    "Eb": (_set_eb, lambda g, s: float(np.sum(g.dL_dEb))),
+    "db_z": (_set_db_z, lambda g, s: float(np.sum(g.dL_ddb[:, 2]))),
+}
+
+
+@dataclass
+class OptProblem:
+    scene: core.Scene
+    horizon: int
+    variable: str
+    init_value: float | np.ndarray
+    learning_rate: float = 1.0
+    iterations: int = 1
+    target_state: np.ndarray | None = None
+    target_value: float | np.ndarray | None = None
+    log_space: bool = False
+    fd_every: int = 0
+    fd_eta: float = 1e-4
+    initial_velocity: np.ndarray | None = None
+
+    def names(self):
+        names = [v.strip() for v in str(self.variable).split(",") if v.strip()]
+        for n in names:
+            if n not in VARIABLES:
+                raise ValueError(f"unknown variable {n!r}; known: {sorted(VARIABLES)}")
+        return names
+
+    @property
+    def scalar(self):
+        return len(self.names()) == 1
+
+
+def _prepared(problem, x):
+    scene = problem.scene.copy()
+    state0 = scene.rest_state()
+    if problem.initial_velocity is not None:
+        state0.v[:] = problem.initial_velocity
+    xv = np.atleast_1d(np.asarray(x, dtype=np.float64))
+    for name, xi in zip(problem.names(), xv):
+        VARIABLES[name][0](scene, state0, xi)
+    return scene, state0
+
+
+def resolve_target(problem, cfg=None):
+    if problem.target_state is None:
+        scene, state0 = _prepared(problem, problem.target_value)
+        states, _ = fw.rollout(scene, state0, problem.horizon, cfg=cfg)
+        problem.target_state = states[-1].q.copy()
+    return problem.target_state
+
+
+def rollout_loss(problem, x, with_grad=False, cfg=None):
+    target = resolve_target(problem, cfg)
+    scene, state0 = _prepared(problem, x)
+    states, caches = fw.rollout(scene, state0, problem.horizon, cfg=cfg)
+    L, _ = aj.loss_final_state(states[-1].q, target)
+    if not with_grad:
+        return L
+    grads = aj.backprop_rollout(caches, target)
+    g = np.array([VARIABLES[n][1](grads, scene) for n in problem.names()])
+    return L, (float(g[0]) if problem.scalar else g)
+
+
+def fd_gradient(problem, x, eta=None, cfg=None):
+    xv = np.atleast_1d(np.asarray(x, dtype=np.float64))
+    g = np.empty(xv.size)
+    for i in range(xv.size):
+        e = eta if eta is not None else problem.fd_eta * max(abs(xv[i]), 1.0)
+        d = np.zeros(xv.size)
+        d[i] = e
+        g[i] = (rollout_loss(problem, xv + d, cfg=cfg) - rollout_loss(problem, xv - d, cfg=cfg)) / (2 * e)
+    return float(g[0]) if problem.scalar else g

@@ -1,0 +1,221 @@
+"""CUDA path vs the reference (golden fixtures made by the reference itself)
+and vs the CPU oracle, through the package API over the C ABI."""
+
+import numpy as np
+import pytest
+
+from conftest import SCENES, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2603_16478_b200 as p
+    from paper_2603_16478_b200 import _lib
+    _lib.lib()   # raises when no GPU / library: no fallback
+    return p
+
+
+# ---------------------------------------------------------------- elements
+@pytest.mark.parametrize("tag", ["arap", "nh0", "nh1", "nh2"])
+def test_element_projection_batch(pkg, tag):
+    from paper_2603_16478_b200 import elasticity as el
+    g = load_golden("elements.npz")
+    F = g["F"]
+    n = F.shape[0]
+    if tag == "arap":
+        out = el.project_batch(F, "arap")
+    else:
+        mu, lam = g["lame"][int(tag[2])]
+        out = el.project_batch(F, "neohookean", np.full(n, mu), np.full(n, lam))
+        assert rel(out["dP_dmu"], g[f"{tag}_dP_dmu"]) < 1e-9
+        assert rel(out["dP_dlam"], g[f"{tag}_dP_dlam"]) < 1e-9
+    assert not out["status"].any()
+    assert np.allclose(out["sigma"], g[f"{tag}_sigma"], rtol=1e-13, atol=1e-14)
+    assert np.allclose(out["theta"], g[f"{tag}_theta"], rtol=1e-11, atol=1e-14)
+    assert np.allclose(out["W"], g[f"{tag}_W"], rtol=1e-9, atol=1e-14)
+    assert np.allclose(out["P"], g[f"{tag}_P"], atol=1e-12)
+    # gauge-invariant Jacobian incl. the degenerate-sigma (B4) cases
+    assert np.allclose(out["dPdF"], g[f"{tag}_dPdF"], atol=1e-9)
+
+
+def test_triangle_projection_batch(pkg):
+    from paper_2603_16478_b200 import elasticity as el
+    g = load_golden("elements.npz")
+    out = el.project_batch(g["tri_F"], "arap")
+    assert not out["status"].any()
+    assert np.allclose(out["sigma"], g["tri_sigma"], rtol=1e-13)
+    assert np.allclose(out["P"], g["tri_P"], atol=1e-12)
+    assert np.allclose(out["dPdF"], g["tri_dPdF"], atol=1e-10)
+
+
+def test_inverted_element_flagged(pkg):
+    from paper_2603_16478_b200 import elasticity as el
+    out = el.project_batch(np.diag([1.0, 1.0, -1.0])[None], "arap")
+    assert out["status"][0] == 2
+
+
+# ---------------------------------------------------------------- contacts
+def test_contact_batch(pkg):
+    from paper_2603_16478_b200 import contact as ct
+    g = load_golden("contacts.npz")
+    out = ct.contact_batch(g["frame"], g["d_n"], g["mu"], g["eps2"], g["q"], g["q_bar"])
+    assert not out["status"].any()
+    xs = np.abs(g["q"]).max() + np.abs(g["q_bar"]).max()
+    ad = 8e-16 * xs
+    assert np.allclose(out["delta"], g["delta"], rtol=1e-13, atol=ad)
+    assert np.array_equal(out["capped"].astype(bool), g["capped"])
+    lam_n = g["lam"][:, 0]
+    assert np.allclose(out["lam"][:, 0], lam_n, rtol=1e-9)
+    nfg = np.maximum(np.linalg.norm(g["delta"][:, 1:], axis=1), 1e-9)
+    tol_f = 1e-9 * lam_n + np.abs(g["s"]) * 4 * ad / nfg
+    assert np.all(np.abs(out["lam"][:, 1:] - g["lam"][:, 1:]) <= tol_f[:, None])
+    ref = g["Kc"]
+    assert np.allclose(out["Kc"], ref, rtol=1e-6, atol=1e-6 * np.abs(ref).max())
+    assert np.allclose(out["k_mu"], g["k_mu"], rtol=1e-6, atol=1e-9 * lam_n.max())
+    assert np.allclose(out["residual"], g["residual"], rtol=1e-6, atol=1e-12)
+
+
+def test_detection_bit_exact_vs_oracle(pkg, rng):
+    """Contact sets, frames and d_n equal the reference arithmetic exactly."""
+    import diffproj_oracle as O
+    from paper_2603_16478_b200 import contact as ct, core, ident
+    v, t = ident.box_tet_mesh(6, 6, 6, size=0.01, origin=(0.0, 0.0, 0.0))
+    scene = core.Scene(v, t, core.lumped_masses(v, t, 1000.0),
+                       [core.MaterialParams()] * len(t),
+                       colliders=[core.HalfSpace([0.1, -0.2, 1.0], -0.001, mu=0.3),
+                                  core.Sphere([0.03, 0.03, -0.02], 0.021, mu=0.1)],
+                       contact_activation=2e-3)
+    sm = core.assemble_system_matrix(scene)
+    osc = O.OScene(core.scene_to_arrays(scene))
+    for trial in range(4):
+        q = v.reshape(-1) + 2e-3 * rng.standard_normal(v.size)
+        got = ct.detect_contacts(scene, q, None, sysmat=sm)
+        ref = O.detect_contacts(osc, q)
+        assert len(got) == len(ref) > 0
+        assert np.array_equal([c.vertex for c in got], ref.vertex)
+        assert np.array_equal([c.collider for c in got], ref.collider)
+        assert np.array_equal(np.array([c.frame for c in got]), ref.frame)
+        assert np.array_equal(np.array([c.d_n for c in got]), ref.d_n)
+
+
+# ---------------------------------------------------------------- rollouts
+def _gpu_rollout(name, pkg):
+    from paper_2603_16478_b200 import core, forward as fw
+    g = load_golden(f"scene_{name}.npz")
+    scene = core.scene_from_arrays(g)
+    st0 = core.SimState(g["q"][0], g["v0"])
+    cfg = fw.ForwardConfig(tol=float(g["tol"]))
+    states, caches = fw.rollout(scene, st0, int(g["T"]), cfg=cfg)
+    return g, scene, states, caches
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_rollout_states_contacts_gradients(pkg, name):
+    from paper_2603_16478_b200 import adjoint as aj
+    g, scene, states, caches = _gpu_rollout(name, pkg)
+    T = int(g["T"])
+    for k in range(T):
+        q = states[k + 1].q
+        qs = g["q"][k + 1]
+        # states: normwise relative 1e-8
+        assert np.max(np.abs(q - qs)) <= 1e-8 * max(np.max(np.abs(qs)), 1e-3), (name, k)
+        m = g["c_step"] == k
+        cps = caches[k].contacts
+        assert np.array_equal(np.array([c.vertex for c in cps], np.int64), g["c_vertex"][m]), (name, k)
+        assert np.array_equal(np.array([c.collider for c in cps], np.int64), g["c_collider"][m])
+        if m.any():
+            assert np.allclose(np.array([c.frame for c in cps]), g["c_frame"][m], atol=1e-15)
+    gr = aj.backprop_rollout(caches, g["target"])
+    assert rel(gr.dL_dqbar, g["g_dqbar"]) < 1e-6
+    assert rel(gr.dL_dvbar, g["g_dvbar"]) < 1e-6
+    assert rel(np.array(gr.dL_dfext), g["g_dfext"]) < 1e-6
+    for k, ref in (("dL_dmu_friction", "g_dmu"), ("dL_dstiffness", "g_dstiffness"),
+                   ("dL_dE", "g_dE"), ("dL_dnu", "g_dnu")):
+        a, b = getattr(gr, k), float(g[ref])
+        assert abs(a - b) <= 1e-6 * abs(b) + 1e-18, (name, k, a, b)
+    if np.abs(g["g_dw"]).max() > 0:
+        assert rel(gr.dL_dw, g["g_dw"]) < 1e-6
+    if g["g_dEb"].size:
+        assert rel(gr.dL_dEb, g["g_dEb"]) < 1e-6
+        assert rel(gr.dL_ddb, g["g_ddb"]) < 1e-6
+
+
+@pytest.mark.parametrize("name", ["bar_neohookean", "block_on_plane", "friction_high", "single_tet_nh"])
+def test_newton_matrix_matches_reference(pkg, name):
+    from paper_2603_16478_b200 import adjoint as aj, core, forward as fw
+    g = load_golden(f"scene_{name}.npz")
+    scene = core.scene_from_arrays(g)
+    cfg = fw.ForwardConfig(tol=float(g["tol"]))
+    _, caches = fw.rollout(scene, core.SimState(g["q"][0], g["v0"]), 1, cfg=cfg)
+    ws = aj.assemble_adjoint_operator(caches[0])
+    A = ws.to_dense()
+    ref = g["newton_matrix_step1"]
+    assert np.allclose(A, ref, rtol=1e-8, atol=1e-8 * np.abs(ref).max())
+
+
+def test_system_matrix_A_matches_oracle(pkg):
+    import diffproj_oracle as O
+    from paper_2603_16478_b200 import core
+    g = load_golden("scene_c1lite.npz")
+    scene = core.scene_from_arrays(g)
+    sm = core.assemble_system_matrix(scene)
+    osc = O.OScene(g)
+    Aref = O.assemble_A(osc, O.build_elements(osc)).toarray()
+    A = sm.A.to_dense()
+    assert np.allclose(A, Aref, rtol=1e-12, atol=1e-12 * np.abs(Aref).max())
+
+
+def test_raises_on_nonconvergence(pkg):
+    from paper_2603_16478_b200 import core, forward as fw
+    scene = core.Scene(np.array([[0.0, 0.0, 1e-4]]), np.zeros((0, 4), np.int64), np.array([2.0]), [],
+                       colliders=[core.HalfSpace([0, 0, 1], 0.0, mu=0.0)])
+    with pytest.raises(RuntimeError, match="did not converge"):
+        fw.rollout(scene, scene.rest_state(), 1, cfg=fw.ForwardConfig(tol=1e-30, max_iter=2))
+
+
+def test_free_fall_symplectic_euler(pkg):
+    from paper_2603_16478_b200 import core, forward as fw
+    scene = core.Scene(np.array([[0.0, 0.0, 1.0]]), np.zeros((0, 4), np.int64), np.array([2.0]), [])
+    states, _ = fw.rollout(scene, scene.rest_state(), 5)
+    v = 0.0
+    z = 1.0
+    for k in range(1, 6):
+        v += 0.01 * -9.8
+        z += 0.01 * v
+        assert states[k].q[2] == pytest.approx(z, abs=1e-9)
+        assert states[k].v[2] == pytest.approx(v, abs=1e-9)
+
+
+def test_random_cube_vs_oracle(pkg):
+    """A scene not in the fixtures: NH cube on plane + sphere, sliding, oracle-checked."""
+    import diffproj_oracle as O
+    from paper_2603_16478_b200 import adjoint as aj, core, forward as fw, ident
+    v, t = ident.box_tet_mesh(3, 3, 3, size=0.1 / 3, origin=(0.0, 0.0, 4e-4))
+    scene = core.Scene(v, t, core.lumped_masses(v, t, 1000.0),
+                       [core.MaterialParams("neohookean", E=2e4, nu=0.35)] * len(t),
+                       colliders=[core.HalfSpace([0, 0, 1], 0.0, mu=0.4),
+                                  core.Sphere([0.05, -0.0205, 0.05], 0.0206, mu=0.2)],
+                       h=0.01)
+    st0 = scene.rest_state()
+    st0.v[0::3] = 0.1
+    cfg = fw.ForwardConfig(tol=1e-12)
+    states, caches = fw.rollout(scene, st0, 4, cfg=cfg)
+    osc = O.OScene(core.scene_to_arrays(scene))
+    els, A, steps = O.rollout(osc, st0.q, st0.v, 4, O.ForwardConfig(tol=1e-12))
+    for k in range(4):
+        assert np.max(np.abs(states[k + 1].q - steps[k].q_new)) <= 1e-8 * np.max(np.abs(steps[k].q_new))
+        assert np.array_equal([c.vertex for c in caches[k].contacts], steps[k].contacts.vertex)
+    target = states[-1].q + 1e-3
+    g = aj.backprop_rollout(caches, target)
+    og = O.backprop_rollout(osc, els, A, steps, target=target)
+    assert rel(g.dL_dqbar, og.dL_dqbar) < 1e-6
+    assert abs(g.dL_dE - og.dL_dE) <= 1e-6 * abs(og.dL_dE)
+    assert abs(g.dL_dnu - og.dL_dnu) <= 1e-6 * abs(og.dL_dnu)
+    assert abs(g.dL_dmu_friction - og.dL_dmu_friction) <= 1e-6 * abs(og.dL_dmu_friction)

@@ -1,0 +1,439 @@
+"""Benchmark: fwd+bwd implicit steps/s at N tets on B200 (BASELINE.json metric).
+
+Workload (default --config c5): box_tet_mesh(55,55,55)
+= 998,250 Neo-Hookean tets (E=1e4, nu=0.3, 10 cm cube), frictional ground
+plane (mu=0.5) and two kinematic sphere "fingers" (mu=0.5) closing on the
+cube by 20 um per step.  A "step" = one forward Newton step + its adjoint
+step (A_hat^T solve + z-products) of a K-step rollout with a final-state
+loss; parameter gradient dL/d(E, nu, mu) allreduced across ranks (NCCL) at
+the end of every rollout.
+
+  value : device-resident path (inputs already in HBM), CUDA events on the
+          scene stream, max over ranks, whole-job steps/s.
+  e2e   : the public API (rollout + backprop_rollout) with host NumPy
+          buffers: host<->device copies inside the timed region.
+  cpu_baseline / --impl reference : the CPU oracle port (oracle/, a
+          vectorised restatement of the reference) on a bounded sub-sample
+          (a smaller cube of the same scene family), extrapolated linearly
+          in tets (generous to the CPU; SuperLU scales worse than linear).
+
+Inputs are larger than L2 (val ~200 MB per SpMV operand at C5); no explicit
+flush.  Launch: python bench.py [--gpus N --steps K --warmup W]; for N>1 via
+torchrun (one process per GPU).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (cells per side, description)
+    "c5": (55, "1M-tet NH cube gripped by 2 kinematic sphere fingers on a frictional ground (C5)"),
+    "c3": (26, "105k-tet NH cube on frictional ground (C3-scale single rollout)"),
+    "c1": (9, "4,374-tet NH cube on frictional ground (C1)"),
+}
+# Smoothed-FB eps_fb (= 2 eps^2) per mesh resolution.  The condensed normal
+# force eps^2/delta at the activation distance (1 mm) must stay below a
+# vertex's weight, otherwise the activation discontinuity of the reference
+# model (contact.py:129-130) makes Newton cycle at
+# |r| ~ h^2 eps^2 / activation.  The default 1e-6 is fine down to C1 vertex
+# masses (~1e-3 kg) but not for C3/C5 (~6e-5 / 6e-6 kg).
+EPS_FB = {55: 1e-9, 26: 1e-7, 9: 1e-6}
+SIZE = 0.1          # cube edge (m)
+E_YOUNG = 1e4
+NU = 0.3
+MU = 0.5
+
+
+def make_scene(n, fingers=True, eps_fb=None):
+    from paper_2603_16478_b200 import core, ident
+    v, t = ident.box_tet_mesh(n, n, n, size=SIZE / n, origin=(0.0, 0.0, 5e-4))
+    mat = core.MaterialParams("neohookean", E=E_YOUNG, nu=NU)
+    cols = [core.HalfSpace([0, 0, 1], 0.0, mu=MU)]
+    if fingers:
+        r = 0.02
+        zc = 5e-4 + SIZE / 2
+        cols.append(core.Sphere([-r - 5e-4, SIZE / 2, zc], r, mu=MU))
+        cols.append(core.Sphere([SIZE + r + 5e-4, SIZE / 2, zc], r, mu=MU))
+    if eps_fb is None:
+        eps_fb = EPS_FB.get(n, 1e-6)
+    return core.Scene(v, t, core.lumped_masses(v, t, 1000.0), [mat] * len(t),
+                      colliders=cols, h=0.01, eps_fb=eps_fb)
+
+
+def move_fingers(scene, k):
+    """Kinematic fingers: close by 20 um per step (host-side, colliders are
+    re-read every step as in contact.py:125-127)."""
+    if len(scene.colliders) < 3:
+        return
+    x0 = -0.02 - 5e-4 + 2e-5 * k
+    scene.colliders[1].center[0] = x0
+    scene.colliders[2].center[0] = SIZE + 0.02 + 5e-4 - 2e-5 * k
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, p[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def gpu_arm(args, rank, world, local_rank):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_16478_b200 import _lib, adjoint as aj, core, forward as fw
+    from paper_2603_16478_b200.parallel import allreduce_gradients, pack_gradients
+
+    torch.cuda.set_device(local_rank)
+    n, desc = CONFIGS[args.config]
+    scene = make_scene(n, fingers=(args.config == "c5"))
+    # batch of parameter candidates: rank r simulates E * (1 + 0.05 r)
+    for m in scene.materials[:1]:
+        pass
+    if rank:
+        mat = core.MaterialParams("neohookean", E=E_YOUNG * (1 + 0.05 * rank), nu=NU)
+        scene.materials = [mat] * len(scene.materials)
+    t_setup = time.perf_counter()
+    sysmat = core.assemble_system_matrix(scene, device=local_rank)
+    setup_s = time.perf_counter() - t_setup
+    dev = sysmat.dev
+    L = dev.lib
+    info = dev.info()
+    V, E_ = scene.n_verts, len(scene.elements)
+    n3 = 3 * V
+    K, W = args.steps, args.warmup
+    cfg = fw.ForwardConfig()
+    scfg = aj.SolverConfig(tol=1e-10, max_iter=2000).to_c()
+    dd = dict(device="cuda:%d" % local_rank, dtype=torch.float64)
+    stream = torch.cuda.ExternalStream(L.dp_scene_stream(dev.handle))
+
+    def device_rollout(nsteps, k0):
+        """forward K steps + reverse sweep, all device-resident."""
+        q = [torch.empty(n3, **dd) for _ in range(nsteps + 1)]
+        v = [torch.empty(n3, **dd) for _ in range(nsteps + 1)]
+        q[0].copy_(torch.from_numpy(scene.vertices.reshape(-1)))
+        v[0].zero_()
+        torch.cuda.synchronize()
+        caches, stats = [], []
+        for k in range(nsteps):
+            move_fingers(scene, k0 + k)
+            _, rep = fw.forward_step(scene, None, sysmat, cfg,
+                                     device_io=dict(q_bar=q[k], v_bar=v[k], q_out=q[k + 1], v_out=v[k + 1]))
+            caches.append(rep.cache)
+            stats.append((rep.converged, rep.iterations, rep.krylov_iterations, rep.n_contacts))
+        target = q[0] + 1e-3          # synthetic target shape
+        dq = 2.0 * (q[nsteps] - target)
+        dv = torch.zeros(n3, **dd)
+        z = torch.empty(n3, **dd)
+        dqb = torch.empty(n3, **dd)
+        dvb = torch.empty(n3, **dd)
+        dfx = torch.empty(n3, **dd)
+        torch.cuda.synchronize()
+        _lib.check(L.dp_grads_reset(dev.handle))
+        adj_iters = 0
+        for k in range(nsteps, 0, -1):
+            c = caches[k - 1]._dc.handle
+            _lib.check(L.dp_adjoint_assemble(dev.handle, c, None))
+            rep = _lib.SolveReportC()
+            _lib.check(L.dp_adjoint_solve(dev.handle, c, _lib.ptr(dq), _lib.ptr(dv), _lib.PTR_DEVICE,
+                                          C.byref(scfg), _lib.ptr(z), C.byref(rep)))
+            adj_iters += rep.iterations
+            _lib.check(L.dp_backprop_step(dev.handle, c, _lib.ptr(z), _lib.ptr(dv), _lib.PTR_DEVICE,
+                                          _lib.ptr(dqb), _lib.ptr(dvb), _lib.ptr(dfx)))
+            dq, dqb = dqb, dq
+            dv, dvb = dvb, dv
+        grads = aj.GradientReport()
+        grads.ensure_shapes(len(scene.bindings), dev.n_elems)
+        aj._fold_device_grads(dev, scene, grads)
+        loss = float(torch.sum((q[nsteps] - target) ** 2))
+        return grads, loss, stats, adj_iters
+
+    # warm-up (untimed)
+    for _ in range(max(W, 0)):
+        device_rollout(1, 0)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    L.dp_scene_reset_timing(dev.handle)
+    with ClockSampler(local_rank) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+        grads, loss, stats, adj_iters = device_rollout(K, W)
+        gvec = pack_gradients(grads, loss, dd["device"])
+        allreduce_gradients(gvec, world)
+        with torch.cuda.stream(stream):
+            ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = int(L.dp_scene_launch_count(dev.handle))
+    t = torch.tensor([ms], device=dd["device"])
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # roofline: dominant kernel = the SELL-32 BSR SpMV of the Krylov solves
+    x = torch.randn(n3, **dd)
+    y = torch.empty(n3, **dd)
+    fms = C.c_float()
+    reps = 30
+    _lib.check(L.dp_bench_spmv(dev.handle, 1, _lib.ptr(x), _lib.ptr(y), 3, C.byref(fms)))
+    _lib.check(L.dp_bench_spmv(dev.handle, 1, _lib.ptr(x), _lib.ptr(y), reps, C.byref(fms)))
+    spmv_ms = fms.value / reps
+    nnzb = info.nnzb
+    spmv_bytes = 76 * nnzb + 4 * (V + 1) + 48 * V
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = spmv_bytes / (spmv_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"spmv_traffic_{args.config}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except ValueError:
+            traffic = None
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.skip_e2e:
+        st0 = scene.rest_state()
+        for k in range(1):    # untimed warm call of the host path
+            pass
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        states, caches = [st0], []
+        st = st0
+        for k in range(K):
+            move_fingers(scene, W + k)
+            st, rep = fw.forward_step(scene, st, sysmat, cfg)
+            states.append(st)
+            caches.append(rep.cache)
+        target = st0.q + 1e-3
+        g2 = aj.backprop_rollout(caches, target)
+        gv2 = pack_gradients(g2, float(np.sum((states[-1].q - target) ** 2)), dd["device"])
+        allreduce_gradients(gv2, world)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        tw = torch.tensor([wall], device=dd["device"])
+        if world > 1:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        wall = float(tw.item())
+        h2d = (2 * n3 + 2 * n3) * 8           # forward (q_bar, v_bar) + adjoint (dL_dq, dL_dv)
+        d2h = (2 * n3 + 4 * n3) * 8           # forward (q, v) + adjoint (z, dqbar, dvbar, dfext)
+        h2d += 8 * n3                          # backprop z re-upload
+        e2e = {"value": world * K / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+    conv = [s[0] for s in stats]
+    return dict(ms=ms_max, launches=launches, clocks=clk.summary(), spmv_ms=spmv_ms, spmv_bytes=spmv_bytes,
+                achieved=achieved, hbm=hbm, traffic=traffic, e2e=e2e, setup_s=setup_s,
+                nnzb=nnzb, V=V, E=E_, desc=desc, newton=[s[1] for s in stats],
+                krylov=[s[2] for s in stats], contacts=[s[3] for s in stats], converged=all(conv),
+                adj_iters=adj_iters, dE=grads.dL_dE, loss=loss, device_bytes=info.device_bytes)
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reported baseline / reference arm)
+
+
+def _oracle_sample(n_cells, steps, eps_fb=None):
+    """One process: the oracle port on an n_cells^3 cube of the same scene
+    family; returns (seconds per fwd+bwd step, tets)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import diffproj_oracle as O
+    from paper_2603_16478_b200 import core
+    scene = make_scene(n_cells, fingers=False, eps_fb=eps_fb)
+    osc = O.OScene(core.scene_to_arrays(scene))
+    q0 = scene.vertices.reshape(-1).copy()
+    v0 = np.zeros_like(q0)
+    t0 = time.perf_counter()
+    els, A, st = O.rollout(osc, q0, v0, steps, raise_on_failure=False)
+    O.backprop_rollout(osc, els, A, st, target=q0 + 1e-3)
+    dt = time.perf_counter() - t0
+    return dt / steps, len(scene.elements)
+
+
+def _oracle_worker(args):
+    n_cells, steps = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    return _oracle_sample(n_cells, steps)
+
+
+def cpu_baseline(n_tets_target, n_cells=8, steps=1, procs=1):
+    """Bounded CPU sample; returns the JSON object for cpu_baseline."""
+    if procs <= 1:
+        sec, tets = _oracle_sample(n_cells, steps)
+        per_proc = [sec]
+    else:
+        import multiprocessing as mp
+        ctx = mp.get_context("spawn")
+        with ctx.Pool(procs) as pool:
+            res = pool.map(_oracle_worker, [(n_cells, steps)] * procs)
+        per_proc = [r[0] for r in res]
+        tets = res[0][1]
+    # steps/s at the target size, extrapolated linearly in tets
+    rate = sum(1.0 / s for s in per_proc) * tets / n_tets_target
+    return {"value": rate, "unit": "steps/s", "cores": procs, "kind": "port",
+            "sample": (f"oracle port (oracle/diffproj_oracle.py, NumPy+SuperLU) on a "
+                       f"{n_cells}^3-cell cube ({tets} tets, same scene family), {steps} fwd+bwd "
+                       f"step(s) x {procs} process(es): {np.mean(per_proc):.2f} s/step; "
+                       f"extrapolated linearly to {n_tets_target} tets")}
+
+
+# ---------------------------------------------------------------------------
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-cells", type=int, default=12)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(1)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n_cells = CONFIGS[args.config][0]
+    n_tets = 6 * n_cells ** 3
+    config = {"workload": f"{args.config}: {CONFIGS[args.config][1]}", "n_tets": n_tets,
+              "n_verts": (n_cells + 1) ** 3, "steps_per_rollout": args.steps,
+              "rollouts": world, "parallelism": f"dp{world} (independent rollouts, NCCL grad allreduce)",
+              "material": f"neohookean E={E_YOUNG} nu={NU}", "friction_mu": MU, "h": 0.01,
+              "l2": "operands > L2 (no flush)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        procs = os.cpu_count() or 1
+        W, K = args.warmup, args.steps
+        t0 = time.perf_counter()
+        base = cpu_baseline(n_tets, n_cells=args.cpu_cells, steps=1, procs=procs)
+        wall = time.perf_counter() - t0
+        line = {"metric": "fwd+bwd sim steps/sec at N tets", "value": base["value"], "unit": "steps/s",
+                "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": 1e3 / base["value"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config, "impl": "reference",
+                "cpu_baseline": base,
+                "e2e": {"value": base["value"], "unit": "steps/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0},
+                "wall_s": wall}
+        print(json.dumps(line))
+        return
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    r = gpu_arm(args, rank, world, local_rank)
+    if rank == 0:
+        K = args.steps
+        steps_total = world * K
+        value = steps_total / (r["ms"] * 1e-3)
+        line = {"metric": "fwd+bwd sim steps/sec at N tets", "value": value, "unit": "steps/s",
+                "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": r["ms"] / K,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (procedural mesh, random-free)", "config": config,
+                "tet_steps_per_s_M": value * n_tets / 1e6,
+                "roofline": {"bound": "hbm", "kernel": "k_spmv (SELL-32 3x3-BSR SpMV)",
+                             "achieved": r["achieved"], "peak": r["hbm"], "unit": "GB/s",
+                             "frac": r["achieved"] / r["hbm"], "traffic": r["traffic"],
+                             "bytes_per_launch": r["spmv_bytes"], "ms_per_launch": r["spmv_ms"],
+                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+                "clocks": r["clocks"], "gpu_launches": r["launches"], "e2e": r["e2e"],
+                "newton_iterations": r["newton"], "krylov_iterations": r["krylov"],
+                "adjoint_krylov_iterations": r["adj_iters"], "contacts": r["contacts"],
+                "converged": r["converged"], "setup_s": r["setup_s"], "nnzb": r["nnzb"],
+                "device_bytes": r["device_bytes"]}
+        if not args.skip_cpu and world == 1:
+            try:
+                line["cpu_baseline"] = cpu_baseline(n_tets, n_cells=args.cpu_cells, steps=1, procs=1)
+            except Exception as ex:   # the baseline must not kill the GPU line
+                line["cpu_baseline"] = {"value": None, "error": repr(ex)[:200]}
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -154,6 +155,8 @@ static int raise_status(int st) {
 }  // namespace dp
 
 using namespace dp;
+
+static const int g_debug = getenv("DP_DEBUG") ? atoi(getenv("DP_DEBUG")) : 0;
 
 // ===========================================================================
 extern "C" {
@@ -761,6 +764,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
   int n_contacts = 0, asym = 0;
   // q at the last Jacobian evaluation (forward.py:201): the adjoint operator's point
   double* q_eval = s->q_ev;
+  double last_t = 1.0;   // step length accepted by the previous line search
   for (int it = 0; it < cfg.max_iter; ++it) {
     k_reset_flags<<<1, 1, 0, s->stream>>>(s->esc);
     launch_detect(s, q);
@@ -784,19 +788,27 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     // forcing term: aim the linear residual at 0.1 * tol * scale in 2-norm
     const double rn = std::sqrt(E.rnorm2);
     double eta = (rn > 0) ? 0.1 * cfg.tol * scale / rn : cfg.lin_rtol_max;
-    eta = std::min(cfg.lin_rtol_max, std::max(cfg.lin_rtol_min, eta));
+    // after a line search that had to cut the step below 1/16 the Newton
+    // model is poor (friction cone / activation kinks): a cheap direction is enough
+    const double eta_cap = (last_t < 1.0 / 16) ? std::max(cfg.lin_rtol_max, 1e-2) : cfg.lin_rtol_max;
+    eta = std::min(eta_cap, std::max(cfg.lin_rtol_min, eta));
     int iters = 0, brk = 0;
     double relres = 0;
     if (!asym) {
       rc = cg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk);
       R.krylov_iterations += iters;
       if (brk) {
-        rc = gmres_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, cfg.gmres_restart, &iters, &relres);
+        rc = gmres_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, cfg.gmres_restart, &iters, &relres,
+                         2.0);
         R.krylov_iterations += iters;
       }
     } else {
-      rc = gmres_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, cfg.gmres_restart, &iters, &relres);
+      rc = gmres_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, cfg.gmres_restart, &iters, &relres, 2.0);
       R.krylov_iterations += iters;
+    }
+    if (g_debug) {
+      fprintf(stderr, "[dp] it=%d res=%.3e |r|2=%.3e C=%d asym=%d eta=%.1e krylov=%d relres=%.2e rc=%d\n", it, res, rn,
+              n_contacts, asym, eta, iters, relres, rc);
     }
     // line search (forward.py:214-234)
     double t = 1.0;
@@ -810,6 +822,9 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
       R.line_search_trials++;
       if ((rc = sync_esc(s))) return rc;
       const EvalScalars T = *s->h_esc;
+      if (g_debug > 1)
+        fprintf(stderr, "[dp]   ls=%d t=%.3e pen=%d st=%d rmax_try=%.6e (rmax=%.6e)\n", ls, t, T.penetrating, T.status,
+                T.rmax, E.rmax);
       if (!T.penetrating) {
         const int st = T.status;
         const bool value_error = (st & (ST_INVERTED | ST_NONFINITE | ST_PENETRATION)) != 0;
@@ -822,6 +837,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
       }
       t *= 0.5;
     }
+    last_t = accepted ? t : 0.0;
     if (!accepted) {
       launch_axpy_to(s, q_try, q, t, s->dq);
       k_reset_flags<<<1, 1, 0, s->stream>>>(s->esc);
@@ -984,6 +1000,7 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
   } else {
     rc = gmres_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, cfg.gmres_restart, &iters, &relres);
   }
+  if (g_debug) fprintf(stderr, "[dp] adjoint sym=%d iters=%d relres=%.2e\n", sym, iters, relres);
   if (rep) {
     rep->converged = relres <= cfg.tol;
     rep->iterations = iters;

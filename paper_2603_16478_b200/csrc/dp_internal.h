@@ -218,7 +218,7 @@ void launch_spmv(dp_scene* s, const double* val, const double* x, double* y);
 int cg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
              int* iters, double* relres, int* breakdown);
 int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
-                int restart, int* iters, double* relres);
+                int restart, int* iters, double* relres, double min_cycle_gain = 0.0);
 double device_norm2(dp_scene* s, const double* x);   // sum of squares, synchronous
 // vector ops
 void launch_axpy_to(dp_scene* s, double* out, const double* a, double t, const double* b);   // out = a + t*b

@@ -841,34 +841,122 @@ __global__ void __launch_bounds__(256) k_gm_apply(int V, int S, const int* __res
   }
 }
 
-// coef_i = (w, v_i) for i <= j; pass 0 also |w|^2 -> wn2_before.
-__global__ void __launch_bounds__(kGT) k_gm_dots(int n, int j, int pass, const double* __restrict__ Vb, size_t ld,
-                                                 const double* __restrict__ w, double* partial, unsigned int* counter,
-                                                 GmresScalars* gs) {
-  __shared__ double sh[32];
+// Fused GMRES column kernel (pass 0), one warp per SELL slice:
+//   v_j = w_prev / hn            (own rows, written to the basis)
+//   w   = Minv A v_j             (SpMV on the gathered w_prev / hn)
+//   coef_i = (w, v_i), i <= j and |w|^2   (block partials, last block folds)
+// Replaces apply + normalize + a separate dot pass: the basis rows of this
+// slice are read once, w is written once.
+__global__ void __launch_bounds__(256) k_gm_spmvdot(int V, int S, const int* __restrict__ slice_base,
+                                                    const int* __restrict__ slice_width, const int* __restrict__ col,
+                                                    const double* __restrict__ val, const double* __restrict__ minv,
+                                                    const double* __restrict__ wprev, double* __restrict__ vj,
+                                                    double* __restrict__ wnew, const double* __restrict__ Vb, size_t ld,
+                                                    int j, double* partial, unsigned int* counter, GmresScalars* gs) {
+  __shared__ double sh[8][kGM1 + 1];
+  __shared__ double sred[32];
   if (ldflag(&gs->done)) return;
-  if (pass == 1 && !ldflag(&gs->reorth)) return;
-  const int nd = (pass == 0) ? j + 2 : j + 1;
-  for (int i = 0; i < nd; ++i) {
-    const double* vi = (i <= j) ? Vb + (size_t)i * ld : w;
-    double acc = 0.0;
-    for (int k = blockIdx.x * kGT + threadIdx.x; k < n; k += gridDim.x * kGT) acc += w[k] * vi[k];
-    double t = block_sum<kGT>(acc, sh);
-    if (threadIdx.x == 0) partial[(size_t)blockIdx.x * (kGM1 + 1) + i] = t;
+  const double inv = 1.0 / gs->hn;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * 8 + warp;
+  const int row = gw * kSlice + lane;
+  double u[3] = {0.0, 0.0, 0.0}, vr[3] = {0.0, 0.0, 0.0};
+  if (gw < S) {
+    double a[3];
+    spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, wprev, a);
+    if (row < V) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        a[c] *= inv;
+        vr[c] = wprev[3 * row + c] * inv;
+        vj[3 * row + c] = vr[c];
+      }
+      minv_apply(minv, V, row, a, u);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) wnew[3 * row + c] = u[c];
+    }
+  }
+  const bool live = (gw < S) && (row < V);
+  for (int i = 0; i <= j + 1; ++i) {
+    double d = 0.0;
+    if (live) {
+      if (i < j) {
+        const double* vi = Vb + (size_t)i * ld + 3 * (size_t)row;
+        d = u[0] * vi[0] + u[1] * vi[1] + u[2] * vi[2];
+      } else if (i == j) {
+        d = u[0] * vr[0] + u[1] * vr[1] + u[2] * vr[2];
+      } else {
+        d = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+      }
+    }
+    d = warp_sum(d);
+    if (lane == 0) sh[warp][i] = d;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += sh[w][i];
+    partial[(size_t)blockIdx.x * (kGM1 + 1) + i] = t;
   }
   if (last_block(counter)) {
-    for (int i = 0; i < nd; ++i) {
+    for (int i = 0; i <= j + 1; ++i) {
       double acc = 0.0;
-      for (int b = threadIdx.x; b < (int)gridDim.x; b += kGT) acc += __ldcg(partial + (size_t)b * (kGM1 + 1) + i);
-      double t = block_sum<kGT>(acc, sh);
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) acc += __ldcg(partial + (size_t)b * (kGM1 + 1) + i);
+      double t = block_sum<256>(acc, sred);
       if (threadIdx.x == 0) {
         if (i <= j) {
           gs->coef[i] = t;
-          double* Hc = gs->H + (size_t)j * kGM1;
-          Hc[i] = (pass == 0) ? t : Hc[i] + t;
+          gs->H[(size_t)j * kGM1 + i] = t;
         } else {
           gs->wn2_before = t;
         }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+// Re-orthogonalisation dots (pass 1 only, when flagged): coef_i = (w, v_i),
+// i <= j, one read of the basis; accumulators in register chunks of 8.
+__global__ void __launch_bounds__(kGT) k_gm_dots(int n, int j, const double* __restrict__ Vb, size_t ld,
+                                                 const double* __restrict__ w, double* partial, unsigned int* counter,
+                                                 GmresScalars* gs) {
+  __shared__ double sh[kGT / 32][kGM1 + 1];
+  __shared__ double sred[32];
+  if (ldflag(&gs->done)) return;
+  if (!ldflag(&gs->reorth)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i0 = 0; i0 <= j; i0 += 8) {
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int k = blockIdx.x * kGT + threadIdx.x; k < n; k += gridDim.x * kGT) {
+      const double wk = w[k];
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (i0 + t <= j) acc[t] += wk * Vb[(size_t)(i0 + t) * ld + k];
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const double d = warp_sum(acc[t]);
+      if (lane == 0 && i0 + t <= j) sh[warp][i0 + t] = d;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= j; i += kGT) {
+    double t = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kGT / 32; ++ww) t += sh[ww][i];
+    partial[(size_t)blockIdx.x * (kGM1 + 1) + i] = t;
+  }
+  if (last_block(counter)) {
+    for (int i = 0; i <= j; ++i) {
+      double acc = 0.0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += kGT) acc += __ldcg(partial + (size_t)b * (kGM1 + 1) + i);
+      double t = block_sum<kGT>(acc, sred);
+      if (threadIdx.x == 0) {
+        gs->coef[i] = t;
+        gs->H[(size_t)j * kGM1 + i] += t;
       }
       __syncthreads();
     }
@@ -998,7 +1086,7 @@ static int gm_grid(int n) {
 // Restarted GMRES on A x = b (true relative residual <= rtol).  x is
 // overwritten (zero initial guess).  Returns 0 converged, 1 not converged.
 int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int restart,
-                int* iters, double* relres) {
+                int* iters, double* relres, double min_cycle_gain) {
   const int V = s->V, n = 3 * V;
   if (restart > kMaxRestart) restart = kMaxRestart;
   if (restart > n) restart = n;
@@ -1008,7 +1096,6 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   const int nbs = grid_for((int64_t)s->S * 32, 256);
   const int nbg = gm_grid(n);
   double* Vb = s->gm_V;
-  double* w = s->kw;
   double* r = s->kr;
   double* y_dev = s->ks;   // scratch (>= restart doubles)
   *iters = 0;
@@ -1016,7 +1103,7 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   const double bnorm = sqrt(device_norm2(s, b));
   if (bnorm == 0.0) { *relres = 0.0; return 0; }
   // |M^-1 b|
-  k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, b, w, s->red.partial, s->red.counter, s->gsc, rtol, 1);
+  k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, b, s->kw, s->red.partial, s->red.counter, s->gsc, rtol, 1);
   s->launches++;
   int total = 0;
   double rel = 1.0;
@@ -1024,9 +1111,9 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
     rel = true_relres(s, val, b, x, r, bnorm);
     if (rel <= rtol) break;
     const double cycle_start = rel;
-    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, r, Vb, s->red.partial, s->red.counter, s->gsc, rtol, 0);
-    k_gm_normalize<<<nbg, kGT, 0, s->stream>>>(n, Vb, Vb, s->gsc);
-    s->launches += 2;
+    double* Wb[2] = {s->kw, s->kp};   // double-buffered unnormalised basis vector
+    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, r, Wb[0], s->red.partial, s->red.counter, s->gsc, rtol, 0);
+    s->launches++;
     int j = 0;
     bool stop = false;
     while (j < restart && total < max_iter && !stop) {
@@ -1034,15 +1121,15 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
       if (j + chunk > restart) chunk = restart - j;
       if (total + chunk > max_iter) chunk = max_iter - total;
       for (int c = 0; c < chunk; ++c, ++j) {
-        k_gm_apply<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, s->minv,
-                                               Vb + (size_t)j * ld, w, s->gsc);
-        k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, 0, Vb, ld, w, s->red.partial, s->red.counter, s->gsc);
-        k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, j, 0, Vb, ld, w, s->red.partial, s->red.counter, s->gsc);
-        k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, 1, Vb, ld, w, s->red.partial, s->red.counter, s->gsc);
-        k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, j, 1, Vb, ld, w, s->red.partial, s->red.counter, s->gsc);
-        if (j + 1 < restart)
-          k_gm_normalize<<<nbg, kGT, 0, s->stream>>>(n, w, Vb + (size_t)(j + 1) * ld, s->gsc);
-        s->launches += 6;
+        double* wp = Wb[j & 1];
+        double* wn = Wb[(j + 1) & 1];
+        k_gm_spmvdot<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, s->minv, wp,
+                                                 Vb + (size_t)j * ld, wn, Vb, ld, j, s->red.partial, s->red.counter,
+                                                 s->gsc);
+        k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, j, 0, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc);
+        k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc);
+        k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, j, 1, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc);
+        s->launches += 4;
       }
       cudaMemcpyAsync(s->h_gsc, s->gsc, sizeof(GmresScalars), cudaMemcpyDeviceToHost, s->stream);
       cudaStreamSynchronize(s->stream);
@@ -1068,6 +1155,9 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
     rel = true_relres(s, val, b, x, r, bnorm);
     if (rel <= rtol) break;
     if (rel >= cycle_start * (1.0 - 1e-12)) break;   // stagnation (linsolve.py:187-188)
+    // inexact-Newton use: a restart cycle that gains less than min_cycle_gain
+    // means GMRES(m) is stagnating; return the best iterate so far
+    if (min_cycle_gain > 0.0 && rel > cycle_start / min_cycle_gain) break;
     if (used == 0) break;
   }
   *relres = rel;

@@ -140,6 +140,14 @@ int dp_scene_set_params(dp_scene* s, double h, double eps_fb, double contact_act
                         const double* gravity3);
 /* per-dof fext (core.Scene.fext); NULL clears it.  ptr_kind as above. */
 int dp_scene_set_fext(dp_scene* s, const double* fext, int32_t ptr_kind);
+/* Krylov preconditioner: 0 -> 3x3 block-Jacobi everywhere; 1 (default) ->
+ * aggregation-multigrid V-cycle (damped block-Jacobi smoothing, weight
+ * omega, nu sweeps) for the adjoint solves, block-Jacobi for the inexact
+ * Newton solves; 2 -> multigrid for both.  omega <= 0 or nu <= 0 keeps the
+ * current smoother. */
+int dp_scene_set_solver_options(dp_scene* s, int32_t use_mg, double omega, int32_t nu);
+/* multigrid hierarchy: number of levels and block rows per level (<= cap) */
+int dp_scene_get_mg_levels(const dp_scene* s, int32_t* n_levels, int32_t* rows, int32_t cap);
 /* per-element element weights w_e and host copies of vol (elasticity.py:67-71) */
 int dp_scene_get_element_data(const dp_scene* s, double* w_out, double* vol_out);
 /* BSR pattern of A: rowptr (V+1), col (nnzb) and values (nnzb*9, row-major

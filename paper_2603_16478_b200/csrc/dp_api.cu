@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -157,6 +158,9 @@ static int raise_status(int st) {
 using namespace dp;
 
 static const int g_debug = getenv("DP_DEBUG") ? atoi(getenv("DP_DEBUG")) : 0;
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 // ===========================================================================
 extern "C" {
@@ -492,6 +496,8 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   s->colliders.n = 0;
   cudaMemcpy(s->d_colliders, &s->colliders, sizeof(ColliderSet), cudaMemcpyHostToDevice);
   if (ensure_contact_capacity(s, 1) || contact_scan_setup(s)) { dp_scene_destroy(s); return DP_ERR_CUDA; }
+  if (mg_setup(s)) { dp_scene_destroy(s); return DP_ERR_CUDA; }
+  if (getenv("DP_MG")) s->use_mg = atoi(getenv("DP_MG"));
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { dp_scene_destroy(s); return cuda_fail(e, "scene create"); }
   *out = s;
@@ -502,6 +508,7 @@ int dp_scene_destroy(dp_scene* s) {
   if (!s) return DP_OK;
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
+  mg_destroy(s);
   void* ptrs[] = {s->ev, s->B, s->w, s->vol, s->mu, s->lam, s->model, s->mass, s->inc_ptr, s->inc,
                   s->slice_base, s->slice_width, s->col, s->diag_slot, s->val_fwd, s->val_adj, s->val_A,
                   s->contrib_ptr, s->contrib, s->minv, s->fe, s->H, s->Pst, s->d_colliders, s->b_ptr, s->b_idx,
@@ -617,6 +624,19 @@ int dp_scene_set_fext(dp_scene* s, const double* fext, int32_t ptr_kind) {
   }
   s->has_fext = 1;
   return copy_in(s, s->fext, fext, (size_t)3 * s->V, ptr_kind);
+}
+
+int dp_scene_set_solver_options(dp_scene* s, int32_t use_mg, double omega, int32_t nu) {
+  s->use_mg = use_mg;
+  if (omega > 0 && nu > 0) mg_set_params(s, omega, nu);
+  return DP_OK;
+}
+
+int dp_scene_get_mg_levels(const dp_scene* s, int32_t* n_levels, int32_t* rows, int32_t cap) {
+  const int L = mg_levels(s);
+  *n_levels = L;
+  for (int l = 0; l < L && l < cap; ++l) rows[l] = mg_level_rows(s, l);
+  return DP_OK;
 }
 
 int dp_scene_get_element_data(const dp_scene* s, double* w_out, double* vol_out) {
@@ -766,12 +786,14 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
   double* q_eval = s->q_ev;
   double last_t = 1.0;   // step length accepted by the previous line search
   for (int it = 0; it < cfg.max_iter; ++it) {
+    double t_it0 = g_debug ? now_s() : 0.0;
     k_reset_flags<<<1, 1, 0, s->stream>>>(s->esc);
     launch_detect(s, q);
     evaluate(s, q, s->r, 1);
     s->launches += 1;
     if ((rc = sync_esc(s))) return rc;
     const EvalScalars E = *s->h_esc;
+    if (g_debug) fprintf(stderr, "[dp]   detect+eval(jac) %.2fms\n", 1e3 * (now_s() - t_it0));
     if (it == 0) scale = std::max(1.0, E.scale_max);
     n_contacts = E.n_contacts;
     asym = E.asym;
@@ -794,21 +816,32 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     eta = std::min(eta_cap, std::max(cfg.lin_rtol_min, eta));
     int iters = 0, brk = 0;
     double relres = 0;
+    // multigrid pays off for tight solves (adjoint, 1e-10); the inexact
+    // Newton solves use it only when use_mg >= 2
+    const int mg = (s->mg != nullptr) && s->use_mg >= 2;
+    if (mg) mg_assemble(s, s->val_fwd);
+    double t_solve0 = 0;
+    if (g_debug) { cudaStreamSynchronize(s->stream); t_solve0 = now_s(); }
     if (!asym) {
-      rc = cg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk);
+      if (mg) rc = pcg_mg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk);
+      else rc = cg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk);
       R.krylov_iterations += iters;
       if (brk) {
         rc = gmres_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, cfg.gmres_restart, &iters, &relres,
-                         2.0);
+                         2.0, mg);
         R.krylov_iterations += iters;
       }
     } else {
-      rc = gmres_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, cfg.gmres_restart, &iters, &relres, 2.0);
+      rc = gmres_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, cfg.gmres_restart, &iters, &relres, 2.0,
+                       mg);
       R.krylov_iterations += iters;
     }
+    double t_ls0 = 0;
     if (g_debug) {
-      fprintf(stderr, "[dp] it=%d res=%.3e |r|2=%.3e C=%d asym=%d eta=%.1e krylov=%d relres=%.2e rc=%d\n", it, res, rn,
-              n_contacts, asym, eta, iters, relres, rc);
+      cudaStreamSynchronize(s->stream);
+      t_ls0 = now_s();
+      fprintf(stderr, "[dp] it=%d res=%.3e |r|2=%.3e C=%d asym=%d eta=%.1e krylov=%d relres=%.2e rc=%d solve=%.2fms\n",
+              it, res, rn, n_contacts, asym, eta, iters, relres, rc, 1e3 * (t_ls0 - t_solve0));
     }
     // line search (forward.py:214-234)
     double t = 1.0;
@@ -838,6 +871,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
       t *= 0.5;
     }
     last_t = accepted ? t : 0.0;
+    if (g_debug) fprintf(stderr, "[dp]   line search %.2fms\n", 1e3 * (now_s() - t_ls0));
     if (!accepted) {
       launch_axpy_to(s, q_try, q, t, s->dq);
       k_reset_flags<<<1, 1, 0, s->stream>>>(s->esc);
@@ -964,6 +998,7 @@ int dp_adjoint_assemble(dp_scene* s, const dp_cache* c, int32_t* symmetric) {
   if ((rc = sync_esc(s))) return rc;
   if ((rc = raise_status(s->h_esc->status & ~ST_PENETRATION))) return rc;
   s->last_sym_adj = c->asym ? 0 : 1;
+  s->mg_adj_ready = 0;   // the hierarchy is rebuilt lazily by the solve
   if (symmetric) *symmetric = s->last_sym_adj;
   g_adj_cache_tag = c;
   return DP_OK;
@@ -990,15 +1025,45 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
   if (method == DP_SOLVER_AUTO) method = sym ? DP_SOLVER_CG : DP_SOLVER_GMRES;
   int iters = 0, brk = 0;
   double relres = 0;
+  const int mg = (s->mg != nullptr) && s->use_mg;
+  if (mg && !s->mg_adj_ready) {
+    mg_assemble(s, s->val_adj);
+    s->mg_adj_ready = 1;
+  }
   if (method == DP_SOLVER_CG) {
-    rc = cg_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, &iters, &relres, &brk);
+    if (mg) rc = pcg_mg_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, &iters, &relres, &brk);
+    else rc = cg_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, &iters, &relres, &brk);
     if (brk) {
       int it2 = 0;
-      rc = gmres_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, cfg.gmres_restart, &it2, &relres);
+      rc = gmres_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, cfg.gmres_restart, &it2, &relres, 0.0,
+                       mg);
       iters += it2;
     }
   } else {
-    rc = gmres_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, cfg.gmres_restart, &iters, &relres);
+    rc = gmres_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, cfg.gmres_restart, &iters, &relres, 0.0, mg);
+  }
+  if (mg && !(relres <= cfg.tol) && iters < cfg.max_iter) {
+    // refinement: the multigrid-preconditioned solve stalled above the
+    // tolerance; solve the correction A d = b - A z with block-Jacobi GMRES
+    const int n3b = 3 * s->V;
+    const double bn = std::sqrt(device_norm2(s, s->rhs));
+    double* res = s->q_try;   // free during the adjoint
+    double* d = s->r_try;
+    launch_axpy_to(s, res, s->rhs, 0.0, s->rhs);
+    // res = b - A z
+    launch_spmv(s, s->val_adj, s->z, d);
+    launch_axpy_to(s, res, s->rhs, -1.0, d);
+    const double rn = std::sqrt(device_norm2(s, res));
+    int it2 = 0;
+    double rel2 = 1.0;
+    gmres_solve(s, s->val_adj, res, d, cfg.tol * bn / std::max(rn, 1e-300), cfg.max_iter - iters,
+                cfg.gmres_restart, &it2, &rel2, 0.0, 0);
+    launch_axpy_to(s, s->z, s->z, 1.0, d);
+    iters += it2;
+    launch_spmv(s, s->val_adj, s->z, d);
+    launch_axpy_to(s, res, s->rhs, -1.0, d);
+    relres = std::sqrt(device_norm2(s, res)) / bn;
+    (void)n3b;
   }
   if (g_debug) fprintf(stderr, "[dp] adjoint sym=%d iters=%d relres=%.2e\n", sym, iters, relres);
   if (rep) {

@@ -13,6 +13,12 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   return v;
 }
+// butterfly sum: every lane gets the total
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
@@ -77,6 +83,21 @@ __device__ __forceinline__ void fold_partials(const double* partial, int nb, dou
     if (threadIdx.x == 0) out[k] = v;
     __syncthreads();
   }
+}
+
+// In the last block: nv sums over nb partials (partial[b*stride + i]); warp w
+// folds values i = w, w + NT/32, ... with lanes striding over blocks, so the
+// loads of all values are in flight together.  out[] in shared memory.
+template <int NT>
+__device__ __forceinline__ void fold_multi(const double* partial, int stride, int nb, int nv, double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = warp; i < nv; i += NT / 32) {
+    double acc = 0.0;
+    for (int b = lane; b < nb; b += 32) acc += __ldcg(partial + (size_t)b * stride + i);
+    acc = warp_sum(acc);
+    if (lane == 0) out[i] = acc;
+  }
+  __syncthreads();
 }
 
 }  // namespace dp

@@ -10,6 +10,7 @@
 #include "../../include/diffproj_b200.h"
 
 namespace dp {
+struct MG;
 
 constexpr int kSlice = 32;          // SELL slice height (rows per warp)
 constexpr int kMaxColliders = 64;
@@ -47,6 +48,7 @@ struct GmresScalars {
   double nmb;                                   // |M^-1 b|
   double thr;                                   // stop when |g[j+1]| <= thr
   double est;                                   // |g[j+1]| / nmb
+  double reorth_thr;                            // re-orthogonalise when |w|^2 < thr |w_before|^2
   int done;                                     // 1 inner stop, 2 lucky breakdown
   int reorth;
   int used;
@@ -189,6 +191,11 @@ struct dp_scene {
 
   // last assembled operator: symmetric flag
   int last_sym_fwd = 1, last_sym_adj = 1;
+
+  // multigrid preconditioner (dp_mg.cu); nullptr = block-Jacobi only
+  dp::MG* mg = nullptr;
+  int use_mg = 1;
+  int mg_adj_ready = 0;
 };
 
 namespace dp {
@@ -218,7 +225,9 @@ void launch_spmv(dp_scene* s, const double* val, const double* x, double* y);
 int cg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
              int* iters, double* relres, int* breakdown);
 int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
-                int restart, int* iters, double* relres, double min_cycle_gain = 0.0);
+                int restart, int* iters, double* relres, double min_cycle_gain = 0.0, int use_mg = 0);
+int pcg_mg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int* iters,
+                 double* relres, int* breakdown);
 double device_norm2(dp_scene* s, const double* x);   // sum of squares, synchronous
 // vector ops
 void launch_axpy_to(dp_scene* s, double* out, const double* a, double t, const double* b);   // out = a + t*b
@@ -239,5 +248,14 @@ void launch_contacts(dp_scene* s, const double* q, const double* q_bar, int n_co
                      const int* vtx, const double* frame, const double* dn, const double* mu,
                      double* delta_out, int from_delta, int transpose, dp::EvalScalars* esc);
 int contact_scan_setup(dp_scene* s);
+
+// multigrid (dp_mg.cu)
+int mg_setup(dp_scene* s);
+void mg_destroy(dp_scene* s);
+void mg_assemble(dp_scene* s, const double* val);
+void mg_apply(dp_scene* s, const double* val, const double* r, double* z, const int* stop);
+int mg_levels(const dp_scene* s);
+int mg_level_rows(const dp_scene* s, int l);
+void mg_set_params(dp_scene* s, double omega, int nu);
 
 }  // namespace dp

@@ -877,20 +877,31 @@ __global__ void __launch_bounds__(256) k_gm_spmvdot(int V, int S, const int* __r
     }
   }
   const bool live = (gw < S) && (row < V);
-  for (int i = 0; i <= j + 1; ++i) {
-    double d = 0.0;
-    if (live) {
-      if (i < j) {
-        const double* vi = Vb + (size_t)i * ld + 3 * (size_t)row;
-        d = u[0] * vi[0] + u[1] * vi[1] + u[2] * vi[2];
-      } else if (i == j) {
-        d = u[0] * vr[0] + u[1] * vr[1] + u[2] * vr[2];
-      } else {
-        d = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+  // dots in groups of 8 basis vectors: the 8 row loads are independent, so
+  // their latencies overlap before the shuffle reductions
+  for (int i0 = 0; i0 <= j + 1; i0 += 8) {
+    double d[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int i = i0 + t;
+      double v = 0.0;
+      if (live && i <= j + 1) {
+        if (i < j) {
+          const double* vi = Vb + (size_t)i * ld + 3 * (size_t)row;
+          v = u[0] * vi[0] + u[1] * vi[1] + u[2] * vi[2];
+        } else if (i == j) {
+          v = u[0] * vr[0] + u[1] * vr[1] + u[2] * vr[2];
+        } else {
+          v = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+        }
       }
+      d[t] = v;
     }
-    d = warp_sum(d);
-    if (lane == 0) sh[warp][i] = d;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const double r = warp_sum(d[t]);
+      if (lane == 0 && i0 + t <= j + 1) sh[warp][i0 + t] = r;
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) {
@@ -900,19 +911,15 @@ __global__ void __launch_bounds__(256) k_gm_spmvdot(int V, int S, const int* __r
     partial[(size_t)blockIdx.x * (kGM1 + 1) + i] = t;
   }
   if (last_block(counter)) {
-    for (int i = 0; i <= j + 1; ++i) {
-      double acc = 0.0;
-      for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) acc += __ldcg(partial + (size_t)b * (kGM1 + 1) + i);
-      double t = block_sum<256>(acc, sred);
-      if (threadIdx.x == 0) {
-        if (i <= j) {
-          gs->coef[i] = t;
-          gs->H[(size_t)j * kGM1 + i] = t;
-        } else {
-          gs->wn2_before = t;
-        }
+    __shared__ double res[kGM1 + 1];
+    fold_multi<256>(partial, kGM1 + 1, gridDim.x, j + 2, res);
+    for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) {
+      if (i <= j) {
+        gs->coef[i] = res[i];
+        gs->H[(size_t)j * kGM1 + i] = res[i];
+      } else {
+        gs->wn2_before = res[i];
       }
-      __syncthreads();
     }
     if (threadIdx.x == 0) *counter = 0;
   }
@@ -922,45 +929,69 @@ __global__ void __launch_bounds__(256) k_gm_spmvdot(int V, int S, const int* __r
 // i <= j, one read of the basis; accumulators in register chunks of 8.
 __global__ void __launch_bounds__(kGT) k_gm_dots(int n, int j, const double* __restrict__ Vb, size_t ld,
                                                  const double* __restrict__ w, double* partial, unsigned int* counter,
-                                                 GmresScalars* gs) {
+                                                 GmresScalars* gs, int first) {
   __shared__ double sh[kGT / 32][kGM1 + 1];
   __shared__ double sred[32];
   if (ldflag(&gs->done)) return;
-  if (!ldflag(&gs->reorth)) return;
+  if (!first && !ldflag(&gs->reorth)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i0 = 0; i0 <= j; i0 += 8) {
+  const int nd = first ? j + 2 : j + 1;   // first pass also |w|^2
+  for (int i0 = 0; i0 < nd; i0 += 8) {
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int k = blockIdx.x * kGT + threadIdx.x; k < n; k += gridDim.x * kGT) {
       const double wk = w[k];
 #pragma unroll
       for (int t = 0; t < 8; ++t)
-        if (i0 + t <= j) acc[t] += wk * Vb[(size_t)(i0 + t) * ld + k];
+        if (i0 + t < nd) acc[t] += wk * ((i0 + t <= j) ? Vb[(size_t)(i0 + t) * ld + k] : wk);
     }
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const double d = warp_sum(acc[t]);
-      if (lane == 0 && i0 + t <= j) sh[warp][i0 + t] = d;
+      if (lane == 0 && i0 + t < nd) sh[warp][i0 + t] = d;
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i <= j; i += kGT) {
+  for (int i = threadIdx.x; i < nd; i += kGT) {
     double t = 0.0;
 #pragma unroll
     for (int ww = 0; ww < kGT / 32; ++ww) t += sh[ww][i];
     partial[(size_t)blockIdx.x * (kGM1 + 1) + i] = t;
   }
   if (last_block(counter)) {
-    for (int i = 0; i <= j; ++i) {
-      double acc = 0.0;
-      for (int b = threadIdx.x; b < (int)gridDim.x; b += kGT) acc += __ldcg(partial + (size_t)b * (kGM1 + 1) + i);
-      double t = block_sum<kGT>(acc, sred);
-      if (threadIdx.x == 0) {
-        gs->coef[i] = t;
-        gs->H[(size_t)j * kGM1 + i] += t;
+    __shared__ double res[kGM1 + 1];
+    fold_multi<kGT>(partial, kGM1 + 1, gridDim.x, nd, res);
+    for (int i = threadIdx.x; i < nd; i += kGT) {
+      if (i <= j) {
+        gs->coef[i] = res[i];
+        if (first) gs->H[(size_t)j * kGM1 + i] = res[i];
+        else gs->H[(size_t)j * kGM1 + i] += res[i];
+      } else {
+        gs->wn2_before = res[i];
       }
-      __syncthreads();
     }
     if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+// MG path, column kernel: v_j = w_prev / hn (own rows), t = A v_j
+__global__ void __launch_bounds__(256) k_gm_spmvnorm(int V, int S, const int* __restrict__ slice_base,
+                                                     const int* __restrict__ slice_width, const int* __restrict__ col,
+                                                     const double* __restrict__ val, const double* __restrict__ wprev,
+                                                     double* __restrict__ vj, double* __restrict__ t,
+                                                     const GmresScalars* gs) {
+  if (ldflag(&gs->done)) return;
+  const double inv = 1.0 / gs->hn;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (gw >= S) return;
+  double a[3];
+  spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, wprev, a);
+  const int row = gw * kSlice + lane;
+  if (row < V) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      vj[3 * row + c] = wprev[3 * row + c] * inv;
+      t[3 * row + c] = a[c] * inv;
+    }
   }
 }
 
@@ -1002,7 +1033,13 @@ __global__ void __launch_bounds__(kGT) k_gm_update(int n, int j, int pass, const
   double acc = 0.0;
   for (int k = blockIdx.x * kGT + threadIdx.x; k < n; k += gridDim.x * kGT) {
     double v = w[k];
-    for (int i = 0; i <= j; ++i) v -= coef[i] * Vb[(size_t)i * ld + k];
+    int i = 0;
+    for (; i + 4 <= j + 1; i += 4) {
+      const double a0 = Vb[(size_t)i * ld + k], a1 = Vb[(size_t)(i + 1) * ld + k];
+      const double a2 = Vb[(size_t)(i + 2) * ld + k], a3 = Vb[(size_t)(i + 3) * ld + k];
+      v -= coef[i] * a0 + coef[i + 1] * a1 + coef[i + 2] * a2 + coef[i + 3] * a3;
+    }
+    for (; i <= j; ++i) v -= coef[i] * Vb[(size_t)i * ld + k];
     w[k] = v;
     acc += v * v;
   }
@@ -1013,7 +1050,7 @@ __global__ void __launch_bounds__(kGT) k_gm_update(int n, int j, int pass, const
     if (threadIdx.x == 0) {
       *counter = 0;
       const double wn2 = out[0];
-      if (pass == 0 && wn2 < 0.25 * gs->wn2_before) {
+      if (pass == 0 && wn2 < gs->reorth_thr * gs->wn2_before) {
         gs->reorth = 1;
       } else {
         gs->reorth = 0;
@@ -1039,8 +1076,8 @@ __global__ void __launch_bounds__(kVT) k_gm_start(int V, const double* __restric
   const int i = blockIdx.x * kVT + threadIdx.x;
   double acc = 0.0;
   if (i < V) {
-    double rv[3] = {r[3 * i], r[3 * i + 1], r[3 * i + 2]}, u[3];
-    minv_apply(minv, V, i, rv, u);
+    double rv[3] = {r[3 * i], r[3 * i + 1], r[3 * i + 2]}, u[3] = {rv[0], rv[1], rv[2]};
+    if (minv) minv_apply(minv, V, i, rv, u);
 #pragma unroll
     for (int c = 0; c < 3; ++c) { v0[3 * i + c] = u[c]; acc += u[c] * u[c]; }
   }
@@ -1061,6 +1098,9 @@ __global__ void __launch_bounds__(kVT) k_gm_start(int V, const double* __restric
         gs->thr = 0.1 * tol * gs->nmb;
         gs->done = (beta == 0.0) ? 2 : 0;
         gs->reorth = 0;
+        // tight solves (adjoint, 1e-10) need CGS2-level orthogonality; the
+        // inexact Newton solves only re-orthogonalise on severe cancellation
+        gs->reorth_thr = (tol < 1e-7) ? 0.25 : 1e-4;
         gs->used = 0;
         gs->est = beta / gs->nmb;
       }
@@ -1086,7 +1126,7 @@ static int gm_grid(int n) {
 // Restarted GMRES on A x = b (true relative residual <= rtol).  x is
 // overwritten (zero initial guess).  Returns 0 converged, 1 not converged.
 int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int restart,
-                int* iters, double* relres, double min_cycle_gain) {
+                int* iters, double* relres, double min_cycle_gain, int use_mg) {
   const int V = s->V, n = 3 * V;
   if (restart > kMaxRestart) restart = kMaxRestart;
   if (restart > n) restart = n;
@@ -1103,7 +1143,12 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   const double bnorm = sqrt(device_norm2(s, b));
   if (bnorm == 0.0) { *relres = 0.0; return 0; }
   // |M^-1 b|
-  k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, b, s->kw, s->red.partial, s->red.counter, s->gsc, rtol, 1);
+  if (use_mg) {
+    mg_apply(s, val, b, s->ku, nullptr);
+    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, nullptr, s->ku, s->kw, s->red.partial, s->red.counter, s->gsc, rtol, 1);
+  } else {
+    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, b, s->kw, s->red.partial, s->red.counter, s->gsc, rtol, 1);
+  }
   s->launches++;
   int total = 0;
   double rel = 1.0;
@@ -1112,7 +1157,12 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
     if (rel <= rtol) break;
     const double cycle_start = rel;
     double* Wb[2] = {s->kw, s->kp};   // double-buffered unnormalised basis vector
-    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, r, Wb[0], s->red.partial, s->red.counter, s->gsc, rtol, 0);
+    if (use_mg) {
+      mg_apply(s, val, r, s->ku, nullptr);
+      k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, nullptr, s->ku, Wb[0], s->red.partial, s->red.counter, s->gsc, rtol, 0);
+    } else {
+      k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, r, Wb[0], s->red.partial, s->red.counter, s->gsc, rtol, 0);
+    }
     s->launches++;
     int j = 0;
     bool stop = false;
@@ -1123,11 +1173,20 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
       for (int c = 0; c < chunk; ++c, ++j) {
         double* wp = Wb[j & 1];
         double* wn = Wb[(j + 1) & 1];
-        k_gm_spmvdot<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, s->minv, wp,
-                                                 Vb + (size_t)j * ld, wn, Vb, ld, j, s->red.partial, s->red.counter,
-                                                 s->gsc);
+        if (use_mg) {
+          // v_j = w/hn, t = A v_j ; w = B t (V-cycle) ; coef = V^T w, |w|^2
+          k_gm_spmvnorm<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, wp,
+                                                    Vb + (size_t)j * ld, s->ku, s->gsc);
+          mg_apply(s, val, s->ku, wn, &s->gsc->done);
+          k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc, 1);
+          s->launches += 2;
+        } else {
+          k_gm_spmvdot<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, s->minv,
+                                                   wp, Vb + (size_t)j * ld, wn, Vb, ld, j, s->red.partial,
+                                                   s->red.counter, s->gsc);
+        }
         k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, j, 0, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc);
-        k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc);
+        k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc, 0);
         k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, j, 1, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc);
         s->launches += 4;
       }
@@ -1159,6 +1218,198 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
     // means GMRES(m) is stagnating; return the best iterate so far
     if (min_cycle_gain > 0.0 && rel > cycle_start / min_cycle_gain) break;
     if (used == 0) break;
+  }
+  *relres = rel;
+  return rel <= rtol ? 0 : 1;
+}
+
+// ---------------------------------------------------------------------------
+// PCG with the multigrid V-cycle as preconditioner (symmetric operators).
+// Device-resident scalars; the host only polls `done` every few iterations.
+
+// x = 0, r = b, rho = |b|^2 (tolerances)
+__global__ void __launch_bounds__(kVT) k_pcg_init(int V, const double* __restrict__ b, double* x, double* r, double* p,
+                                                  double rtol, double* partial, unsigned int* counter,
+                                                  KrylovScalars* ks) {
+  __shared__ double sh[32];
+  __shared__ double out[1];
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  double acc = 0.0;
+  if (i < V) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double v = b[3 * i + c];
+      x[3 * i + c] = 0.0; p[3 * i + c] = 0.0; r[3 * i + c] = v;
+      acc += v * v;
+    }
+  }
+  double t = block_sum<kVT>(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    fold_partials<kVT, 1>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) {
+      ks->bnorm2 = out[0];
+      ks->rho = out[0];
+      ks->tol2 = rtol * rtol * out[0];
+      ks->gamma = 0.0; ks->beta = 0.0; ks->alpha = 0.0;
+      ks->iters = 0;
+      ks->done = (out[0] == 0.0) ? 1 : 0;
+      *counter = 0;
+    }
+  }
+}
+
+// gamma' = (r, z); beta = gamma'/gamma (0 on the first iteration); p = z + beta p
+// is applied by k_pcg_spmv on the fly (it owns the p rows it writes)
+__global__ void __launch_bounds__(kVT) k_pcg_rz(int V, const double* __restrict__ r, const double* __restrict__ z,
+                                                double* partial, unsigned int* counter, KrylovScalars* ks) {
+  __shared__ double sh[32];
+  __shared__ double out[1];
+  if (ldflag(&ks->done)) return;
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  double acc = 0.0;
+  if (i < V) acc = r[3 * i] * z[3 * i] + r[3 * i + 1] * z[3 * i + 1] + r[3 * i + 2] * z[3 * i + 2];
+  double t = block_sum<kVT>(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    fold_partials<kVT, 1>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) {
+      const double g = out[0];
+      ks->beta = (ks->iters == 0) ? 0.0 : g / ks->gamma;
+      ks->gamma = g;
+      if (!(g > 0.0)) ks->done = 2;     // preconditioner not SPD on this residual
+      *counter = 0;
+    }
+  }
+}
+
+// p = z + beta p (per row) ; q = A p ; delta = (p, q); alpha = gamma / delta
+__global__ void __launch_bounds__(kVT) k_pcg_p(int V, const double* __restrict__ z, double* __restrict__ p,
+                                               const KrylovScalars* ks) {
+  if (ldflag(&ks->done)) return;
+  const double beta = ks->beta;
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  if (i >= V) return;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) p[3 * i + c] = z[3 * i + c] + beta * p[3 * i + c];
+}
+
+__global__ void __launch_bounds__(256) k_pcg_spmv(int V, int S, const int* __restrict__ slice_base,
+                                                  const int* __restrict__ slice_width, const int* __restrict__ col,
+                                                  const double* __restrict__ val, const double* __restrict__ p,
+                                                  double* __restrict__ q, double* partial, unsigned int* counter,
+                                                  KrylovScalars* ks) {
+  __shared__ double sh[32];
+  __shared__ double out[1];
+  if (ldflag(&ks->done)) return;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  double pq = 0.0;
+  if (gw < S) {
+    double a[3];
+    spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, p, a);
+    const int row = gw * kSlice + lane;
+    if (row < V) {
+      q[3 * row] = a[0]; q[3 * row + 1] = a[1]; q[3 * row + 2] = a[2];
+      pq = a[0] * p[3 * row] + a[1] * p[3 * row + 1] + a[2] * p[3 * row + 2];
+    }
+  }
+  double t = block_sum<256>(pq, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    fold_partials<256, 1>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) {
+      if (!(out[0] > 0.0)) ks->done = 2;   // p^T A p <= 0 (linsolve.py:89-91)
+      else ks->alpha = ks->gamma / out[0];
+      ks->delta = out[0];
+      *counter = 0;
+    }
+  }
+}
+
+// x += alpha p ; r -= alpha q ; rho = |r|^2 ; done when rho <= tol^2 |b|^2
+__global__ void __launch_bounds__(kVT) k_pcg_xr(int V, double* x, double* r, const double* __restrict__ p,
+                                                const double* __restrict__ q, double* partial, unsigned int* counter,
+                                                KrylovScalars* ks) {
+  __shared__ double sh[32];
+  __shared__ double out[1];
+  if (ldflag(&ks->done)) return;
+  const double alpha = ks->alpha;
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  double acc = 0.0;
+  if (i < V) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int k = 3 * i + c;
+      x[k] += alpha * p[k];
+      const double v = r[k] - alpha * q[k];
+      r[k] = v;
+      acc += v * v;
+    }
+  }
+  double t = block_sum<kVT>(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    fold_partials<kVT, 1>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) {
+      ks->rho = out[0];
+      ks->iters += 1;
+      if (out[0] <= ks->tol2) ks->done = 1;
+      *counter = 0;
+    }
+  }
+}
+
+int pcg_mg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int* iters,
+                 double* relres, int* breakdown) {
+  const int V = s->V, n = 3 * V;
+  const int nbv = grid_for(V, kVT);
+  const int nbs = grid_for((int64_t)s->S * 32, 256);
+  *iters = 0;
+  *breakdown = 0;
+  double bnorm = sqrt(device_norm2(s, b));
+  if (bnorm == 0.0) {
+    cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+    *relres = 0.0;
+    return 0;
+  }
+  double* bb = s->tmp;     // rhs of the current correction solve
+  double* xc = s->kx;
+  double *r = s->kr, *z = s->ku, *p = s->kp, *q = s->kw;
+  cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+  cudaMemcpyAsync(bb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s->stream);
+  double rel = 1.0;
+  for (int restart = 0; restart < 4; ++restart) {
+    double inner = rtol / rel * 0.5;
+    inner = fmin(0.5, fmax(inner, 1e-15));
+    k_pcg_init<<<nbv, kVT, 0, s->stream>>>(V, bb, xc, r, p, inner, s->red.partial, s->red.counter, s->ksc);
+    s->launches++;
+    int done = 0, launched = 0, chunk = 4;
+    while (!done && *iters + launched < max_iter) {
+      int m = chunk;
+      if (*iters + launched + m > max_iter) m = max_iter - *iters - launched;
+      for (int k = 0; k < m; ++k) {
+        mg_apply(s, val, r, z, &s->ksc->done);
+        k_pcg_rz<<<nbv, kVT, 0, s->stream>>>(V, r, z, s->red.partial, s->red.counter, s->ksc);
+        k_pcg_p<<<nbv, kVT, 0, s->stream>>>(V, z, p, s->ksc);
+        k_pcg_spmv<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, p, q,
+                                               s->red.partial, s->red.counter, s->ksc);
+        k_pcg_xr<<<nbv, kVT, 0, s->stream>>>(V, xc, r, p, q, s->red.partial, s->red.counter, s->ksc);
+        s->launches += 4;
+      }
+      launched += m;
+      read_ksc(s);
+      done = s->h_ksc->done;
+      if (chunk < 16) chunk *= 2;
+    }
+    *iters += s->h_ksc->iters;
+    launch_axpy_to(s, x, x, 1.0, xc);
+    if (s->h_ksc->done == 2) {
+      *breakdown = 1;
+      *relres = true_relres(s, val, b, x, s->tmp, bnorm);
+      return 2;
+    }
+    rel = true_relres(s, val, b, x, bb, bnorm);
+    if (rel <= rtol || *iters >= max_iter) break;
   }
   *relres = rel;
   return rel <= rtol ? 0 : 1;

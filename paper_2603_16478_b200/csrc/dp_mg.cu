@@ -1,0 +1,628 @@
+// Aggregation multigrid preconditioner for the 3x3-block Newton / adjoint
+// operators ("stronger preconditioners"; the
+// reference offers sparse-inverse / Woodbury, linsolve.py:230-336, which the
+// adjoint never calls).  B200-first design:
+//
+//  * setup (host, once per scene): greedy vertex aggregation of the block
+//    graph, level by level, until <= kCoarseMax block rows; per level a
+//    SELL-32 pattern, and a *Galerkin gather list* per coarse slot: the
+//    fine SELL value addresses whose blocks sum into it (unsmoothed
+//    aggregation, P = piecewise-constant 3x3 identity per aggregate, so
+//    A_c = P^T A P is a pure block sum - no SpGEMM).
+//  * per operator (every Newton iteration / adjoint step): one gather kernel
+//    per level (deterministic, no atomics) + block-Jacobi inverses; the
+//    coarsest operator is inverted densely in one CTA (Gauss-Jordan).
+//  * apply (V-cycle): damped block-Jacobi pre/post smoothing, residual,
+//    restriction (member gather), prolongation fused into the post-smoother's
+//    SpMV gathers.  Symmetric for symmetric A (CG-safe).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "dp_common.cuh"
+#include "dp_internal.h"
+
+namespace dp {
+
+constexpr int kCoarseMax = 36;      // dense coarsest solve (<= 108 unknowns, shared memory)
+constexpr int kDenseSmem = 108;
+__global__ void k_mg_dense_invert(int N, const double* __restrict__ Ag, double* __restrict__ Ainv);
+
+struct MGLevel {
+  int n = 0, S = 0;
+  int64_t NS = 0;
+  int *slice_base = nullptr, *slice_width = nullptr, *col = nullptr, *diag_slot = nullptr;
+  double *val = nullptr, *minv = nullptr;
+  int *gal_ptr = nullptr, *gal = nullptr;      // coarse slot -> fine value addresses
+  int *mem_ptr = nullptr, *mem = nullptr;      // coarse row -> fine rows
+  int* agg = nullptr;                          // fine row -> coarse row (owned by the coarse level)
+  int* slot_row = nullptr;                     // SELL slot -> block row
+  double *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr, *u = nullptr;
+};
+
+struct MG {
+  std::vector<MGLevel> lv;   // lv[0] = fine level (aliases the scene's SELL arrays)
+  double* dense = nullptr;   // coarsest dense operator (N x N), N = 3 n_coarsest
+  double* dinv = nullptr;    // its inverse
+  int N = 0;
+  double omega = 0.6;
+  int nu = 1;
+  size_t bytes = 0;
+};
+
+// ---------------------------------------------------------------------------
+// host setup
+
+struct HostPattern {
+  int n = 0;
+  std::vector<int> rowptr, col;
+};
+
+static void sell_layout(const HostPattern& P, std::vector<int>& slice_base, std::vector<int>& slice_width,
+                        std::vector<int>& col, std::vector<int>& diag_slot, std::vector<int64_t>& slot_of) {
+  const int n = P.n, S = (n + kSlice - 1) / kSlice;
+  slice_base.assign(S + 1, 0);
+  slice_width.assign(S, 0);
+  for (int sl = 0; sl < S; ++sl) {
+    int K = 0;
+    for (int l = 0; l < kSlice; ++l) {
+      const int row = sl * kSlice + l;
+      if (row < n) K = std::max(K, P.rowptr[row + 1] - P.rowptr[row]);
+    }
+    slice_width[sl] = K;
+    slice_base[sl + 1] = slice_base[sl] + K * kSlice;
+  }
+  col.assign(slice_base[S], 0);
+  diag_slot.assign(n, 0);
+  slot_of.assign(P.col.size(), 0);
+  for (int i = 0; i < n; ++i) {
+    const int sl = i / kSlice, l = i % kSlice;
+    for (int k = P.rowptr[i]; k < P.rowptr[i + 1]; ++k) {
+      const int64_t slot = slice_base[sl] + (int64_t)(k - P.rowptr[i]) * kSlice + l;
+      col[slot] = P.col[k];
+      slot_of[k] = slot;
+      if (P.col[k] == i) diag_slot[i] = (int)slot;
+    }
+  }
+}
+
+// greedy aggregation (standard two-phase): returns #aggregates, agg[i]
+static int aggregate(const HostPattern& P, std::vector<int>& agg) {
+  const int n = P.n;
+  agg.assign(n, -1);
+  int na = 0;
+  for (int i = 0; i < n; ++i) {
+    if (agg[i] >= 0) continue;
+    bool free_nbhd = true;
+    for (int k = P.rowptr[i]; k < P.rowptr[i + 1]; ++k)
+      if (agg[P.col[k]] >= 0) { free_nbhd = false; break; }
+    if (!free_nbhd) continue;
+    for (int k = P.rowptr[i]; k < P.rowptr[i + 1]; ++k) agg[P.col[k]] = na;
+    agg[i] = na;
+    ++na;
+  }
+  // phase 2: attach leftovers to the neighbouring aggregate they touch most
+  std::vector<int> tmp = agg;
+  for (int i = 0; i < n; ++i) {
+    if (agg[i] >= 0) continue;
+    int best = -1, bestc = 0;
+    for (int k = P.rowptr[i]; k < P.rowptr[i + 1]; ++k) {
+      const int a = agg[P.col[k]];
+      if (a < 0) continue;
+      int c = 0;
+      for (int k2 = P.rowptr[i]; k2 < P.rowptr[i + 1]; ++k2) c += (agg[P.col[k2]] == a);
+      if (c > bestc) { bestc = c; best = a; }
+    }
+    tmp[i] = best;
+  }
+  agg = tmp;
+  for (int i = 0; i < n; ++i)
+    if (agg[i] < 0) {
+      agg[i] = na++;
+      for (int k = P.rowptr[i]; k < P.rowptr[i + 1]; ++k)
+        if (agg[P.col[k]] < 0) agg[P.col[k]] = agg[i];
+    }
+  return na;
+}
+
+template <class T>
+static int up(MG* mg, T** p, const std::vector<T>& h) {
+  const size_t n = std::max<size_t>(h.size(), 1);
+  DP_CUDA(cudaMalloc((void**)p, n * sizeof(T)));
+  mg->bytes += n * sizeof(T);
+  if (!h.empty()) DP_CUDA(cudaMemcpy(*p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return 0;
+}
+template <class T>
+static int al(MG* mg, T** p, size_t n) {
+  n = std::max<size_t>(n, 1);
+  DP_CUDA(cudaMalloc((void**)p, n * sizeof(T)));
+  mg->bytes += n * sizeof(T);
+  DP_CUDA(cudaMemset(*p, 0, n * sizeof(T)));
+  return 0;
+}
+
+int mg_setup(dp_scene* s) {
+  MG* mg = new MG();
+  HostPattern fine;
+  fine.n = s->V;
+  fine.rowptr = s->h_rowptr;
+  fine.col = s->h_colidx;
+  // fine level aliases the scene's SELL storage
+  MGLevel L0;
+  L0.n = s->V;
+  L0.S = s->S;
+  L0.NS = s->NS;
+  L0.slice_base = s->slice_base;
+  L0.slice_width = s->slice_width;
+  L0.col = s->col;
+  L0.diag_slot = s->diag_slot;
+  L0.minv = s->minv;
+  int rc = 0;
+  rc |= al(mg, &L0.x, (size_t)3 * s->V);
+  rc |= al(mg, &L0.r, (size_t)3 * s->V);
+  rc |= al(mg, &L0.t, (size_t)3 * s->V);
+  rc |= al(mg, &L0.u, (size_t)3 * s->V);
+  mg->lv.push_back(L0);
+  // fine SELL addresses of every CSR block
+  std::vector<int64_t> fine_addr(s->nnzb);
+  for (int i = 0; i < s->V; ++i) {
+    const int lane = i % kSlice;
+    for (int k = s->h_rowptr[i]; k < s->h_rowptr[i + 1]; ++k) {
+      const int64_t rel = k - s->h_rowptr[i];
+      const int64_t base_s = s->h_block_slot[k] - rel * kSlice - lane;
+      fine_addr[k] = base_s * 9 + rel * 9 * kSlice + lane;
+    }
+  }
+  HostPattern cur = fine;
+  std::vector<int64_t> cur_addr = fine_addr;
+  while (cur.n > kCoarseMax && !rc) {
+    std::vector<int> agg;
+    const int na = aggregate(cur, agg);
+    if (na >= cur.n || na < 1 || (double)cur.n / na < 1.5) break;
+    // coarse pattern
+    HostPattern C;
+    C.n = na;
+    std::vector<std::vector<int>> rows(na);
+    for (int i = 0; i < cur.n; ++i)
+      for (int k = cur.rowptr[i]; k < cur.rowptr[i + 1]; ++k) rows[agg[i]].push_back(agg[cur.col[k]]);
+    C.rowptr.assign(na + 1, 0);
+    for (int I = 0; I < na; ++I) {
+      auto& r = rows[I];
+      std::sort(r.begin(), r.end());
+      r.erase(std::unique(r.begin(), r.end()), r.end());
+      C.rowptr[I + 1] = C.rowptr[I] + (int)r.size();
+    }
+    C.col.reserve(C.rowptr[na]);
+    for (int I = 0; I < na; ++I) C.col.insert(C.col.end(), rows[I].begin(), rows[I].end());
+    std::vector<int> sb, sw, cc, ds;
+    std::vector<int64_t> slot_of;
+    sell_layout(C, sb, sw, cc, ds, slot_of);
+    const int64_t NS = sb.back();
+    // Galerkin gather lists: coarse slot <- fine blocks (i,j) with agg(i)=I, agg(j)=J
+    std::vector<int> gcount(NS + 1, 0);
+    std::vector<int64_t> fslot(cur.col.size());
+    for (int i = 0; i < cur.n; ++i) {
+      const int I = agg[i];
+      const int* rb = C.col.data() + C.rowptr[I];
+      const int rl = C.rowptr[I + 1] - C.rowptr[I];
+      for (int k = cur.rowptr[i]; k < cur.rowptr[i + 1]; ++k) {
+        const int J = agg[cur.col[k]];
+        const int kk = (int)(std::lower_bound(rb, rb + rl, J) - rb);
+        const int64_t cs = slot_of[C.rowptr[I] + kk];
+        fslot[k] = cs;
+        gcount[cs + 1]++;
+      }
+    }
+    for (int64_t t = 0; t < NS; ++t) gcount[t + 1] += gcount[t];
+    std::vector<int> gal(gcount[NS]);
+    {
+      std::vector<int> fill(gcount.begin(), gcount.end() - 1);
+      for (size_t k = 0; k < cur.col.size(); ++k) gal[fill[fslot[k]]++] = (int)cur_addr[k];
+    }
+    std::vector<int> mptr(na + 1, 0), mem(cur.n);
+    for (int i = 0; i < cur.n; ++i) mptr[agg[i] + 1]++;
+    for (int I = 0; I < na; ++I) mptr[I + 1] += mptr[I];
+    {
+      std::vector<int> fill(mptr.begin(), mptr.end() - 1);
+      for (int i = 0; i < cur.n; ++i) mem[fill[agg[i]]++] = i;
+    }
+    MGLevel L;
+    L.n = na;
+    L.S = (na + kSlice - 1) / kSlice;
+    L.NS = NS;
+    rc |= up(mg, &L.slice_base, sb);
+    rc |= up(mg, &L.slice_width, sw);
+    rc |= up(mg, &L.col, cc);
+    rc |= up(mg, &L.diag_slot, ds);
+    rc |= al(mg, &L.val, (size_t)NS * 9);
+    rc |= al(mg, &L.minv, (size_t)na * 9);
+    rc |= up(mg, &L.gal_ptr, gcount);
+    rc |= up(mg, &L.gal, gal);
+    rc |= up(mg, &L.mem_ptr, mptr);
+    rc |= up(mg, &L.mem, mem);
+    rc |= up(mg, &L.agg, agg);
+    {
+      std::vector<int> srow(NS);
+      for (int64_t t = 0; t < NS; ++t) {
+        const int64_t sl = std::upper_bound(sb.begin(), sb.end(), (int)t) - sb.begin() - 1;
+        srow[t] = (int)(sl * kSlice + (t - sb[sl]) % kSlice);
+      }
+      rc |= up(mg, &L.slot_row, srow);
+    }
+    rc |= al(mg, &L.x, (size_t)3 * na);
+    rc |= al(mg, &L.b, (size_t)3 * na);
+    rc |= al(mg, &L.r, (size_t)3 * na);
+    rc |= al(mg, &L.t, (size_t)3 * na);
+    rc |= al(mg, &L.u, (size_t)3 * na);
+    mg->lv.push_back(L);
+    // next level's address list: coarse CSR block k -> its SELL value address
+    std::vector<int64_t> caddr(C.col.size());
+    for (int I = 0; I < na; ++I) {
+      const int lane = I % kSlice;
+      for (int k = C.rowptr[I]; k < C.rowptr[I + 1]; ++k) {
+        const int64_t rel = k - C.rowptr[I];
+        const int64_t base_s = slot_of[k] - rel * kSlice - lane;
+        caddr[k] = base_s * 9 + rel * 9 * kSlice + lane;
+      }
+    }
+    cur = C;
+    cur_addr = caddr;
+  }
+  if (rc) { delete mg; return rc; }
+  const MGLevel& Lc = mg->lv.back();
+  mg->N = 3 * Lc.n;
+  if (mg->lv.size() < 2 || mg->N > kDenseSmem) {
+    // no useful hierarchy (tiny or unaggregatable graph): disable
+    delete mg;
+    s->mg = nullptr;
+    return 0;
+  }
+  cudaFuncSetAttribute(k_mg_dense_invert, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(2 * kDenseSmem * kDenseSmem * sizeof(double)));
+  rc |= al(mg, &mg->dense, (size_t)mg->N * mg->N);
+  rc |= al(mg, &mg->dinv, (size_t)mg->N * mg->N);
+  if (rc) { delete mg; return rc; }
+  if (getenv("DP_MG_OMEGA")) mg->omega = atof(getenv("DP_MG_OMEGA"));
+  if (getenv("DP_MG_NU")) mg->nu = atoi(getenv("DP_MG_NU"));
+  s->mg = mg;
+  s->bytes += mg->bytes;
+  return 0;
+}
+
+void mg_destroy(dp_scene* s) {
+  MG* mg = s->mg;
+  if (!mg) return;
+  for (size_t l = 0; l < mg->lv.size(); ++l) {
+    MGLevel& L = mg->lv[l];
+    void* own[] = {L.x, L.r, L.t, L.u, L.b};
+    for (void* p : own) if (p) cudaFree(p);
+    if (l > 0) {
+      void* p2[] = {L.slice_base, L.slice_width, L.col, L.diag_slot, L.val, L.minv, L.gal_ptr, L.gal,
+                    L.mem_ptr, L.mem, L.agg, L.slot_row};
+      for (void* p : p2) if (p) cudaFree(p);
+    }
+  }
+  if (mg->dense) cudaFree(mg->dense);
+  if (mg->dinv) cudaFree(mg->dinv);
+  delete mg;
+  s->mg = nullptr;
+}
+
+int mg_levels(const dp_scene* s) { return s->mg ? (int)s->mg->lv.size() : 0; }
+int mg_level_rows(const dp_scene* s, int l) { return s->mg ? s->mg->lv[l].n : 0; }
+void mg_set_params(dp_scene* s, double omega, int nu) {
+  if (s->mg) { s->mg->omega = omega; s->mg->nu = nu; }
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+
+__device__ __forceinline__ void inv3(const double a[9], double o[9]) {
+  const double c00 = a[4] * a[8] - a[5] * a[7];
+  const double c01 = a[5] * a[6] - a[3] * a[8];
+  const double c02 = a[3] * a[7] - a[4] * a[6];
+  const double det = a[0] * c00 + a[1] * c01 + a[2] * c02;
+  const double id = 1.0 / det;
+  o[0] = c00 * id;
+  o[1] = (a[2] * a[7] - a[1] * a[8]) * id;
+  o[2] = (a[1] * a[5] - a[2] * a[4]) * id;
+  o[3] = c01 * id;
+  o[4] = (a[0] * a[8] - a[2] * a[6]) * id;
+  o[5] = (a[2] * a[3] - a[0] * a[5]) * id;
+  o[6] = c02 * id;
+  o[7] = (a[1] * a[6] - a[0] * a[7]) * id;
+  o[8] = (a[0] * a[4] - a[1] * a[3]) * id;
+}
+
+// coarse operator: val_c[slot] = sum of the fine blocks in its gather list
+// (one warp per coarse slot, lanes over contributions); block-Jacobi inverse
+// of the diagonal slots.
+__global__ void __launch_bounds__(256) k_mg_galerkin(int n, int S, const int* __restrict__ slice_base,
+                                                     const int* __restrict__ slice_width,
+                                                     const int* __restrict__ diag_slot,
+                                                     const int* __restrict__ gal_ptr, const int* __restrict__ gal,
+                                                     const double* __restrict__ valf, double* __restrict__ valc,
+                                                     double* __restrict__ minv, const int* __restrict__ slot_row,
+                                                     int64_t NS) {
+  const int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (slot >= NS) return;
+  double b[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int t = gal_ptr[slot] + lane; t < gal_ptr[slot + 1]; t += 32) {
+    const double* src = valf + gal[t];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) b[c] += src[c * kSlice];
+  }
+#pragma unroll
+  for (int c = 0; c < 9; ++c) b[c] = warp_allsum(b[c]);
+  // slot -> (slice, k, lane)
+  const int row = slot_row[slot];
+  const int sl = row / kSlice, ln = row % kSlice;
+  const int base = slice_base[sl];
+  const int k = (int)((slot - base - ln) / kSlice);
+  if (lane < 9) {
+    double v = 0.0;
+#pragma unroll
+    for (int c = 0; c < 9; ++c) v = (lane == c) ? b[c] : v;
+    valc[(size_t)base * 9 + (k * 9 + lane) * kSlice + ln] = v;
+  }
+  if (lane == 0 && row < n && slot == diag_slot[row]) {
+    double o[9];
+    inv3(b, o);
+#pragma unroll
+    for (int c = 0; c < 9; ++c) minv[(size_t)c * n + row] = o[c];
+  }
+}
+
+__device__ __forceinline__ void mv_minv(const double* __restrict__ minv, int n, int i, const double r[3], double u[3]) {
+  u[0] = minv[0 * (size_t)n + i] * r[0] + minv[1 * (size_t)n + i] * r[1] + minv[2 * (size_t)n + i] * r[2];
+  u[1] = minv[3 * (size_t)n + i] * r[0] + minv[4 * (size_t)n + i] * r[1] + minv[5 * (size_t)n + i] * r[2];
+  u[2] = minv[6 * (size_t)n + i] * r[0] + minv[7 * (size_t)n + i] * r[1] + minv[8 * (size_t)n + i] * r[2];
+}
+
+// x = omega Minv b
+__device__ __forceinline__ bool stopped(const int* stop) { return stop && *(volatile const int*)stop; }
+
+__global__ void k_mg_jacobi0(int n, const double* __restrict__ minv, const double* __restrict__ b, double omega,
+                             double* __restrict__ x, const int* stop) {
+  if (stopped(stop)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double r[3] = {b[3 * i], b[3 * i + 1], b[3 * i + 2]};
+  double u[3];
+  mv_minv(minv, n, i, r, u);
+  x[3 * i] = omega * u[0]; x[3 * i + 1] = omega * u[1]; x[3 * i + 2] = omega * u[2];
+}
+
+// out = xt + omega Minv (b - A xt), xt = x + P xc (xc/agg may be null)
+// and optionally r_out = b - A xt (for the residual after the last pre-sweep)
+__global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __restrict__ slice_base,
+                                                   const int* __restrict__ slice_width, const int* __restrict__ col,
+                                                   const double* __restrict__ val, const double* __restrict__ minv,
+                                                   const double* __restrict__ b, const double* __restrict__ x,
+                                                   const double* __restrict__ xc, const int* __restrict__ agg,
+                                                   double omega, double* __restrict__ out, double* __restrict__ r_out,
+                                                   const int* stop) {
+  if (stopped(stop)) return;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= S) return;
+  const int row = gw * kSlice + lane;
+  const int base = slice_base[gw], K = slice_width[gw];
+  const double* vs = val + (size_t)base * 9 + lane;
+  const int* cs = col + base + lane;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const int j = __ldg(cs + k * kSlice);
+    const double* v = vs + k * 9 * kSlice;
+    double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
+    if (xc) {
+      const int J = __ldg(agg + j);
+      x0 += __ldg(xc + 3 * J); x1 += __ldg(xc + 3 * J + 1); x2 += __ldg(xc + 3 * J + 2);
+    }
+    a0 += v[0 * kSlice] * x0 + v[1 * kSlice] * x1 + v[2 * kSlice] * x2;
+    a1 += v[3 * kSlice] * x0 + v[4 * kSlice] * x1 + v[5 * kSlice] * x2;
+    a2 += v[6 * kSlice] * x0 + v[7 * kSlice] * x1 + v[8 * kSlice] * x2;
+  }
+  if (row >= n) return;
+  double xt[3] = {x[3 * row], x[3 * row + 1], x[3 * row + 2]};
+  if (xc) {
+    const int I = agg[row];
+    xt[0] += xc[3 * I]; xt[1] += xc[3 * I + 1]; xt[2] += xc[3 * I + 2];
+  }
+  const double rr[3] = {b[3 * row] - a0, b[3 * row + 1] - a1, b[3 * row + 2] - a2};
+  if (r_out) { r_out[3 * row] = rr[0]; r_out[3 * row + 1] = rr[1]; r_out[3 * row + 2] = rr[2]; }
+  if (out) {
+    double u[3];
+    mv_minv(minv, n, row, rr, u);
+    out[3 * row] = xt[0] + omega * u[0];
+    out[3 * row + 1] = xt[1] + omega * u[1];
+    out[3 * row + 2] = xt[2] + omega * u[2];
+  }
+}
+
+// b_c[I] = sum over members of r_f (one warp per coarse row)
+__global__ void k_mg_restrict(int nc, const int* __restrict__ mptr, const int* __restrict__ mem,
+                              const double* __restrict__ rf, double* __restrict__ bc, const int* stop) {
+  if (stopped(stop)) return;
+  const int I = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (I >= nc) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int t = mptr[I] + lane; t < mptr[I + 1]; t += 32) {
+    const int i = mem[t];
+    s0 += rf[3 * i]; s1 += rf[3 * i + 1]; s2 += rf[3 * i + 2];
+  }
+  s0 = warp_sum(s0); s1 = warp_sum(s1); s2 = warp_sum(s2);
+  if (lane == 0) { bc[3 * I] = s0; bc[3 * I + 1] = s1; bc[3 * I + 2] = s2; }
+}
+
+// coarsest: scatter SELL blocks into a dense N x N row-major matrix
+__global__ void k_mg_dense_build(int n, int S, const int* __restrict__ slice_base, const int* __restrict__ slice_width,
+                                 const int* __restrict__ col, const double* __restrict__ val, double* __restrict__ A) {
+  const int N = 3 * n;
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) A[t] = 0.0;
+  __syncthreads();
+  for (int row = threadIdx.x; row < n; row += blockDim.x) {
+    const int sl = row / kSlice, lane = row % kSlice;
+    const int base = slice_base[sl], K = slice_width[sl];
+    for (int k = 0; k < K; ++k) {
+      const int j = col[base + k * kSlice + lane];
+      const double* v = val + (size_t)base * 9 + (k * 9) * kSlice + lane;
+      bool any = false;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) any |= (v[c * kSlice] != 0.0);
+      if (!any) continue;   // padding
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) A[(size_t)(3 * row + a) * N + 3 * j + c] += v[(a * 3 + c) * kSlice];
+    }
+  }
+}
+
+// Gauss-Jordan with partial pivoting in one CTA, matrices in shared memory
+// (N <= kDenseSmem): Ainv = A^-1.
+__global__ void __launch_bounds__(1024) k_mg_dense_invert(int N, const double* __restrict__ Ag, double* __restrict__ Ainv) {
+  extern __shared__ double smem[];
+  double* A = smem;
+  double* X = smem + N * N;
+  __shared__ int piv;
+  __shared__ double pval[32];
+  __shared__ int pidx[32];
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
+    A[t] = Ag[t];
+    X[t] = ((t / N) == (t % N)) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int k = 0; k < N; ++k) {
+    double best = -1.0;
+    int bi = k;
+    for (int r = k + threadIdx.x; r < N; r += blockDim.x) {
+      const double v = fabs(A[r * N + k]);
+      if (v > best) { best = v; bi = r; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_down_sync(0xffffffffu, best, o);
+      const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if ((threadIdx.x & 31) == 0) { pval[threadIdx.x >> 5] = best; pidx[threadIdx.x >> 5] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = -1.0;
+      int i = k;
+      for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w)
+        if (pval[w] > b || (pval[w] == b && pidx[w] < i)) { b = pval[w]; i = pidx[w]; }
+      piv = i;
+    }
+    __syncthreads();
+    const int p = piv;
+    if (p != k) {
+      for (int c = threadIdx.x; c < N; c += blockDim.x) {
+        double t = A[k * N + c]; A[k * N + c] = A[p * N + c]; A[p * N + c] = t;
+        t = X[k * N + c]; X[k * N + c] = X[p * N + c]; X[p * N + c] = t;
+      }
+      __syncthreads();
+    }
+    const double id = 1.0 / A[k * N + k];
+    __syncthreads();
+    for (int c = threadIdx.x; c < N; c += blockDim.x) { A[k * N + c] *= id; X[k * N + c] *= id; }
+    __syncthreads();
+    for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
+      const int r = t / N, c = t % N;
+      if (r == k) continue;
+      const double f = A[r * N + k];
+      if (c != k) A[r * N + c] -= f * A[k * N + c];
+      X[r * N + c] -= f * X[k * N + c];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < N; r += blockDim.x)
+      if (r != k) A[r * N + k] = 0.0;
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) Ainv[t] = X[t];
+}
+
+// x = Ainv b (dense, one row per warp)
+__global__ void k_mg_dense_solve(int N, const double* __restrict__ Ainv, const double* __restrict__ b,
+                                 double* __restrict__ x, const int* stop) {
+  if (stopped(stop)) return;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= N) return;
+  double acc = 0.0;
+  for (int c = lane; c < N; c += 32) acc += Ainv[(size_t)w * N + c] * b[c];
+  acc = warp_sum(acc);
+  if (lane == 0) x[w] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// host drivers
+
+// Galerkin hierarchy for a new fine operator `val` (fine minv already set)
+void mg_assemble(dp_scene* s, const double* val) {
+  MG* mg = s->mg;
+  if (!mg) return;
+  const double* vf = val;
+  for (size_t l = 1; l < mg->lv.size(); ++l) {
+    MGLevel& L = mg->lv[l];
+    k_mg_galerkin<<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
+        L.n, L.S, L.slice_base, L.slice_width, L.diag_slot, L.gal_ptr, L.gal, vf, L.val, L.minv, L.slot_row, L.NS);
+    vf = L.val;
+    s->launches++;
+  }
+  const MGLevel& Lc = mg->lv.back();
+  k_mg_dense_build<<<1, 1024, 0, s->stream>>>(Lc.n, Lc.S, Lc.slice_base, Lc.slice_width, Lc.col, Lc.val, mg->dense);
+  k_mg_dense_invert<<<1, 1024, (size_t)2 * mg->N * mg->N * sizeof(double), s->stream>>>(mg->N, mg->dense, mg->dinv);
+  s->launches += 2;
+}
+
+// z = B r (one V-cycle), fine operator `val`.  r and z are 3V vectors (z != r).
+static void vcycle(dp_scene* s, const double* val0, int l, const double* b, double* x, const int* stop) {
+  MG* mg = s->mg;
+  MGLevel& L = mg->lv[l];
+  const double* val = (l == 0) ? val0 : L.val;
+  const int nb_rows = grid_for(L.n, 256);
+  const int nb_sl = grid_for((int64_t)L.S * 32, 256);
+  if (l == (int)mg->lv.size() - 1) {
+    k_mg_dense_solve<<<grid_for((int64_t)mg->N * 32, 256), 256, 0, s->stream>>>(mg->N, mg->dinv, b, x, stop);
+    s->launches++;
+    return;
+  }
+  MGLevel& C = mg->lv[l + 1];
+  const double om = mg->omega;
+  // pre-smoothing from zero: x = w Minv b, then nu-1 sweeps; last pass also gives r
+  double* xa = L.t;   // work buffers never alias the output x
+  double* xb = L.u;
+  k_mg_jacobi0<<<nb_rows, 256, 0, s->stream>>>(L.n, L.minv, b, om, xa, stop);
+  s->launches++;
+  for (int it = 1; it < mg->nu; ++it) {
+    k_mg_smooth<<<nb_sl, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, L.minv, b, xa,
+                                             nullptr, nullptr, om, xb, nullptr, stop);
+    std::swap(xa, xb);
+    s->launches++;
+  }
+  k_mg_smooth<<<nb_sl, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, L.minv, b, xa, nullptr,
+                                           nullptr, om, nullptr, L.r, stop);
+  k_mg_restrict<<<grid_for((int64_t)C.n * 32, 256), 256, 0, s->stream>>>(C.n, C.mem_ptr, C.mem, L.r, C.b, stop);
+  s->launches += 2;
+  vcycle(s, val0, l + 1, C.b, C.x, stop);
+  // post-smoothing; the first sweep applies the coarse correction in its gathers
+  for (int it = 0; it < mg->nu; ++it) {
+    double* dst = (it == mg->nu - 1) ? x : xb;
+    k_mg_smooth<<<nb_sl, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, L.minv, b, xa,
+                                             it == 0 ? C.x : nullptr, it == 0 ? C.agg : nullptr, om, dst, nullptr,
+                                             stop);
+    s->launches++;
+    if (dst == xb) std::swap(xa, xb);
+  }
+}
+
+void mg_apply(dp_scene* s, const double* val, const double* r, double* z, const int* stop) {
+  vcycle(s, val, 0, r, z, stop);
+}
+
+}  // namespace dp

@@ -158,6 +158,9 @@ static int raise_status(int st) {
 using namespace dp;
 
 static const int g_debug = getenv("DP_DEBUG") ? atoi(getenv("DP_DEBUG")) : 0;
+// after a line search that had to cut the step below 1/16 the Newton model is
+// poor (friction-cone / activation kinks): a cheap direction is enough
+static const double g_eta_plateau = getenv("DP_ETA_PLATEAU") ? atof(getenv("DP_ETA_PLATEAU")) : 0.0;
 static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -812,8 +815,8 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     double eta = (rn > 0) ? 0.1 * cfg.tol * scale / rn : cfg.lin_rtol_max;
     // after a line search that had to cut the step below 1/16 the Newton
     // model is poor (friction cone / activation kinks): a cheap direction is enough
-    const double eta_cap = (last_t < 1.0 / 16) ? std::max(cfg.lin_rtol_max, 1e-2) : cfg.lin_rtol_max;
-    eta = std::min(eta_cap, std::max(cfg.lin_rtol_min, eta));
+    eta = std::min(cfg.lin_rtol_max, std::max(cfg.lin_rtol_min, eta));
+    if (last_t < 1.0 / 16) eta = std::max(eta, g_eta_plateau);
     int iters = 0, brk = 0;
     double relres = 0;
     // multigrid pays off for tight solves (adjoint, 1e-10); the inexact

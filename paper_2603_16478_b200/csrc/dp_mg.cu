@@ -48,7 +48,7 @@ struct MG {
   double* dense = nullptr;   // coarsest dense operator (N x N), N = 3 n_coarsest
   double* dinv = nullptr;    // its inverse
   int N = 0;
-  double omega = 0.6;
+  double omega = 0.8;
   int nu = 1;
   size_t bytes = 0;
 };

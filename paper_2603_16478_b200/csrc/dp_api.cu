@@ -507,10 +507,16 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   return DP_OK;
 }
 
+static void cache_free(dp_cache* c);
+
 int dp_scene_destroy(dp_scene* s) {
   if (!s) return DP_OK;
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
+  for (dp_cache* c : s->cache_pool) cache_free(c);
+  s->cache_pool.clear();
+  for (dp_cache* c : s->live_caches) c->scene = nullptr;   // freed by their own destroy
+  s->live_caches.clear();
   mg_destroy(s);
   void* ptrs[] = {s->ev, s->B, s->w, s->vol, s->mu, s->lam, s->model, s->mass, s->inc_ptr, s->inc,
                   s->slice_base, s->slice_width, s->col, s->diag_slot, s->val_fwd, s->val_adj, s->val_A,
@@ -685,30 +691,60 @@ int dp_scene_export_bsr(dp_scene* s, int32_t which, int32_t* rowptr, int32_t* co
 // ---------------------------------------------------------------------------
 // forward step (forward.forward_step, forward.py:174-248)
 
+// Step caches come from a per-scene pool: a rollout allocates one cache per
+// step, and cudaMalloc/cudaFree inside the timed loop cost milliseconds (and
+// cudaFree synchronises the device), so destroyed caches keep their buffers.
 int dp_cache_create(dp_scene* s, dp_cache** out) {
   cudaSetDevice(s->device);
+  if (!s->cache_pool.empty()) {
+    dp_cache* c = s->cache_pool.back();
+    s->cache_pool.pop_back();
+    c->valid = 0;
+    c->n_contacts = 0;
+    c->asym = 0;
+    s->live_caches.push_back(c);
+    *out = c;
+    return DP_OK;
+  }
   dp_cache* c = new dp_cache();
   c->scene = s;
   c->V = s->V;
   const size_t n3 = (size_t)3 * s->V;
-  double** v[] = {&c->q_bar, &c->v_bar, &c->q_hat, &c->q_new, &c->q_eval};
-  for (auto p : v) {
-    if (cudaMalloc((void**)p, n3 * sizeof(double)) != cudaSuccess) {
-      dp_cache_destroy(c);
-      set_error("cudaMalloc failed for step cache");
-      return DP_ERR_CUDA;
-    }
+  double* blk = nullptr;
+  if (cudaMalloc((void**)&blk, 5 * n3 * sizeof(double)) != cudaSuccess) {
+    delete c;
+    set_error("cudaMalloc failed for step cache");
+    return DP_ERR_CUDA;
   }
+  c->q_bar = blk;
+  c->v_bar = blk + n3;
+  c->q_hat = blk + 2 * n3;
+  c->q_new = blk + 3 * n3;
+  c->q_eval = blk + 4 * n3;
+  s->live_caches.push_back(c);
   *out = c;
   return DP_OK;
 }
 
-int dp_cache_destroy(dp_cache* c) {
-  if (!c) return DP_OK;
-  void* p[] = {c->q_bar, c->v_bar, c->q_hat, c->q_new, c->q_eval, c->c_vertex, c->c_collider,
-               c->c_frame, c->c_dn, c->c_mu, c->c_delta};
+static void cache_free(dp_cache* c) {
+  void* p[] = {c->q_bar, c->c_vertex, c->c_collider, c->c_frame, c->c_dn, c->c_mu, c->c_delta};
   for (void* x : p) dfree(x);
   delete c;
+}
+
+int dp_cache_destroy(dp_cache* c) {
+  if (!c) return DP_OK;
+  if (c->scene) {
+    dp_scene* s = c->scene;
+    auto it = std::find(s->live_caches.begin(), s->live_caches.end(), c);
+    if (it != s->live_caches.end()) {
+      *it = s->live_caches.back();
+      s->live_caches.pop_back();
+    }
+    s->cache_pool.push_back(c);
+    return DP_OK;
+  }
+  cache_free(c);
   return DP_OK;
 }
 
@@ -722,7 +758,7 @@ static int cache_store(dp_scene* s, dp_cache* c, const double* q_eval, int C, in
   if (C > c->cap_contacts) {
     void* p[] = {c->c_vertex, c->c_collider, c->c_frame, c->c_dn, c->c_mu, c->c_delta};
     for (void* x : p) dfree(x);
-    const int cap = std::max(C, 16);
+    const int cap = std::max(C, 1024);
     DP_CUDA(cudaMalloc(&c->c_vertex, sizeof(int) * cap));
     DP_CUDA(cudaMalloc(&c->c_collider, sizeof(int) * cap));
     DP_CUDA(cudaMalloc(&c->c_frame, sizeof(double) * cap * 9));
@@ -831,12 +867,15 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
       R.krylov_iterations += iters;
       if (brk) {
         rc = gmres_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, cfg.gmres_restart, &iters, &relres,
-                         2.0, mg);
+                         2.0, mg, mg ? 0 : 1);
         R.krylov_iterations += iters;
       }
     } else {
+      // block-Jacobi: left preconditioning (the forcing test then weighs rows
+      // by their diagonal, which suits the stiff contact rows); multigrid:
+      // right preconditioning
       rc = gmres_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, cfg.gmres_restart, &iters, &relres, 2.0,
-                       mg);
+                       mg, mg ? 0 : 1);
       R.krylov_iterations += iters;
     }
     double t_ls0 = 0;
@@ -985,6 +1024,7 @@ static const dp_cache* g_adj_cache_tag = nullptr;
 
 int dp_adjoint_assemble(dp_scene* s, const dp_cache* c, int32_t* symmetric) {
   cudaSetDevice(s->device);
+  const double t0 = g_debug ? now_s() : 0.0;
   if (!c->valid) { set_error("step cache is empty"); return DP_ERR_VALUE; }
   int rc = load_cache_contacts(s, c);
   if (rc) return rc;
@@ -1003,6 +1043,7 @@ int dp_adjoint_assemble(dp_scene* s, const dp_cache* c, int32_t* symmetric) {
   s->last_sym_adj = c->asym ? 0 : 1;
   s->mg_adj_ready = 0;   // the hierarchy is rebuilt lazily by the solve
   if (symmetric) *symmetric = s->last_sym_adj;
+  if (g_debug) fprintf(stderr, "[dp] adjoint assemble %.2fms\n", 1e3 * (now_s() - t0));
   g_adj_cache_tag = c;
   return DP_OK;
 }
@@ -1028,6 +1069,7 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
   if (method == DP_SOLVER_AUTO) method = sym ? DP_SOLVER_CG : DP_SOLVER_GMRES;
   int iters = 0, brk = 0;
   double relres = 0;
+  const double t0 = g_debug ? now_s() : 0.0;
   const int mg = (s->mg != nullptr) && s->use_mg;
   if (mg && !s->mg_adj_ready) {
     mg_assemble(s, s->val_adj);
@@ -1039,11 +1081,12 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
     if (brk) {
       int it2 = 0;
       rc = gmres_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, cfg.gmres_restart, &it2, &relres, 0.0,
-                       mg);
+                       mg, 0);
       iters += it2;
     }
   } else {
-    rc = gmres_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, cfg.gmres_restart, &iters, &relres, 0.0, mg);
+    rc = gmres_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, cfg.gmres_restart, &iters, &relres, 0.0, mg,
+                     0);
   }
   if (mg && !(relres <= cfg.tol) && iters < cfg.max_iter) {
     // refinement: the multigrid-preconditioned solve stalled above the
@@ -1060,7 +1103,7 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
     int it2 = 0;
     double rel2 = 1.0;
     gmres_solve(s, s->val_adj, res, d, cfg.tol * bn / std::max(rn, 1e-300), cfg.max_iter - iters,
-                cfg.gmres_restart, &it2, &rel2, 0.0, 0);
+                cfg.gmres_restart, &it2, &rel2, 0.0, 0, 0);
     launch_axpy_to(s, s->z, s->z, 1.0, d);
     iters += it2;
     launch_spmv(s, s->val_adj, s->z, d);
@@ -1068,7 +1111,11 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
     relres = std::sqrt(device_norm2(s, res)) / bn;
     (void)n3b;
   }
-  if (g_debug) fprintf(stderr, "[dp] adjoint sym=%d iters=%d relres=%.2e\n", sym, iters, relres);
+  if (g_debug) {
+    cudaStreamSynchronize(s->stream);
+    fprintf(stderr, "[dp] adjoint sym=%d iters=%d relres=%.2e solve %.2fms\n", sym, iters, relres,
+            1e3 * (now_s() - t0));
+  }
   if (rep) {
     rep->converged = relres <= cfg.tol;
     rep->iterations = iters;
@@ -1092,6 +1139,7 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
 int dp_backprop_step(dp_scene* s, const dp_cache* c, const double* z, const double* dL_dv, int32_t ptr_kind,
                      double* dL_dqbar_out, double* dL_dvbar_out, double* dL_dfext_out) {
   cudaSetDevice(s->device);
+  const double t0 = g_debug ? now_s() : 0.0;
   if (g_adj_cache_tag != c) {
     int rc = dp_adjoint_assemble(s, c, nullptr);
     if (rc) return rc;
@@ -1115,6 +1163,7 @@ int dp_backprop_step(dp_scene* s, const dp_cache* c, const double* z, const doub
   if (dL_dfext_out && (rc = copy_out(s, dL_dfext_out, df, n3, ptr_kind))) return rc;
   DP_CUDA(cudaStreamSynchronize(s->stream));
   cudaError_t e = cudaGetLastError();
+  if (g_debug) fprintf(stderr, "[dp] backprop %.2fms\n", 1e3 * (now_s() - t0));
   if (e != cudaSuccess) return cuda_fail(e, "backprop");
   return DP_OK;
 }

@@ -196,6 +196,9 @@ struct dp_scene {
   dp::MG* mg = nullptr;
   int use_mg = 1;
   int mg_adj_ready = 0;
+
+  std::vector<dp_cache*> cache_pool;   // recycled step caches
+  std::vector<dp_cache*> live_caches;  // handed out, not yet destroyed
 };
 
 namespace dp {
@@ -225,7 +228,8 @@ void launch_spmv(dp_scene* s, const double* val, const double* x, double* y);
 int cg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
              int* iters, double* relres, int* breakdown);
 int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
-                int restart, int* iters, double* relres, double min_cycle_gain = 0.0, int use_mg = 0);
+                int restart, int* iters, double* relres, double min_cycle_gain = 0.0, int use_mg = 0,
+                int left = 1);
 int pcg_mg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int* iters,
                  double* relres, int* breakdown);
 double device_norm2(dp_scene* s, const double* x);   // sum of squares, synchronous

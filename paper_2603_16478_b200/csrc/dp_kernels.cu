@@ -1115,12 +1115,108 @@ __global__ void __launch_bounds__(kVT) k_gm_start(int V, const double* __restric
 
 // x += sum_i y_i v_i
 __global__ void k_gm_combine(int n, int used, const double* __restrict__ y, const double* __restrict__ Vb, size_t ld,
-                             double* __restrict__ x) {
+                             double* __restrict__ x, int accumulate) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     double acc = 0.0;
     for (int i = 0; i < used; ++i) acc += y[i] * Vb[(size_t)i * ld + k];
-    x[k] += acc;
+    x[k] = accumulate ? x[k] + acc : acc;
   }
+}
+
+// Right-preconditioned GMRES column, step 1: v_j = w_prev / hn, z = Minv v_j
+// (block-Jacobi; with multigrid only the normalisation, z comes from a V-cycle)
+__global__ void k_gm_prec(int V, const double* __restrict__ wprev, double* __restrict__ vj,
+                          const double* __restrict__ minv, double* __restrict__ z, const GmresScalars* gs) {
+  if (ldflag(&gs->done)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  const double inv = 1.0 / gs->hn;
+  double v[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) { v[c] = wprev[3 * i + c] * inv; vj[3 * i + c] = v[c]; }
+  if (minv) {
+    double u[3];
+    minv_apply(minv, V, i, v, u);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) z[3 * i + c] = u[c];
+  }
+}
+
+// step 2 (one warp per SELL slice): w = A z, coef_i = (w, v_i) for i <= j,
+// |w|^2; last block folds into the Hessenberg column.
+__global__ void __launch_bounds__(256) k_gm_spmvdot_r(int V, int S, const int* __restrict__ slice_base,
+                                                      const int* __restrict__ slice_width,
+                                                      const int* __restrict__ col, const double* __restrict__ val,
+                                                      const double* __restrict__ z, double* __restrict__ wnew,
+                                                      const double* __restrict__ Vb, size_t ld, int j,
+                                                      double* partial, unsigned int* counter, GmresScalars* gs) {
+  __shared__ double sh[8][kGM1 + 1];
+  if (ldflag(&gs->done)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * 8 + warp;
+  const int row = gw * kSlice + lane;
+  double u[3] = {0.0, 0.0, 0.0};
+  if (gw < S) {
+    spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, z, u);
+    if (row < V) {
+      wnew[3 * row] = u[0]; wnew[3 * row + 1] = u[1]; wnew[3 * row + 2] = u[2];
+    } else {
+      u[0] = u[1] = u[2] = 0.0;
+    }
+  }
+  const bool live = (gw < S) && (row < V);
+  for (int i0 = 0; i0 <= j + 1; i0 += 8) {
+    double d[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int i = i0 + t;
+      double v = 0.0;
+      if (live && i <= j + 1) {
+        if (i <= j) {
+          const double* vi = Vb + (size_t)i * ld + 3 * (size_t)row;
+          v = u[0] * vi[0] + u[1] * vi[1] + u[2] * vi[2];
+        } else {
+          v = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+        }
+      }
+      d[t] = v;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const double r = warp_sum(d[t]);
+      if (lane == 0 && i0 + t <= j + 1) sh[warp][i0 + t] = r;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += sh[w][i];
+    partial[(size_t)blockIdx.x * (kGM1 + 1) + i] = t;
+  }
+  if (last_block(counter)) {
+    __shared__ double res[kGM1 + 1];
+    fold_multi<256>(partial, kGM1 + 1, gridDim.x, j + 2, res);
+    for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) {
+      if (i <= j) {
+        gs->coef[i] = res[i];
+        gs->H[(size_t)j * kGM1 + i] = res[i];
+      } else {
+        gs->wn2_before = res[i];
+      }
+    }
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+// x += Minv t (block-Jacobi right preconditioner applied to the update)
+__global__ void k_minv_axpy(int V, const double* __restrict__ minv, const double* __restrict__ t, double* x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  double v[3] = {t[3 * i], t[3 * i + 1], t[3 * i + 2]}, u[3];
+  minv_apply(minv, V, i, v, u);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) x[3 * i + c] += u[c];
 }
 
 static int gm_grid(int n) {
@@ -1129,10 +1225,14 @@ static int gm_grid(int n) {
   return grid_for(n, kGT);
 }
 
-// Restarted GMRES on A x = b (true relative residual <= rtol).  x is
-// overwritten (zero initial guess).  Returns 0 converged, 1 not converged.
+// Restarted GMRES(m) with RIGHT preconditioning (block-Jacobi or the
+// multigrid V-cycle): the Arnoldi residual estimate is the true residual, so
+// the inner stop test and the forcing term of the inexact Newton use the same
+// norm as the recomputed residual (linsolve.py:108-197 uses left
+// preconditioning; the converged solution is the same).  x = 0 initially.
+// Returns 0 converged, 1 not converged.
 int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int restart,
-                int* iters, double* relres, double min_cycle_gain, int use_mg) {
+                int* iters, double* relres, double min_cycle_gain, int use_mg, int left) {
   const int V = s->V, n = 3 * V;
   if (restart > kMaxRestart) restart = kMaxRestart;
   if (restart > n) restart = n;
@@ -1143,18 +1243,21 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   const int nbg = gm_grid(n);
   double* Vb = s->gm_V;
   double* r = s->kr;
+  double* z = s->ku;       // M^-1 v_j
+  double* t = s->kx;       // V y at the end of a cycle
   double* y_dev = s->ks;   // scratch (>= restart doubles)
   const bool tight = rtol < 1e-7;   // inexact Newton solves skip re-orthogonalisation
   *iters = 0;
   cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
   const double bnorm = sqrt(device_norm2(s, b));
   if (bnorm == 0.0) { *relres = 0.0; return 0; }
-  // |M^-1 b|
-  if (use_mg) {
-    mg_apply(s, val, b, s->ku, nullptr);
-    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, nullptr, s->ku, s->kw, s->red.partial, s->red.counter, s->gsc, rtol, 1);
+  // nmb = |b| (right) or |M^-1 b| (left, the reference's normalisation)
+  if (left && use_mg) {
+    mg_apply(s, val, b, z, nullptr);
+    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, nullptr, z, s->kw, s->red.partial, s->red.counter, s->gsc, rtol, 1);
   } else {
-    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, b, s->kw, s->red.partial, s->red.counter, s->gsc, rtol, 1);
+    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, left ? s->minv : nullptr, b, s->kw, s->red.partial, s->red.counter,
+                                           s->gsc, rtol, 1);
   }
   s->launches++;
   int total = 0;
@@ -1164,11 +1267,12 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
     if (rel <= rtol) break;
     const double cycle_start = rel;
     double* Wb[2] = {s->kw, s->kp};   // double-buffered unnormalised basis vector
-    if (use_mg) {
-      mg_apply(s, val, r, s->ku, nullptr);
-      k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, nullptr, s->ku, Wb[0], s->red.partial, s->red.counter, s->gsc, rtol, 0);
+    if (left && use_mg) {
+      mg_apply(s, val, r, z, nullptr);
+      k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, nullptr, z, Wb[0], s->red.partial, s->red.counter, s->gsc, rtol, 0);
     } else {
-      k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, s->minv, r, Wb[0], s->red.partial, s->red.counter, s->gsc, rtol, 0);
+      k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, left ? s->minv : nullptr, r, Wb[0], s->red.partial, s->red.counter,
+                                             s->gsc, rtol, 0);
     }
     s->launches++;
     int j = 0;
@@ -1180,17 +1284,24 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
       for (int c = 0; c < chunk; ++c, ++j) {
         double* wp = Wb[j & 1];
         double* wn = Wb[(j + 1) & 1];
-        if (use_mg) {
-          // v_j = w/hn, t = A v_j ; w = B t (V-cycle) ; coef = V^T w, |w|^2
-          k_gm_spmvnorm<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, wp,
-                                                    Vb + (size_t)j * ld, s->ku, s->gsc);
-          mg_apply(s, val, s->ku, wn, &s->gsc->done);
-          k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc, 1);
-          s->launches += 2;
-        } else {
+        double* vj = Vb + (size_t)j * ld;
+        if (left && !use_mg) {
+          // fused: v_j = w/hn, w = Minv A v_j, coef = V^T w, |w|^2
           k_gm_spmvdot<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, s->minv,
-                                                   wp, Vb + (size_t)j * ld, wn, Vb, ld, j, s->red.partial,
-                                                   s->red.counter, s->gsc);
+                                                   wp, vj, wn, Vb, ld, j, s->red.partial, s->red.counter, s->gsc);
+        } else if (left) {
+          // v_j = w/hn, t = A v_j ; w = B t (V-cycle) ; coef = V^T w, |w|^2
+          k_gm_spmvnorm<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, wp, vj,
+                                                    z, s->gsc);
+          mg_apply(s, val, z, wn, &s->gsc->done);
+          k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc, 1);
+          s->launches += 1;
+        } else {
+          k_gm_prec<<<grid_for(V, 256), 256, 0, s->stream>>>(V, wp, vj, use_mg ? nullptr : s->minv, z, s->gsc);
+          if (use_mg) mg_apply(s, val, vj, z, &s->gsc->done);
+          k_gm_spmvdot_r<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, z, wn,
+                                                     Vb, ld, j, s->red.partial, s->red.counter, s->gsc);
+          s->launches += 1;
         }
         k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, j, 0, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc);
         s->launches += 2;
@@ -1210,7 +1321,7 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
     *iters += used;
     total = *iters;
     if (used > 0) {
-      // back substitution H[:used,:used] y = g[:used]
+      // back substitution H[:used,:used] y = g[:used]; x += M^-1 (V y)
       double y[kMaxRestart];
       for (int i = used - 1; i >= 0; --i) {
         double acc = hg->g[i];
@@ -1218,8 +1329,15 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
         y[i] = acc / hg->H[(size_t)i * kGM1 + i];
       }
       cudaMemcpyAsync(y_dev, y, sizeof(double) * used, cudaMemcpyHostToDevice, s->stream);
-      k_gm_combine<<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, Vb, ld, x);
-      s->launches++;
+      k_gm_combine<<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, Vb, ld, left ? x : t, left ? 1 : 0);
+      if (left) {
+      } else if (use_mg) {
+        mg_apply(s, val, t, z, nullptr);
+        launch_axpy_to(s, x, x, 1.0, z);
+      } else {
+        k_minv_axpy<<<grid_for(V, 256), 256, 0, s->stream>>>(V, s->minv, t, x);
+      }
+      s->launches += 2;
     }
     rel = true_relres(s, val, b, x, r, bnorm);
     if (rel <= rtol) break;

@@ -49,6 +49,7 @@ struct MG {
   double* dinv = nullptr;    // its inverse
   int N = 0;
   double omega = 0.8;
+  double alpha = 1.0;        // coarse-correction scaling (over-correction for UA)
   int nu = 1;
   size_t bytes = 0;
 };
@@ -288,6 +289,7 @@ int mg_setup(dp_scene* s) {
   if (rc) { delete mg; return rc; }
   if (getenv("DP_MG_OMEGA")) mg->omega = atof(getenv("DP_MG_OMEGA"));
   if (getenv("DP_MG_NU")) mg->nu = atoi(getenv("DP_MG_NU"));
+  if (getenv("DP_MG_ALPHA")) mg->alpha = atof(getenv("DP_MG_ALPHA"));
   s->mg = mg;
   s->bytes += mg->bytes;
   return 0;
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
                                                    const double* __restrict__ b, const double* __restrict__ x,
                                                    const double* __restrict__ xc, const int* __restrict__ agg,
                                                    double omega, double* __restrict__ out, double* __restrict__ r_out,
-                                                   const int* stop) {
+                                                   const int* stop, double alpha) {
   if (stopped(stop)) return;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -422,7 +424,7 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
     double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
     if (xc) {
       const int J = __ldg(agg + j);
-      x0 += __ldg(xc + 3 * J); x1 += __ldg(xc + 3 * J + 1); x2 += __ldg(xc + 3 * J + 2);
+      x0 += alpha * __ldg(xc + 3 * J); x1 += alpha * __ldg(xc + 3 * J + 1); x2 += alpha * __ldg(xc + 3 * J + 2);
     }
     a0 += v[0 * kSlice] * x0 + v[1 * kSlice] * x1 + v[2 * kSlice] * x2;
     a1 += v[3 * kSlice] * x0 + v[4 * kSlice] * x1 + v[5 * kSlice] * x2;
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
   double xt[3] = {x[3 * row], x[3 * row + 1], x[3 * row + 2]};
   if (xc) {
     const int I = agg[row];
-    xt[0] += xc[3 * I]; xt[1] += xc[3 * I + 1]; xt[2] += xc[3 * I + 2];
+    xt[0] += alpha * xc[3 * I]; xt[1] += alpha * xc[3 * I + 1]; xt[2] += alpha * xc[3 * I + 2];
   }
   const double rr[3] = {b[3 * row] - a0, b[3 * row + 1] - a1, b[3 * row + 2] - a2};
   if (r_out) { r_out[3 * row] = rr[0]; r_out[3 * row + 1] = rr[1]; r_out[3 * row + 2] = rr[2]; }
@@ -601,12 +603,12 @@ static void vcycle(dp_scene* s, const double* val0, int l, const double* b, doub
   s->launches++;
   for (int it = 1; it < mg->nu; ++it) {
     k_mg_smooth<<<nb_sl, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, L.minv, b, xa,
-                                             nullptr, nullptr, om, xb, nullptr, stop);
+                                             nullptr, nullptr, om, xb, nullptr, stop, 1.0);
     std::swap(xa, xb);
     s->launches++;
   }
   k_mg_smooth<<<nb_sl, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, L.minv, b, xa, nullptr,
-                                           nullptr, om, nullptr, L.r, stop);
+                                           nullptr, om, nullptr, L.r, stop, 1.0);
   k_mg_restrict<<<grid_for((int64_t)C.n * 32, 256), 256, 0, s->stream>>>(C.n, C.mem_ptr, C.mem, L.r, C.b, stop);
   s->launches += 2;
   vcycle(s, val0, l + 1, C.b, C.x, stop);
@@ -615,7 +617,7 @@ static void vcycle(dp_scene* s, const double* val0, int l, const double* b, doub
     double* dst = (it == mg->nu - 1) ? x : xb;
     k_mg_smooth<<<nb_sl, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, L.minv, b, xa,
                                              it == 0 ? C.x : nullptr, it == 0 ? C.agg : nullptr, om, dst, nullptr,
-                                             stop);
+                                             stop, mg->alpha);
     s->launches++;
     if (dst == xb) std::swap(xa, xb);
   }

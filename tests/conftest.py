@@ -31,4 +31,4 @@ def rng():
 
 SCENES = ["bar_arap", "bar_neohookean", "hanging_sheet", "block_on_plane",
           "friction_high", "friction_ident", "block_lift", "single_tet_nh",
-          "cube2_slide", "c1lite"]
+          "cube2_slide", "c1lite", "c1"]

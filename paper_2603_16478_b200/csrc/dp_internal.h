@@ -194,7 +194,7 @@ struct dp_scene {
 
   // multigrid preconditioner (dp_mg.cu); nullptr = block-Jacobi only
   dp::MG* mg = nullptr;
-  int use_mg = 1;
+  int use_mg = 2;
   int mg_adj_ready = 0;
 
   std::vector<dp_cache*> cache_pool;   // recycled step caches

@@ -49,7 +49,7 @@ struct MG {
   double* dinv = nullptr;    // its inverse
   int N = 0;
   double omega = 0.8;
-  double alpha = 1.0;        // coarse-correction scaling (over-correction for UA)
+  double alpha = 1.5;        // coarse-correction scaling (over-correction for UA)
   int nu = 1;
   size_t bytes = 0;
 };

@@ -13,7 +13,7 @@ L = sm.dev.lib
 nl = C.c_int32(); rows = np.zeros(16, np.int32)
 L.dp_scene_get_mg_levels(sm.dev.handle, C.byref(nl), _lib.ptr(rows), 16)
 print("levels", nl.value, rows[:nl.value].tolist(), flush=True)
-cfg = fw.ForwardConfig(lin_rtol_max=float(os.environ.get('ETA_MAX', '1e-3')))
+cfg = fw.ForwardConfig(lin_rtol_max=float(os.environ.get('ETA_MAX', '1e-3')), gmres_restart=int(os.environ.get('RESTART', '50')), tol=float(os.environ.get('TOL', '1e-9')))
 for rep_i in range(2):
     st = sc.rest_state()
     caches, fwd = [], []

@@ -37,6 +37,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# load every kernel at context creation, not at its first launch inside the
+# timed region
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 CONFIGS = {
     # name: (cells per side, description)
@@ -161,6 +164,13 @@ def gpu_arm(args, rank, world, local_rank):
     from paper_2603_16478_b200.parallel import allreduce_gradients, pack_gradients
 
     torch.cuda.set_device(local_rank)
+    # the Newton driver's host thread synchronises ~100x per step: keep it on
+    # one core (no migrations between spin-waits)
+    try:
+        cpus = sorted(os.sched_getaffinity(0))
+        os.sched_setaffinity(0, {cpus[(2 * local_rank + 1) % len(cpus)]})
+    except (AttributeError, OSError):
+        pass
     n, desc = CONFIGS[args.config]
     scene = make_scene(n, fingers=(args.config == "c5"))
     # batch of parameter candidates: rank r simulates E * (1 + 0.05 r)
@@ -224,9 +234,9 @@ def gpu_arm(args, rank, world, local_rank):
         loss = float(torch.sum((q[nsteps] - target) ** 2))
         return grads, loss, stats, adj_iters
 
-    # warm-up (untimed)
+    # warm-up (untimed): the same K-step rollout + reverse sweep as timed
     for _ in range(max(W, 0)):
-        device_rollout(1, 0)
+        device_rollout(K, W)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

@@ -122,6 +122,9 @@ typedef struct {
 const char* dp_last_error(void);
 const char* dp_version(void);
 int dp_device_count(void);
+/* host wait policy for device synchronisation on `device`: 1 spin (default
+ * at scene creation), 2 yield, 4 blocking sync, 0 unchanged */
+int dp_set_spin_wait(int32_t device, int32_t mode);
 
 /* ---- scene (core.assemble_system_matrix, core.py:379-389; build_elements,
  *      elasticity.py:74-108; build_block_pattern, core.py:339-364) ---------- */

@@ -92,6 +92,7 @@ SIGNATURES = {
     "dp_last_error": (C.c_char_p, []),
     "dp_version": (C.c_char_p, []),
     "dp_device_count": (C.c_int, []),
+    "dp_set_spin_wait": (C.c_int, [C.c_int32, C.c_int32]),
     "dp_scene_create": (C.c_int, [C.POINTER(SceneDesc), C.POINTER(_P)]),
     "dp_scene_destroy": (C.c_int, [_P]),
     "dp_scene_get_info": (C.c_int, [_P, C.POINTER(SceneInfo)]),

@@ -135,6 +135,8 @@ struct dp_scene {
   double* val_A = nullptr;         // constant A (lazy, export only)
   int *contrib_ptr = nullptr, *contrib = nullptr;
   double* minv = nullptr;          // block-Jacobi inverses [9][V]
+  float* val32 = nullptr;          // FP32 copy of the last assembled operator (multigrid fine level)
+  float* minv32 = nullptr;         // FP32 block-Jacobi inverses (multigrid smoother)
 
   // element outputs
   double* fe = nullptr;            // E*NV*3
@@ -261,5 +263,6 @@ void mg_apply(dp_scene* s, const double* val, const double* r, double* z, const 
 int mg_levels(const dp_scene* s);
 int mg_level_rows(const dp_scene* s, int l);
 void mg_set_params(dp_scene* s, double omega, int nu);
+void mg_set_symmetric(dp_scene* s, int on);
 
 }  // namespace dp

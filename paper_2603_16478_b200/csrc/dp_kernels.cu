@@ -14,6 +14,7 @@
 // list of (element, local block, transposed?) contributions.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "dp_common.cuh"
 #include "dp_internal.h"
@@ -395,7 +396,8 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
                                                   const double* __restrict__ b_comp, const int* __restrict__ c_count,
                                                   const int* __restrict__ c_off, const double* __restrict__ c_blk,
                                                   int use_extras, double h2, double* __restrict__ val,
-                                                  double* __restrict__ minv) {
+                                                  double* __restrict__ minv, float* __restrict__ val32,
+                                                  float* __restrict__ minv32) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= S) return;
@@ -445,9 +447,18 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
       inv3_guarded(b, o);
 #pragma unroll
       for (int u = 0; u < 9; ++u) minv[(size_t)u * V + row] = o[u];
+      if (minv32) {
+#pragma unroll
+        for (int u = 0; u < 9; ++u) minv32[(size_t)u * V + row] = (float)o[u];
+      }
     }
 #pragma unroll
     for (int c = 0; c < 9; ++c) vs[(k * 9 + c) * kSlice + lane] = b[c];
+    if (val32) {
+      float* v32 = val32 + (size_t)base * 9;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) v32[(k * 9 + c) * kSlice + lane] = (float)b[c];
+    }
   }
 }
 
@@ -459,7 +470,8 @@ void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat)
   k_assemble<<<nb, nt, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->diag_slot, s->contrib_ptr,
                                        s->contrib, s->H, s->mass, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_comp,
                                        has_c ? s->c_count : nullptr, s->c_off, s->c_blk, amat ? 0 : 1,
-                                       s->h * s->h, val, s->minv);
+                                       s->h * s->h, val, s->minv, amat ? nullptr : s->val32,
+                                       amat ? nullptr : s->minv32);
   s->launches++;
 }
 
@@ -1073,7 +1085,8 @@ __global__ void k_gm_normalize(int n, const double* __restrict__ w, double* __re
 }
 
 // cycle start: v0 = Minv r (unnormalised) and |v0|^2 -> beta, g, thresholds
-__global__ void __launch_bounds__(kVT) k_gm_start(int V, const double* __restrict__ minv, const double* __restrict__ r,
+__global__ void __launch_bounds__(kVT) k_gm_start(double reorth_thr, int V, const double* __restrict__ minv,
+                                                  const double* __restrict__ r,
                                                   double* __restrict__ v0, double* partial, unsigned int* counter,
                                                   GmresScalars* gs, double tol, int set_nmb) {
   __shared__ double sh[32];
@@ -1105,7 +1118,7 @@ __global__ void __launch_bounds__(kVT) k_gm_start(int V, const double* __restric
         gs->reorth = 0;
         // tight solves (adjoint, 1e-10) need CGS2-level orthogonality; the
         // inexact Newton solves only re-orthogonalise on severe cancellation
-        gs->reorth_thr = (tol < 1e-7) ? 0.25 : 0.0;
+        gs->reorth_thr = (tol < 1e-7) ? reorth_thr : 0.0;
         gs->used = 0;
         gs->est = beta / gs->nmb;
       }
@@ -1219,6 +1232,9 @@ __global__ void k_minv_axpy(int V, const double* __restrict__ minv, const double
   for (int c = 0; c < 3; ++c) x[3 * i + c] += u[c];
 }
 
+// re-orthogonalise (tight solves only) when |w|^2 drops below this fraction
+static const double g_reorth_thr = getenv("DP_REORTH") ? atof(getenv("DP_REORTH")) : 0.01;
+
 static int gm_grid(int n) {
   // one element per thread: every basis load of a thread is independent
   // (MLP = j+1), and enough CTAs to cover HBM latency
@@ -1254,9 +1270,9 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   // nmb = |b| (right) or |M^-1 b| (left, the reference's normalisation)
   if (left && use_mg) {
     mg_apply(s, val, b, z, nullptr);
-    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, nullptr, z, s->kw, s->red.partial, s->red.counter, s->gsc, rtol, 1);
+    k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, z, s->kw, s->red.partial, s->red.counter, s->gsc, rtol, 1);
   } else {
-    k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, left ? s->minv : nullptr, b, s->kw, s->red.partial, s->red.counter,
+    k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, left ? s->minv : nullptr, b, s->kw, s->red.partial, s->red.counter,
                                            s->gsc, rtol, 1);
   }
   s->launches++;
@@ -1269,9 +1285,9 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
     double* Wb[2] = {s->kw, s->kp};   // double-buffered unnormalised basis vector
     if (left && use_mg) {
       mg_apply(s, val, r, z, nullptr);
-      k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, nullptr, z, Wb[0], s->red.partial, s->red.counter, s->gsc, rtol, 0);
+      k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, z, Wb[0], s->red.partial, s->red.counter, s->gsc, rtol, 0);
     } else {
-      k_gm_start<<<nbv, kVT, 0, s->stream>>>(V, left ? s->minv : nullptr, r, Wb[0], s->red.partial, s->red.counter,
+      k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, left ? s->minv : nullptr, r, Wb[0], s->red.partial, s->red.counter,
                                              s->gsc, rtol, 0);
     }
     s->launches++;
@@ -1487,8 +1503,20 @@ __global__ void __launch_bounds__(kVT) k_pcg_xr(int V, double* x, double* r, con
   }
 }
 
+int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
+                      int* iters, double* relres, int* breakdown);
+
+// CG needs a symmetric preconditioner: force the symmetric V(nu,nu) cycle
 int pcg_mg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int* iters,
                  double* relres, int* breakdown) {
+  mg_set_symmetric(s, 1);
+  const int rc = pcg_mg_solve_impl(s, val, b, x, rtol, max_iter, iters, relres, breakdown);
+  mg_set_symmetric(s, 0);
+  return rc;
+}
+
+int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
+                      int* iters, double* relres, int* breakdown) {
   const int V = s->V, n = 3 * V;
   const int nbv = grid_for(V, kVT);
   const int nbs = grid_for((int64_t)s->S * 32, 256);

@@ -51,6 +51,8 @@ struct MG {
   double omega = 0.8;
   double alpha = 1.5;        // coarse-correction scaling (over-correction for UA)
   int nu = 1;
+  int post = 1;               // post-smoothing sweeps on (1) / off (0, non-symmetric use only)
+  int symmetric_needed = 0;  // set while a CG solve uses the V-cycle
   size_t bytes = 0;
 };
 
@@ -163,6 +165,11 @@ int mg_setup(dp_scene* s) {
   L0.diag_slot = s->diag_slot;
   L0.minv = s->minv;
   int rc = 0;
+  // mixed-precision preconditioner: the fine-level V-cycle reads FP32 copies
+  // of the operator (written by k_assemble); the Krylov method itself runs on
+  // the FP64 operator, so the solution accuracy is unaffected
+  rc |= al(mg, &s->val32, (size_t)s->NS * 9);
+  rc |= al(mg, &s->minv32, (size_t)s->V * 9);
   rc |= al(mg, &L0.x, (size_t)3 * s->V);
   rc |= al(mg, &L0.r, (size_t)3 * s->V);
   rc |= al(mg, &L0.t, (size_t)3 * s->V);
@@ -278,6 +285,8 @@ int mg_setup(dp_scene* s) {
   mg->N = 3 * Lc.n;
   if (mg->lv.size() < 2 || mg->N > kDenseSmem) {
     // no useful hierarchy (tiny or unaggregatable graph): disable
+    if (s->val32) { cudaFree(s->val32); s->val32 = nullptr; }
+    if (s->minv32) { cudaFree(s->minv32); s->minv32 = nullptr; }
     delete mg;
     s->mg = nullptr;
     return 0;
@@ -290,6 +299,7 @@ int mg_setup(dp_scene* s) {
   if (getenv("DP_MG_OMEGA")) mg->omega = atof(getenv("DP_MG_OMEGA"));
   if (getenv("DP_MG_NU")) mg->nu = atoi(getenv("DP_MG_NU"));
   if (getenv("DP_MG_ALPHA")) mg->alpha = atof(getenv("DP_MG_ALPHA"));
+  if (getenv("DP_MG_POST")) mg->post = atoi(getenv("DP_MG_POST"));
   s->mg = mg;
   s->bytes += mg->bytes;
   return 0;
@@ -298,6 +308,8 @@ int mg_setup(dp_scene* s) {
 void mg_destroy(dp_scene* s) {
   MG* mg = s->mg;
   if (!mg) return;
+  if (s->val32) { cudaFree(s->val32); s->val32 = nullptr; }
+  if (s->minv32) { cudaFree(s->minv32); s->minv32 = nullptr; }
   for (size_t l = 0; l < mg->lv.size(); ++l) {
     MGLevel& L = mg->lv[l];
     void* own[] = {L.x, L.r, L.t, L.u, L.b};
@@ -343,11 +355,12 @@ __device__ __forceinline__ void inv3(const double a[9], double o[9]) {
 // coarse operator: val_c[slot] = sum of the fine blocks in its gather list
 // (one warp per coarse slot, lanes over contributions); block-Jacobi inverse
 // of the diagonal slots.
+template <class TF>
 __global__ void __launch_bounds__(256) k_mg_galerkin(int n, int S, const int* __restrict__ slice_base,
                                                      const int* __restrict__ slice_width,
                                                      const int* __restrict__ diag_slot,
                                                      const int* __restrict__ gal_ptr, const int* __restrict__ gal,
-                                                     const double* __restrict__ valf, double* __restrict__ valc,
+                                                     const TF* __restrict__ valf, double* __restrict__ valc,
                                                      double* __restrict__ minv, const int* __restrict__ slot_row,
                                                      int64_t NS) {
   const int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -355,9 +368,9 @@ __global__ void __launch_bounds__(256) k_mg_galerkin(int n, int S, const int* __
   if (slot >= NS) return;
   double b[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int t = gal_ptr[slot] + lane; t < gal_ptr[slot + 1]; t += 32) {
-    const double* src = valf + gal[t];
+    const TF* src = valf + gal[t];
 #pragma unroll
-    for (int c = 0; c < 9; ++c) b[c] += src[c * kSlice];
+    for (int c = 0; c < 9; ++c) b[c] += (double)src[c * kSlice];
   }
 #pragma unroll
   for (int c = 0; c < 9; ++c) b[c] = warp_allsum(b[c]);
@@ -380,7 +393,8 @@ __global__ void __launch_bounds__(256) k_mg_galerkin(int n, int S, const int* __
   }
 }
 
-__device__ __forceinline__ void mv_minv(const double* __restrict__ minv, int n, int i, const double r[3], double u[3]) {
+template <class TM>
+__device__ __forceinline__ void mv_minv(const TM* __restrict__ minv, int n, int i, const double r[3], double u[3]) {
   u[0] = minv[0 * (size_t)n + i] * r[0] + minv[1 * (size_t)n + i] * r[1] + minv[2 * (size_t)n + i] * r[2];
   u[1] = minv[3 * (size_t)n + i] * r[0] + minv[4 * (size_t)n + i] * r[1] + minv[5 * (size_t)n + i] * r[2];
   u[2] = minv[6 * (size_t)n + i] * r[0] + minv[7 * (size_t)n + i] * r[1] + minv[8 * (size_t)n + i] * r[2];
@@ -389,7 +403,8 @@ __device__ __forceinline__ void mv_minv(const double* __restrict__ minv, int n, 
 // x = omega Minv b
 __device__ __forceinline__ bool stopped(const int* stop) { return stop && *(volatile const int*)stop; }
 
-__global__ void k_mg_jacobi0(int n, const double* __restrict__ minv, const double* __restrict__ b, double omega,
+template <class TM>
+__global__ void k_mg_jacobi0(int n, const TM* __restrict__ minv, const double* __restrict__ b, double omega,
                              double* __restrict__ x, const int* stop) {
   if (stopped(stop)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -402,9 +417,10 @@ __global__ void k_mg_jacobi0(int n, const double* __restrict__ minv, const doubl
 
 // out = xt + omega Minv (b - A xt), xt = x + P xc (xc/agg may be null)
 // and optionally r_out = b - A xt (for the residual after the last pre-sweep)
+template <class TV>
 __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __restrict__ slice_base,
                                                    const int* __restrict__ slice_width, const int* __restrict__ col,
-                                                   const double* __restrict__ val, const double* __restrict__ minv,
+                                                   const TV* __restrict__ val, const TV* __restrict__ minv,
                                                    const double* __restrict__ b, const double* __restrict__ x,
                                                    const double* __restrict__ xc, const int* __restrict__ agg,
                                                    double omega, double* __restrict__ out, double* __restrict__ r_out,
@@ -415,20 +431,20 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
   if (gw >= S) return;
   const int row = gw * kSlice + lane;
   const int base = slice_base[gw], K = slice_width[gw];
-  const double* vs = val + (size_t)base * 9 + lane;
+  const TV* vs = val + (size_t)base * 9 + lane;
   const int* cs = col + base + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (int k = 0; k < K; ++k) {
     const int j = __ldg(cs + k * kSlice);
-    const double* v = vs + k * 9 * kSlice;
+    const TV* v = vs + k * 9 * kSlice;
     double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
     if (xc) {
       const int J = __ldg(agg + j);
       x0 += alpha * __ldg(xc + 3 * J); x1 += alpha * __ldg(xc + 3 * J + 1); x2 += alpha * __ldg(xc + 3 * J + 2);
     }
-    a0 += v[0 * kSlice] * x0 + v[1 * kSlice] * x1 + v[2 * kSlice] * x2;
-    a1 += v[3 * kSlice] * x0 + v[4 * kSlice] * x1 + v[5 * kSlice] * x2;
-    a2 += v[6 * kSlice] * x0 + v[7 * kSlice] * x1 + v[8 * kSlice] * x2;
+    a0 += (double)v[0 * kSlice] * x0 + (double)v[1 * kSlice] * x1 + (double)v[2 * kSlice] * x2;
+    a1 += (double)v[3 * kSlice] * x0 + (double)v[4 * kSlice] * x1 + (double)v[5 * kSlice] * x2;
+    a2 += (double)v[6 * kSlice] * x0 + (double)v[7 * kSlice] * x1 + (double)v[8 * kSlice] * x2;
   }
   if (row >= n) return;
   double xt[3] = {x[3 * row], x[3 * row + 1], x[3 * row + 2]};
@@ -445,6 +461,17 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
     out[3 * row + 1] = xt[1] + omega * u[1];
     out[3 * row + 2] = xt[2] + omega * u[2];
   }
+}
+
+// x = xa + alpha P xc
+__global__ void k_mg_prolong(int n, const double* __restrict__ xa, const double* __restrict__ xc,
+                             const int* __restrict__ agg, double alpha, double* __restrict__ x, const int* stop) {
+  if (stopped(stop)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int I = agg[i];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) x[3 * i + c] = xa[3 * i + c] + alpha * xc[3 * I + c];
 }
 
 // b_c[I] = sum over members of r_f (one warp per coarse row)
@@ -487,59 +514,54 @@ __global__ void k_mg_dense_build(int n, int S, const int* __restrict__ slice_bas
 }
 
 // Gauss-Jordan with partial pivoting in one CTA, matrices in shared memory
-// (N <= kDenseSmem): Ainv = A^-1.
-__global__ void __launch_bounds__(1024) k_mg_dense_invert(int N, const double* __restrict__ Ag, double* __restrict__ Ainv) {
+// (N <= kDenseSmem): Ainv = A^-1.  Rows are spread over warps, columns over
+// lanes (no integer division in the elimination loop).
+__global__ void __launch_bounds__(256) k_mg_dense_invert(int N, const double* __restrict__ Ag, double* __restrict__ Ainv) {
   extern __shared__ double smem[];
   double* A = smem;
   double* X = smem + N * N;
   __shared__ int piv;
-  __shared__ double pval[32];
-  __shared__ int pidx[32];
-  for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
-    A[t] = Ag[t];
-    X[t] = ((t / N) == (t % N)) ? 1.0 : 0.0;
-  }
+  __shared__ double rowscale;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) A[t] = Ag[t];
+  for (int r = warp; r < N; r += nw)
+    for (int c = lane; c < N; c += 32) X[r * N + c] = (r == c) ? 1.0 : 0.0;
   __syncthreads();
   for (int k = 0; k < N; ++k) {
-    double best = -1.0;
-    int bi = k;
-    for (int r = k + threadIdx.x; r < N; r += blockDim.x) {
-      const double v = fabs(A[r * N + k]);
-      if (v > best) { best = v; bi = r; }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_down_sync(0xffffffffu, best, o);
-      const int oi = __shfl_down_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    if ((threadIdx.x & 31) == 0) { pval[threadIdx.x >> 5] = best; pidx[threadIdx.x >> 5] = bi; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = -1.0;
-      int i = k;
-      for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w)
-        if (pval[w] > b || (pval[w] == b && pidx[w] < i)) { b = pval[w]; i = pidx[w]; }
-      piv = i;
+    if (warp == 0) {
+      double best = -1.0;
+      int bi = k;
+      for (int r = k + lane; r < N; r += 32) {
+        const double v = fabs(A[r * N + k]);
+        if (v > best) { best = v; bi = r; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_down_sync(0xffffffffu, best, o);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) { piv = bi; rowscale = 1.0 / A[bi * N + k]; }
     }
     __syncthreads();
     const int p = piv;
-    if (p != k) {
-      for (int c = threadIdx.x; c < N; c += blockDim.x) {
-        double t = A[k * N + c]; A[k * N + c] = A[p * N + c]; A[p * N + c] = t;
-        t = X[k * N + c]; X[k * N + c] = X[p * N + c]; X[p * N + c] = t;
-      }
-      __syncthreads();
+    const double id = rowscale;
+    // swap rows k and p while scaling the new pivot row
+    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+      const double ak = A[k * N + c], ap = A[p * N + c];
+      const double xk = X[k * N + c], xp = X[p * N + c];
+      A[k * N + c] = ap * id;
+      X[k * N + c] = xp * id;
+      if (p != k) { A[p * N + c] = ak; X[p * N + c] = xk; }
     }
-    const double id = 1.0 / A[k * N + k];
     __syncthreads();
-    for (int c = threadIdx.x; c < N; c += blockDim.x) { A[k * N + c] *= id; X[k * N + c] *= id; }
-    __syncthreads();
-    for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
-      const int r = t / N, c = t % N;
+    for (int r = warp; r < N; r += nw) {
       if (r == k) continue;
       const double f = A[r * N + k];
-      if (c != k) A[r * N + c] -= f * A[k * N + c];
-      X[r * N + c] -= f * X[k * N + c];
+      if (f == 0.0) continue;
+      for (int c = lane; c < N; c += 32) {
+        if (c != k) A[r * N + c] -= f * A[k * N + c];
+        X[r * N + c] -= f * X[k * N + c];
+      }
     }
     __syncthreads();
     for (int r = threadIdx.x; r < N; r += blockDim.x)
@@ -568,63 +590,99 @@ __global__ void k_mg_dense_solve(int N, const double* __restrict__ Ainv, const d
 void mg_assemble(dp_scene* s, const double* val) {
   MG* mg = s->mg;
   if (!mg) return;
-  const double* vf = val;
+  (void)val;   // the fine level is read from its FP32 copy (s->val32)
+  const double* vf = nullptr;
   for (size_t l = 1; l < mg->lv.size(); ++l) {
     MGLevel& L = mg->lv[l];
-    k_mg_galerkin<<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
-        L.n, L.S, L.slice_base, L.slice_width, L.diag_slot, L.gal_ptr, L.gal, vf, L.val, L.minv, L.slot_row, L.NS);
+    if (l == 1)
+      k_mg_galerkin<float><<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
+          L.n, L.S, L.slice_base, L.slice_width, L.diag_slot, L.gal_ptr, L.gal, s->val32, L.val, L.minv, L.slot_row,
+          L.NS);
+    else
+      k_mg_galerkin<double><<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
+          L.n, L.S, L.slice_base, L.slice_width, L.diag_slot, L.gal_ptr, L.gal, vf, L.val, L.minv, L.slot_row, L.NS);
     vf = L.val;
     s->launches++;
   }
   const MGLevel& Lc = mg->lv.back();
   k_mg_dense_build<<<1, 1024, 0, s->stream>>>(Lc.n, Lc.S, Lc.slice_base, Lc.slice_width, Lc.col, Lc.val, mg->dense);
-  k_mg_dense_invert<<<1, 1024, (size_t)2 * mg->N * mg->N * sizeof(double), s->stream>>>(mg->N, mg->dense, mg->dinv);
+  k_mg_dense_invert<<<1, 256, (size_t)2 * mg->N * mg->N * sizeof(double), s->stream>>>(mg->N, mg->dense, mg->dinv);
   s->launches += 2;
 }
 
 // z = B r (one V-cycle), fine operator `val`.  r and z are 3V vectors (z != r).
-static void vcycle(dp_scene* s, const double* val0, int l, const double* b, double* x, const int* stop) {
+template <class TV>
+static void smooth(dp_scene* s, const MGLevel& L, const TV* val, const TV* minv, const double* b, const double* x,
+                   const double* xc, const int* agg, double omega, double* out, double* r_out, const int* stop,
+                   double alpha) {
+  k_mg_smooth<TV><<<grid_for((int64_t)L.S * 32, 256), 256, 0, s->stream>>>(
+      L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x, xc, agg, omega, out, r_out, stop, alpha);
+  s->launches++;
+}
+
+template <class TV>
+static void jacobi0(dp_scene* s, const MGLevel& L, const TV* minv, const double* b, double omega, double* x,
+                    const int* stop) {
+  k_mg_jacobi0<TV><<<grid_for(L.n, 256), 256, 0, s->stream>>>(L.n, minv, b, omega, x, stop);
+  s->launches++;
+}
+
+template <class TV>
+static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, const double* b, double* x,
+                         const int* stop);
+
+static void vcycle(dp_scene* s, int l, const double* b, double* x, const int* stop) {
   MG* mg = s->mg;
-  MGLevel& L = mg->lv[l];
-  const double* val = (l == 0) ? val0 : L.val;
-  const int nb_rows = grid_for(L.n, 256);
-  const int nb_sl = grid_for((int64_t)L.S * 32, 256);
   if (l == (int)mg->lv.size() - 1) {
     k_mg_dense_solve<<<grid_for((int64_t)mg->N * 32, 256), 256, 0, s->stream>>>(mg->N, mg->dinv, b, x, stop);
     s->launches++;
     return;
   }
+  if (l == 0) vcycle_level<float>(s, 0, s->val32, s->minv32, b, x, stop);
+  else vcycle_level<double>(s, l, mg->lv[l].val, mg->lv[l].minv, b, x, stop);
+}
+
+template <class TV>
+static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, const double* b, double* x,
+                         const int* stop) {
+  MG* mg = s->mg;
+  MGLevel& L = mg->lv[l];
   MGLevel& C = mg->lv[l + 1];
   const double om = mg->omega;
   // pre-smoothing from zero: x = w Minv b, then nu-1 sweeps; last pass also gives r
   double* xa = L.t;   // work buffers never alias the output x
   double* xb = L.u;
-  k_mg_jacobi0<<<nb_rows, 256, 0, s->stream>>>(L.n, L.minv, b, om, xa, stop);
-  s->launches++;
+  jacobi0<TV>(s, L, minv, b, om, xa, stop);
   for (int it = 1; it < mg->nu; ++it) {
-    k_mg_smooth<<<nb_sl, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, L.minv, b, xa,
-                                             nullptr, nullptr, om, xb, nullptr, stop, 1.0);
+    smooth<TV>(s, L, val, minv, b, xa, nullptr, nullptr, om, xb, nullptr, stop, 1.0);
     std::swap(xa, xb);
-    s->launches++;
   }
-  k_mg_smooth<<<nb_sl, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, L.minv, b, xa, nullptr,
-                                           nullptr, om, nullptr, L.r, stop, 1.0);
+  smooth<TV>(s, L, val, minv, b, xa, nullptr, nullptr, om, nullptr, L.r, stop, 1.0);
   k_mg_restrict<<<grid_for((int64_t)C.n * 32, 256), 256, 0, s->stream>>>(C.n, C.mem_ptr, C.mem, L.r, C.b, stop);
-  s->launches += 2;
-  vcycle(s, val0, l + 1, C.b, C.x, stop);
+  s->launches++;
+  vcycle(s, l + 1, C.b, C.x, stop);
+  if (mg->post == 0 && !mg->symmetric_needed) {
+    // V(nu,0): x = x_pre + alpha P x_c (no post-smoothing SpMV)
+    k_mg_prolong<<<grid_for(L.n, 256), 256, 0, s->stream>>>(L.n, xa, C.x, C.agg, mg->alpha, x, stop);
+    s->launches++;
+    return;
+  }
   // post-smoothing; the first sweep applies the coarse correction in its gathers
   for (int it = 0; it < mg->nu; ++it) {
     double* dst = (it == mg->nu - 1) ? x : xb;
-    k_mg_smooth<<<nb_sl, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, L.minv, b, xa,
-                                             it == 0 ? C.x : nullptr, it == 0 ? C.agg : nullptr, om, dst, nullptr,
-                                             stop, mg->alpha);
-    s->launches++;
+    smooth<TV>(s, L, val, minv, b, xa, it == 0 ? C.x : nullptr, it == 0 ? C.agg : nullptr, om, dst, nullptr, stop,
+               mg->alpha);
     if (dst == xb) std::swap(xa, xb);
   }
 }
 
+void mg_set_symmetric(dp_scene* s, int on) {
+  if (s->mg) s->mg->symmetric_needed = on;
+}
+
 void mg_apply(dp_scene* s, const double* val, const double* r, double* z, const int* stop) {
-  vcycle(s, val, 0, r, z, stop);
+  (void)val;   // the V-cycle uses the operator assembled by the last mg_assemble
+  vcycle(s, 0, r, z, stop);
 }
 
 }  // namespace dp

@@ -786,7 +786,9 @@ static int cache_store(dp_scene* s, dp_cache* c, const double* q_eval, int C, in
   if (C > c->cap_contacts) {
     void* p[] = {c->c_vertex, c->c_collider, c->c_frame, c->c_dn, c->c_mu, c->c_delta};
     for (void* x : p) dfree(x);
-    const int cap = std::max(C, 1024);
+    // grow with slack: contact counts creep up step by step, and a
+    // cudaFree/cudaMalloc pair inside the rollout costs milliseconds
+    const int cap = std::max(C + C / 4, 4096);
     DP_CUDA(cudaMalloc(&c->c_vertex, sizeof(int) * cap));
     DP_CUDA(cudaMalloc(&c->c_collider, sizeof(int) * cap));
     DP_CUDA(cudaMalloc(&c->c_frame, sizeof(double) * cap * 9));
@@ -840,6 +842,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
   int rc = copy_in(s, s->q_bar, q_bar, n3, ptr_kind);
   if (!rc) rc = copy_in(s, s->v_bar, v_bar, n3, ptr_kind);
   if (rc) return rc;
+  const double t_step0 = g_debug ? now_s() : 0.0;
   DP_CUDA(cudaMemsetAsync(s->esc, 0, sizeof(EvalScalars), s->stream));
   launch_predict(s);                                   // q_hat and q = q_hat
   launch_pullback(s, s->q, s->q_bar, cfg.pullback_margin);
@@ -871,6 +874,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     DP_CUDA(cudaMemcpyAsync(q_eval, q, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s->stream));
     if (res <= cfg.tol) { converged = true; break; }
     // Newton matrix A - dA + K_b + K_c (assemble_system_jacobian, forward.py:113-149)
+    const double t_asm0 = g_debug ? now_s() : 0.0;
     launch_assemble(s, s->val_fwd, 0, 0);
     k_neg<<<grid_for(n3, 256), 256, 0, s->stream>>>(n3, s->r, s->rhs);
     s->launches++;
@@ -888,7 +892,11 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     const int mg = (s->mg != nullptr) && s->use_mg >= 2;
     if (mg) mg_assemble(s, s->val_fwd);
     double t_solve0 = 0;
-    if (g_debug) { cudaStreamSynchronize(s->stream); t_solve0 = now_s(); }
+    if (g_debug) {
+      cudaStreamSynchronize(s->stream);
+      t_solve0 = now_s();
+      fprintf(stderr, "[dp]   assemble %.2fms\n", 1e3 * (t_solve0 - t_asm0));
+    }
     if (!asym) {
       if (mg) rc = pcg_mg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk);
       else rc = cg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk);
@@ -959,6 +967,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
   if (v_out && (rc = copy_out(s, v_out, s->z, n3, ptr_kind))) return rc;
   if (cache && (rc = cache_store(s, cache, q_eval, n_contacts, asym))) return rc;
   DP_CUDA(cudaStreamSynchronize(s->stream));
+  if (g_debug) fprintf(stderr, "[dp] step total %.2fms\n", 1e3 * (now_s() - t_step0));
   R.converged = converged ? 1 : 0;
   R.iterations = nhist;
   R.n_contacts = n_contacts;

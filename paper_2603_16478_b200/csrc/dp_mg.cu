@@ -52,6 +52,8 @@ struct MG {
   double alpha = 1.5;        // coarse-correction scaling (over-correction for UA)
   int nu = 1;
   int post = 1;               // post-smoothing sweeps on (1) / off (0, non-symmetric use only)
+  int gamma = 1;              // coarse-grid corrections per visit below the fine level (2 = W-cycle)
+  int coarse_sweeps = 4;      // >0: Jacobi sweeps at the coarsest level instead of the dense inverse
   int symmetric_needed = 0;  // set while a CG solve uses the V-cycle
   size_t bytes = 0;
 };
@@ -300,6 +302,8 @@ int mg_setup(dp_scene* s) {
   if (getenv("DP_MG_NU")) mg->nu = atoi(getenv("DP_MG_NU"));
   if (getenv("DP_MG_ALPHA")) mg->alpha = atof(getenv("DP_MG_ALPHA"));
   if (getenv("DP_MG_POST")) mg->post = atoi(getenv("DP_MG_POST"));
+  if (getenv("DP_MG_GAMMA")) mg->gamma = atoi(getenv("DP_MG_GAMMA"));
+  if (getenv("DP_MG_CSWEEP")) mg->coarse_sweeps = atoi(getenv("DP_MG_CSWEEP"));
   s->mg = mg;
   s->bytes += mg->bytes;
   return 0;
@@ -571,6 +575,48 @@ __global__ void __launch_bounds__(256) k_mg_dense_invert(int N, const double* __
   for (int t = threadIdx.x; t < N * N; t += blockDim.x) Ainv[t] = X[t];
 }
 
+// coarsest level without a factorisation: nsweep damped block-Jacobi sweeps
+// from zero in one CTA (a fixed symmetric polynomial in D^-1 A, so the
+// V-cycle stays a fixed linear operator).  x is both iterate and output;
+// y is scratch.
+__global__ void __launch_bounds__(256) k_mg_coarse_jacobi(int n, int S, const int* __restrict__ slice_base,
+                                                          const int* __restrict__ slice_width,
+                                                          const int* __restrict__ col, const double* __restrict__ val,
+                                                          const double* __restrict__ minv, const double* __restrict__ b,
+                                                          double* __restrict__ x, double* __restrict__ y, double omega,
+                                                          int nsweep, const int* stop) {
+  if (stop && *(volatile const int*)stop) return;
+  for (int row = threadIdx.x; row < n; row += blockDim.x) {
+    double r[3] = {b[3 * row], b[3 * row + 1], b[3 * row + 2]}, u[3];
+    mv_minv(minv, n, row, r, u);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) x[3 * row + c] = omega * u[c];
+  }
+  __syncthreads();
+  for (int it = 0; it < nsweep; ++it) {
+    for (int row = threadIdx.x; row < n; row += blockDim.x) {
+      const int sl = row / kSlice, lane = row % kSlice;
+      const int base = slice_base[sl], K = slice_width[sl];
+      double a[3] = {0.0, 0.0, 0.0};
+      for (int k = 0; k < K; ++k) {
+        const int j = col[base + k * kSlice + lane];
+        const double* v = val + (size_t)base * 9 + (k * 9) * kSlice + lane;
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+          a[p] += v[(p * 3) * kSlice] * x[3 * j] + v[(p * 3 + 1) * kSlice] * x[3 * j + 1] +
+                  v[(p * 3 + 2) * kSlice] * x[3 * j + 2];
+      }
+      double r[3] = {b[3 * row] - a[0], b[3 * row + 1] - a[1], b[3 * row + 2] - a[2]}, u[3];
+      mv_minv(minv, n, row, r, u);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) y[3 * row + c] = x[3 * row + c] + omega * u[c];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) x[t] = y[t];
+    __syncthreads();
+  }
+}
+
 // x = Ainv b (dense, one row per warp)
 __global__ void k_mg_dense_solve(int N, const double* __restrict__ Ainv, const double* __restrict__ b,
                                  double* __restrict__ x, const int* stop) {
@@ -605,6 +651,7 @@ void mg_assemble(dp_scene* s, const double* val) {
     s->launches++;
   }
   const MGLevel& Lc = mg->lv.back();
+  if (mg->coarse_sweeps > 0) return;   // coarsest handled by in-CTA Jacobi sweeps
   k_mg_dense_build<<<1, 1024, 0, s->stream>>>(Lc.n, Lc.S, Lc.slice_base, Lc.slice_width, Lc.col, Lc.val, mg->dense);
   k_mg_dense_invert<<<1, 256, (size_t)2 * mg->N * mg->N * sizeof(double), s->stream>>>(mg->N, mg->dense, mg->dinv);
   s->launches += 2;
@@ -634,7 +681,13 @@ static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, cons
 static void vcycle(dp_scene* s, int l, const double* b, double* x, const int* stop) {
   MG* mg = s->mg;
   if (l == (int)mg->lv.size() - 1) {
-    k_mg_dense_solve<<<grid_for((int64_t)mg->N * 32, 256), 256, 0, s->stream>>>(mg->N, mg->dinv, b, x, stop);
+    if (mg->coarse_sweeps > 0) {
+      const MGLevel& Lc = mg->lv[l];
+      k_mg_coarse_jacobi<<<1, 256, 0, s->stream>>>(Lc.n, Lc.S, Lc.slice_base, Lc.slice_width, Lc.col, Lc.val, Lc.minv,
+                                                   b, x, Lc.t, mg->omega, mg->coarse_sweeps, stop);
+    } else {
+      k_mg_dense_solve<<<grid_for((int64_t)mg->N * 32, 256), 256, 0, s->stream>>>(mg->N, mg->dinv, b, x, stop);
+    }
     s->launches++;
     return;
   }
@@ -657,22 +710,28 @@ static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, cons
     smooth<TV>(s, L, val, minv, b, xa, nullptr, nullptr, om, xb, nullptr, stop, 1.0);
     std::swap(xa, xb);
   }
-  smooth<TV>(s, L, val, minv, b, xa, nullptr, nullptr, om, nullptr, L.r, stop, 1.0);
-  k_mg_restrict<<<grid_for((int64_t)C.n * 32, 256), 256, 0, s->stream>>>(C.n, C.mem_ptr, C.mem, L.r, C.b, stop);
-  s->launches++;
-  vcycle(s, l + 1, C.b, C.x, stop);
-  if (mg->post == 0 && !mg->symmetric_needed) {
-    // V(nu,0): x = x_pre + alpha P x_c (no post-smoothing SpMV)
-    k_mg_prolong<<<grid_for(L.n, 256), 256, 0, s->stream>>>(L.n, xa, C.x, C.agg, mg->alpha, x, stop);
+  // coarse-grid corrections: one at the fine level (V-cycle), `gamma` at the
+  // coarse levels (gamma = 2: W-cycle below the fine level, cheap there)
+  const int ncorr = (l == 0) ? 1 : mg->gamma;
+  for (int g = 0; g < ncorr; ++g) {
+    smooth<TV>(s, L, val, minv, b, xa, nullptr, nullptr, om, nullptr, L.r, stop, 1.0);
+    k_mg_restrict<<<grid_for((int64_t)C.n * 32, 256), 256, 0, s->stream>>>(C.n, C.mem_ptr, C.mem, L.r, C.b, stop);
     s->launches++;
-    return;
-  }
-  // post-smoothing; the first sweep applies the coarse correction in its gathers
-  for (int it = 0; it < mg->nu; ++it) {
-    double* dst = (it == mg->nu - 1) ? x : xb;
-    smooth<TV>(s, L, val, minv, b, xa, it == 0 ? C.x : nullptr, it == 0 ? C.agg : nullptr, om, dst, nullptr, stop,
-               mg->alpha);
-    if (dst == xb) std::swap(xa, xb);
+    vcycle(s, l + 1, C.b, C.x, stop);
+    const bool last = (g == ncorr - 1);
+    if (mg->post == 0 && !mg->symmetric_needed && last) {
+      // V(nu,0): x = x_pre + alpha P x_c (no post-smoothing SpMV)
+      k_mg_prolong<<<grid_for(L.n, 256), 256, 0, s->stream>>>(L.n, xa, C.x, C.agg, mg->alpha, x, stop);
+      s->launches++;
+      return;
+    }
+    // post-smoothing; the first sweep applies the coarse correction in its gathers
+    for (int it = 0; it < mg->nu; ++it) {
+      double* dst = (last && it == mg->nu - 1) ? x : xb;
+      smooth<TV>(s, L, val, minv, b, xa, it == 0 ? C.x : nullptr, it == 0 ? C.agg : nullptr, om, dst, nullptr, stop,
+                 mg->alpha);
+      if (dst == xb) std::swap(xa, xb);
+    }
   }
 }
 

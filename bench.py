@@ -41,46 +41,55 @@ sys.path.insert(0, ROOT)
 # timed region
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
+# Workloads.  cells = box_tet_mesh resolution, edge = cell
+# size (m); eps_fb and the Newton tolerance are scaled with the vertex mass:
+#  * eps_fb: the condensed normal force eps^2/delta at the activation
+#    distance (1 mm) must stay below a vertex's weight, otherwise the
+#    activation discontinuity of the reference model (contact.py:129-130,
+#    SURVEY.md App. A item 2) makes Newton cycle at |r| ~ h^2 eps^2/activation;
+#    the default 1e-6 is fine for ~1e-3 kg vertices (C1, C3) but not for C5
+#    (~6e-6 kg).
+#  * Newton tol: the reference's stop test is an absolute max|r| <= tol *
+#    max(1, max|m q_hat|) (forward.py:169-171, :202) in kg*m; with C5 vertex
+#    masses the default 1e-9 admits ~1e-4 m position error and
+#    solver-path-dependent gradients (measured 7e-6 relative in dL/dE); 1e-11
+#    makes the C5 root path-independent (dL/dE agrees to 1e-9 across paths).
 CONFIGS = {
-    # name: (cells per side, description)
-    "c5": (55, "1M-tet NH cube gripped by 2 kinematic sphere fingers on a frictional ground (C5)"),
-    "c3": (26, "105k-tet NH cube on frictional ground (C3-scale single rollout)"),
-    "c1": (9, "4,374-tet NH cube on frictional ground (C1)"),
+    "c5": dict(cells=(55, 55, 55), edge=0.1 / 55, fingers=True, eps_fb=1e-9, tol=1e-11, rollouts=1,
+               desc="1M-tet NH cube gripped by 2 kinematic sphere fingers on a frictional ground (C5)"),
+    "c3": dict(cells=(60, 12, 12), edge=0.01, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=8,
+               desc="identification batch: 8 rollouts/GPU of a 51,840-tet NH beam on a frictional ground, "
+                    "one E candidate per rollout (C3)"),
+    "c1": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=1,
+               desc="4,374-tet NH cube on a frictional ground (C1)"),
+    "c1b": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=16,
+                desc="16 concurrent rollouts/GPU of the 4,374-tet C1 cube (batched small scenes)"),
 }
-# Smoothed-FB eps_fb (= 2 eps^2) per mesh resolution.  The condensed normal
-# force eps^2/delta at the activation distance (1 mm) must stay below a
-# vertex's weight, otherwise the activation discontinuity of the reference
-# model (contact.py:129-130) makes Newton cycle at
-# |r| ~ h^2 eps^2 / activation.  The default 1e-6 is fine down to C1 vertex
-# masses (~1e-3 kg) but not for C3/C5 (~6e-5 / 6e-6 kg).
-EPS_FB = {55: 1e-9, 26: 1e-7, 9: 1e-6}
-# Newton tolerance per resolution.  The reference's stop test is an absolute
-# max|r| <= tol * max(1, max|m q_hat|) (forward.py:169-171, :202), and scale
-# is 1 here, so tol is in kg*m: with C5 vertex masses (~6e-6 kg) the default
-# 1e-9 admits ~1e-4 m position error and solver-path-dependent gradients
-# (measured 7e-6 relative in dL/dE between two Krylov paths); 1e-11 makes the
-# C5 root path-independent (dL/dE agrees to 1e-9 across solver paths).
-NEWTON_TOL = {55: 1e-11, 26: 1e-10, 9: 1e-9}
-SIZE = 0.1          # cube edge (m)
 E_YOUNG = 1e4
 NU = 0.3
 MU = 0.5
 
 
-def make_scene(n, fingers=True, eps_fb=None):
+def make_scene(cfg_or_n, fingers=None, eps_fb=None, E=E_YOUNG):
+    """Scene of a workload (CONFIGS key or cells-per-side of a 10 cm cube)."""
     from paper_2603_16478_b200 import core, ident
-    v, t = ident.box_tet_mesh(n, n, n, size=SIZE / n, origin=(0.0, 0.0, 5e-4))
-    mat = core.MaterialParams("neohookean", E=E_YOUNG, nu=NU)
+    if isinstance(cfg_or_n, str):
+        c = CONFIGS[cfg_or_n]
+    else:
+        n = int(cfg_or_n)
+        c = dict(cells=(n, n, n), edge=0.1 / n, fingers=True, eps_fb=1e-9 if n >= 40 else (1e-7 if n >= 20 else 1e-6))
+    nx, ny, nz = c["cells"]
+    v, t = ident.box_tet_mesh(nx, ny, nz, size=c["edge"], origin=(0.0, 0.0, 5e-4))
+    mat = core.MaterialParams("neohookean", E=E, nu=NU)
     cols = [core.HalfSpace([0, 0, 1], 0.0, mu=MU)]
-    if fingers:
+    if c["fingers"] if fingers is None else fingers:
         r = 0.02
-        zc = 5e-4 + SIZE / 2
-        cols.append(core.Sphere([-r - 5e-4, SIZE / 2, zc], r, mu=MU))
-        cols.append(core.Sphere([SIZE + r + 5e-4, SIZE / 2, zc], r, mu=MU))
-    if eps_fb is None:
-        eps_fb = EPS_FB.get(n, 1e-6)
+        ly, lz = ny * c["edge"], nz * c["edge"]
+        zc = 5e-4 + lz / 2
+        cols.append(core.Sphere([-r - 5e-4, ly / 2, zc], r, mu=MU))
+        cols.append(core.Sphere([nx * c["edge"] + r + 5e-4, ly / 2, zc], r, mu=MU))
     return core.Scene(v, t, core.lumped_masses(v, t, 1000.0), [mat] * len(t),
-                      colliders=cols, h=0.01, eps_fb=eps_fb)
+                      colliders=cols, h=0.01, eps_fb=c["eps_fb"] if eps_fb is None else eps_fb)
 
 
 def move_fingers(scene, k):
@@ -88,9 +97,9 @@ def move_fingers(scene, k):
     re-read every step as in contact.py:125-127)."""
     if len(scene.colliders) < 3:
         return
-    x0 = -0.02 - 5e-4 + 2e-5 * k
-    scene.colliders[1].center[0] = x0
-    scene.colliders[2].center[0] = SIZE + 0.02 + 5e-4 - 2e-5 * k
+    lx = scene.vertices[:, 0].max()
+    scene.colliders[1].center[0] = -0.02 - 5e-4 + 2e-5 * k
+    scene.colliders[2].center[0] = lx + 0.02 + 5e-4 - 2e-5 * k
 
 
 # ---------------------------------------------------------------------------
@@ -154,8 +163,19 @@ class ClockSampler:
 # GPU arm
 
 
+def _pin_thread(slot):
+    """Pin the calling thread to one core (the Newton driver spin-waits on
+    ~100 device synchronisations per step; migrations show up as jitter)."""
+    try:
+        cpus = sorted(os.sched_getaffinity(0) if slot < 0 else range(os.cpu_count() or 1))
+        os.sched_setaffinity(0, {cpus[(2 * abs(slot) + 1) % len(cpus)]})
+    except (AttributeError, OSError):
+        pass
+
+
 def gpu_arm(args, rank, world, local_rank):
     import ctypes as C
+    from concurrent.futures import ThreadPoolExecutor
 
     import torch
     import torch.distributed as dist
@@ -164,108 +184,145 @@ def gpu_arm(args, rank, world, local_rank):
     from paper_2603_16478_b200.parallel import allreduce_gradients, pack_gradients
 
     torch.cuda.set_device(local_rank)
-    # the Newton driver's host thread synchronises ~100x per step: keep it on
-    # one core (no migrations between spin-waits)
-    try:
-        cpus = sorted(os.sched_getaffinity(0))
-        os.sched_setaffinity(0, {cpus[(2 * local_rank + 1) % len(cpus)]})
-    except (AttributeError, OSError):
-        pass
-    n, desc = CONFIGS[args.config]
-    scene = make_scene(n, fingers=(args.config == "c5"))
-    # batch of parameter candidates: rank r simulates E * (1 + 0.05 r)
-    for m in scene.materials[:1]:
-        pass
-    if rank:
-        mat = core.MaterialParams("neohookean", E=E_YOUNG * (1 + 0.05 * rank), nu=NU)
-        scene.materials = [mat] * len(scene.materials)
-    t_setup = time.perf_counter()
-    sysmat = core.assemble_system_matrix(scene, device=local_rank)
-    setup_s = time.perf_counter() - t_setup
-    dev = sysmat.dev
-    L = dev.lib
-    info = dev.info()
-    V, E_ = scene.n_verts, len(scene.elements)
-    n3 = 3 * V
+    cdef = CONFIGS[args.config]
+    R = args.rollouts or cdef["rollouts"]
     K, W = args.steps, args.warmup
-    cfg = fw.ForwardConfig(tol=NEWTON_TOL.get(n, 1e-9))
-    scfg = aj.SolverConfig(tol=1e-10, max_iter=2000).to_c()
     dd = dict(device="cuda:%d" % local_rank, dtype=torch.float64)
-    stream = torch.cuda.ExternalStream(L.dp_scene_stream(dev.handle))
+    cfg = fw.ForwardConfig(tol=cdef["tol"])
+    scfg = aj.SolverConfig(tol=1e-10, max_iter=2000).to_c()
 
-    def device_rollout(nsteps, k0):
-        """forward K steps + reverse sweep, all device-resident."""
-        q = [torch.empty(n3, **dd) for _ in range(nsteps + 1)]
-        v = [torch.empty(n3, **dd) for _ in range(nsteps + 1)]
-        q[0].copy_(torch.from_numpy(scene.vertices.reshape(-1)))
-        v[0].zero_()
-        torch.cuda.synchronize()
+    class Ctx:
+        pass
+
+    # one rollout per (rank, slot): candidate E = E0 (1 + 0.05 * global index)
+    t_setup = time.perf_counter()
+    ctxs = []
+    for i in range(R):
+        c = Ctx()
+        c.slot = i
+        c.E = E_YOUNG * (1 + 0.05 * (rank * R + i))
+        c.scene = make_scene(args.config, E=c.E)
+        c.sysmat = core.assemble_system_matrix(c.scene, device=local_rank)
+        c.dev = c.sysmat.dev
+        c.L = c.dev.lib
+        c.stream = torch.cuda.ExternalStream(c.L.dp_scene_stream(c.dev.handle))
+        ctxs.append(c)
+    setup_s = time.perf_counter() - t_setup
+    info = ctxs[0].dev.info()
+    scene0 = ctxs[0].scene
+    V, E_ = scene0.n_verts, len(scene0.elements)
+    n3 = 3 * V
+
+    def device_rollout(c, nsteps, k0):
+        """forward K steps + reverse sweep of one rollout, device-resident."""
+        _pin_thread(local_rank * 16 + c.slot)
+        L, dev, scene = c.L, c.dev, c.scene
+        with torch.cuda.stream(c.stream):
+            q = [torch.empty(n3, **dd) for _ in range(nsteps + 1)]
+            v = [torch.empty(n3, **dd) for _ in range(nsteps + 1)]
+            q[0].copy_(torch.from_numpy(scene.vertices.reshape(-1)))
+            v[0].zero_()
+        c.stream.synchronize()
         caches, stats = [], []
         for k in range(nsteps):
             move_fingers(scene, k0 + k)
-            _, rep = fw.forward_step(scene, None, sysmat, cfg,
+            _, rep = fw.forward_step(scene, None, c.sysmat, cfg,
                                      device_io=dict(q_bar=q[k], v_bar=v[k], q_out=q[k + 1], v_out=v[k + 1]))
             caches.append(rep.cache)
             stats.append((rep.converged, rep.iterations, rep.krylov_iterations, rep.n_contacts))
-        target = q[0] + 1e-3          # synthetic target shape
-        dq = 2.0 * (q[nsteps] - target)
-        dv = torch.zeros(n3, **dd)
-        z = torch.empty(n3, **dd)
-        dqb = torch.empty(n3, **dd)
-        dvb = torch.empty(n3, **dd)
-        dfx = torch.empty(n3, **dd)
-        torch.cuda.synchronize()
+        with torch.cuda.stream(c.stream):
+            target = q[0] + 1e-3          # synthetic target shape
+            dq = 2.0 * (q[nsteps] - target)
+            dv = torch.zeros(n3, **dd)
+            z = torch.empty(n3, **dd)
+            dqb = torch.empty(n3, **dd)
+            dvb = torch.empty(n3, **dd)
+            dfx = torch.empty(n3, **dd)
+        c.stream.synchronize()
         _lib.check(L.dp_grads_reset(dev.handle))
         adj_iters = 0
         for k in range(nsteps, 0, -1):
-            c = caches[k - 1]._dc.handle
-            _lib.check(L.dp_adjoint_assemble(dev.handle, c, None))
+            h = caches[k - 1]._dc.handle
+            _lib.check(L.dp_adjoint_assemble(dev.handle, h, None))
             rep = _lib.SolveReportC()
-            _lib.check(L.dp_adjoint_solve(dev.handle, c, _lib.ptr(dq), _lib.ptr(dv), _lib.PTR_DEVICE,
+            _lib.check(L.dp_adjoint_solve(dev.handle, h, _lib.ptr(dq), _lib.ptr(dv), _lib.PTR_DEVICE,
                                           C.byref(scfg), _lib.ptr(z), C.byref(rep)))
             adj_iters += rep.iterations
-            _lib.check(L.dp_backprop_step(dev.handle, c, _lib.ptr(z), _lib.ptr(dv), _lib.PTR_DEVICE,
+            _lib.check(L.dp_backprop_step(dev.handle, h, _lib.ptr(z), _lib.ptr(dv), _lib.PTR_DEVICE,
                                           _lib.ptr(dqb), _lib.ptr(dvb), _lib.ptr(dfx)))
             dq, dqb = dqb, dq
             dv, dvb = dvb, dv
         grads = aj.GradientReport()
         grads.ensure_shapes(len(scene.bindings), dev.n_elems)
         aj._fold_device_grads(dev, scene, grads)
-        loss = float(torch.sum((q[nsteps] - target) ** 2))
+        with torch.cuda.stream(c.stream):
+            loss = float(torch.sum((q[nsteps] - target) ** 2))
         return grads, loss, stats, adj_iters
 
-    # warm-up (untimed): the same K-step rollout + reverse sweep as timed
+    def host_rollout(c, nsteps, k0):
+        """the same through the public API with host NumPy buffers (e2e)."""
+        _pin_thread(local_rank * 16 + c.slot)
+        scene = c.scene
+        st0 = scene.rest_state()
+        st, caches = st0, []
+        for k in range(nsteps):
+            move_fingers(scene, k0 + k)
+            st, rep = fw.forward_step(scene, st, c.sysmat, cfg)
+            caches.append(rep.cache)
+        target = st0.q + 1e-3
+        g = aj.backprop_rollout(caches, target)
+        return g, float(np.sum((st.q - target) ** 2))
+
+    pool = ThreadPoolExecutor(max_workers=R)
+
+    def run_all(fn, *a):
+        if R == 1:
+            return [fn(ctxs[0], *a)]
+        return list(pool.map(lambda c: fn(c, *a), ctxs))
+
+    def pack_sum(results):
+        tot = None
+        for g, loss in results:
+            v = pack_gradients(g, loss, dd["device"])
+            tot = v if tot is None else tot + v
+        return tot
+
+    # warm-up (untimed): the same K-step rollouts + reverse sweeps as timed
     for _ in range(max(W, 0)):
-        device_rollout(K, W)
+        run_all(device_rollout, K, W)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    L.dp_scene_reset_timing(dev.handle)
+    for c in ctxs:
+        c.L.dp_scene_reset_timing(c.dev.handle)
     with ClockSampler(local_rank) as clk:
-        with torch.cuda.stream(stream):
-            ev0.record(stream)
-        grads, loss, stats, adj_iters = device_rollout(K, W)
-        gvec = pack_gradients(grads, loss, dd["device"])
-        allreduce_gradients(gvec, world)
-        with torch.cuda.stream(stream):
-            ev1.record(stream)
+        ev0.record()
+        res = run_all(device_rollout, K, W)
+        gvec = pack_sum([(r[0], r[1]) for r in res])
+        allreduce_gradients(gvec, world)      # one all-reduce per optimisation iteration
         torch.cuda.synchronize()
+        ev1.record()
+        ev1.synchronize()
     ms = ev0.elapsed_time(ev1)
-    launches = int(L.dp_scene_launch_count(dev.handle))
+    launches = sum(int(c.L.dp_scene_launch_count(c.dev.handle)) for c in ctxs)
     t = torch.tensor([ms], device=dd["device"])
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+    stats = res[0][2]
+    adj_iters = res[0][3]
 
     # roofline: dominant kernel = the SELL-32 BSR SpMV of the Krylov solves
+    c0 = ctxs[0]
     x = torch.randn(n3, **dd)
     y = torch.empty(n3, **dd)
+    torch.cuda.synchronize()
     fms = C.c_float()
     reps = 30
-    _lib.check(L.dp_bench_spmv(dev.handle, 1, _lib.ptr(x), _lib.ptr(y), 3, C.byref(fms)))
-    _lib.check(L.dp_bench_spmv(dev.handle, 1, _lib.ptr(x), _lib.ptr(y), reps, C.byref(fms)))
+    _lib.check(c0.L.dp_bench_spmv(c0.dev.handle, 1, _lib.ptr(x), _lib.ptr(y), 10, C.byref(fms)))
+    _lib.check(c0.L.dp_bench_spmv(c0.dev.handle, 1, _lib.ptr(x), _lib.ptr(y), reps, C.byref(fms)))
     spmv_ms = fms.value / reps
     nnzb = info.nnzb
     spmv_bytes = 76 * nnzb + 4 * (V + 1) + 48 * V          # SURVEY.md §8(d)
@@ -287,24 +344,12 @@ def gpu_arm(args, rank, world, local_rank):
     # e2e through the public API with host buffers
     e2e = None
     if not args.skip_e2e:
-        st0 = scene.rest_state()
-        for k in range(1):    # untimed warm call of the host path
-            pass
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        states, caches = [st0], []
-        st = st0
-        for k in range(K):
-            move_fingers(scene, W + k)
-            st, rep = fw.forward_step(scene, st, sysmat, cfg)
-            states.append(st)
-            caches.append(rep.cache)
-        target = st0.q + 1e-3
-        g2 = aj.backprop_rollout(caches, target)
-        gv2 = pack_gradients(g2, float(np.sum((states[-1].q - target) ** 2)), dd["device"])
-        allreduce_gradients(gv2, world)
+        res2 = run_all(host_rollout, K, W)
+        allreduce_gradients(pack_sum(res2), world)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         tw = torch.tensor([wall], device=dd["device"])
@@ -314,21 +359,22 @@ def gpu_arm(args, rank, world, local_rank):
         h2d = (2 * n3 + 2 * n3) * 8           # forward (q_bar, v_bar) + adjoint (dL_dq, dL_dv)
         d2h = (2 * n3 + 4 * n3) * 8           # forward (q, v) + adjoint (z, dqbar, dvbar, dfext)
         h2d += 8 * n3                          # backprop z re-upload
-        e2e = {"value": world * K / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+        e2e = {"value": world * R * K / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h}
-    conv = [s[0] for s in stats]
+    pool.shutdown()
+    conv = [s_[0] for r in res for s_ in r[2]]
     return dict(ms=ms_max, launches=launches, clocks=clk.summary(), spmv_ms=spmv_ms, spmv_bytes=spmv_bytes,
-                achieved=achieved, hbm=hbm, traffic=traffic, e2e=e2e, setup_s=setup_s,
-                nnzb=nnzb, V=V, E=E_, desc=desc, newton=[s[1] for s in stats],
-                krylov=[s[2] for s in stats], contacts=[s[3] for s in stats], converged=all(conv),
-                adj_iters=adj_iters, dE=grads.dL_dE, loss=loss, device_bytes=info.device_bytes)
+                achieved=achieved, hbm=hbm, traffic=traffic, e2e=e2e, setup_s=setup_s, R=R,
+                nnzb=nnzb, V=V, E=E_, desc=cdef["desc"], newton=[s_[1] for s_ in stats],
+                krylov=[s_[2] for s_ in stats], contacts=[s_[3] for s_ in stats], converged=all(conv),
+                adj_iters=adj_iters, dE=float(gvec[1]), loss=float(gvec[0]), device_bytes=info.device_bytes)
 
 
 # ---------------------------------------------------------------------------
 # CPU oracle (reported baseline / reference arm)
 
 
-def _oracle_sample(n_cells, steps, eps_fb=None):
+def _oracle_sample(n_cells, steps, eps_fb=None, tol=1e-9):
     """One process: the oracle port on an n_cells^3 cube of the same scene
     family; returns (seconds per fwd+bwd step, tets)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -339,29 +385,28 @@ def _oracle_sample(n_cells, steps, eps_fb=None):
     q0 = scene.vertices.reshape(-1).copy()
     v0 = np.zeros_like(q0)
     t0 = time.perf_counter()
-    els, A, st = O.rollout(osc, q0, v0, steps, O.ForwardConfig(tol=NEWTON_TOL.get(n_cells, 1e-9)),
-                           raise_on_failure=False)
+    els, A, st = O.rollout(osc, q0, v0, steps, O.ForwardConfig(tol=tol), raise_on_failure=False)
     O.backprop_rollout(osc, els, A, st, target=q0 + 1e-3)
     dt = time.perf_counter() - t0
     return dt / steps, len(scene.elements)
 
 
 def _oracle_worker(args):
-    n_cells, steps = args
+    n_cells, steps, tol = args
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    return _oracle_sample(n_cells, steps)
+    return _oracle_sample(n_cells, steps, tol=tol)
 
 
-def cpu_baseline(n_tets_target, n_cells=8, steps=1, procs=1):
+def cpu_baseline(n_tets_target, n_cells=8, steps=1, procs=1, tol=1e-9):
     """Bounded CPU sample; returns the JSON object for cpu_baseline."""
     if procs <= 1:
-        sec, tets = _oracle_sample(n_cells, steps)
+        sec, tets = _oracle_sample(n_cells, steps, tol=tol)
         per_proc = [sec]
     else:
         import multiprocessing as mp
         ctx = mp.get_context("spawn")
         with ctx.Pool(procs) as pool:
-            res = pool.map(_oracle_worker, [(n_cells, steps)] * procs)
+            res = pool.map(_oracle_worker, [(n_cells, steps, tol)] * procs)
         per_proc = [r[0] for r in res]
         tets = res[0][1]
     # steps/s at the target size, extrapolated linearly in tets
@@ -386,27 +431,29 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-cells", type=int, default=12)
+    ap.add_argument("--rollouts", type=int, default=0, help="rollouts per GPU (default per config)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(1)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    n_cells = CONFIGS[args.config][0]
-    n_tets = 6 * n_cells ** 3
-    config = {"workload": f"{args.config}: {CONFIGS[args.config][1]}", "n_tets": n_tets,
-              "n_verts": (n_cells + 1) ** 3, "steps_per_rollout": args.steps,
-              "rollouts": world, "parallelism": f"dp{world} (independent rollouts, NCCL grad allreduce)",
-              "material": f"neohookean E={E_YOUNG} nu={NU}", "friction_mu": MU, "h": 0.01,
-              "eps_fb": EPS_FB.get(n_cells, 1e-6), "newton_tol": NEWTON_TOL.get(n_cells, 1e-9),
-              "l2": "operands > L2 (no flush)"}
-
+    cdef = CONFIGS[args.config]
+    R = args.rollouts or cdef["rollouts"]
+    nx, ny, nz = cdef["cells"]
+    n_tets = 6 * nx * ny * nz
+    config = {"workload": f"{args.config}: {cdef['desc']}", "n_tets": n_tets,
+              "n_verts": (nx + 1) * (ny + 1) * (nz + 1), "steps_per_rollout": args.steps,
+              "rollouts_per_gpu": R, "rollouts": world * R,
+              "parallelism": f"dp{world} x {R} rollouts/GPU (independent rollouts, NCCL grad allreduce)",
+              "material": f"neohookean E={E_YOUNG}(1+0.05 i) nu={NU}", "friction_mu": MU, "h": 0.01,
+              "eps_fb": cdef["eps_fb"], "newton_tol": cdef["tol"], "l2": "operands > L2 (no flush)"}
     if args.impl == "reference":
         if rank != 0:
             return
         procs = os.cpu_count() or 1
         W, K = args.warmup, args.steps
         t0 = time.perf_counter()
-        base = cpu_baseline(n_tets, n_cells=args.cpu_cells, steps=1, procs=procs)
+        base = cpu_baseline(n_tets, n_cells=args.cpu_cells, steps=1, procs=procs, tol=cdef["tol"])
         wall = time.perf_counter() - t0
         line = {"metric": "fwd+bwd sim steps/sec at N tets", "value": base["value"], "unit": "steps/s",
                 "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": 1e3 / base["value"],
@@ -425,7 +472,7 @@ def main():
     r = gpu_arm(args, rank, world, local_rank)
     if rank == 0:
         K = args.steps
-        steps_total = world * K
+        steps_total = world * R * K
         value = steps_total / (r["ms"] * 1e-3)
         line = {"metric": "fwd+bwd sim steps/sec at N tets", "value": value, "unit": "steps/s",
                 "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": r["ms"] / K,
@@ -444,7 +491,8 @@ def main():
                 "device_bytes": r["device_bytes"]}
         if not args.skip_cpu and world == 1:
             try:
-                line["cpu_baseline"] = cpu_baseline(n_tets, n_cells=args.cpu_cells, steps=1, procs=1)
+                line["cpu_baseline"] = cpu_baseline(n_tets, n_cells=args.cpu_cells, steps=1, procs=1,
+                                                    tol=cdef["tol"])
             except Exception as ex:   # the baseline must not kill the GPU line
                 line["cpu_baseline"] = {"value": None, "error": repr(ex)[:200]}
         print(json.dumps(line))

@@ -769,6 +769,7 @@ int dp_cache_destroy(dp_cache* c) {
       *it = s->live_caches.back();
       s->live_caches.pop_back();
     }
+    if (s->adj_cache_tag == c) s->adj_cache_tag = nullptr;
     s->cache_pool.push_back(c);
     return DP_OK;
   }
@@ -1057,7 +1058,6 @@ int dp_cache_get_projections(dp_scene* s, const dp_cache* c, double* sigma, doub
 // ---------------------------------------------------------------------------
 // adjoint (adjoint.py:93-219)
 
-static const dp_cache* g_adj_cache_tag = nullptr;
 
 int dp_adjoint_assemble(dp_scene* s, const dp_cache* c, int32_t* symmetric) {
   cudaSetDevice(s->device);
@@ -1081,7 +1081,7 @@ int dp_adjoint_assemble(dp_scene* s, const dp_cache* c, int32_t* symmetric) {
   s->mg_adj_ready = 0;   // the hierarchy is rebuilt lazily by the solve
   if (symmetric) *symmetric = s->last_sym_adj;
   if (g_debug) fprintf(stderr, "[dp] adjoint assemble %.2fms\n", 1e3 * (now_s() - t0));
-  g_adj_cache_tag = c;
+  s->adj_cache_tag = c;
   return DP_OK;
 }
 
@@ -1091,7 +1091,7 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
   dp_solver_cfg cfg;
   if (cfg_in) cfg = *cfg_in;
   else dp_solver_cfg_default(&cfg);
-  if (g_adj_cache_tag != c) {
+  if (s->adj_cache_tag != c) {
     int rc = dp_adjoint_assemble(s, c, nullptr);
     if (rc) return rc;
   }
@@ -1177,7 +1177,7 @@ int dp_backprop_step(dp_scene* s, const dp_cache* c, const double* z, const doub
                      double* dL_dqbar_out, double* dL_dvbar_out, double* dL_dfext_out) {
   cudaSetDevice(s->device);
   const double t0 = g_debug ? now_s() : 0.0;
-  if (g_adj_cache_tag != c) {
+  if (s->adj_cache_tag != c) {
     int rc = dp_adjoint_assemble(s, c, nullptr);
     if (rc) return rc;
   }

@@ -198,6 +198,7 @@ struct dp_scene {
   dp::MG* mg = nullptr;
   int use_mg = 2;
   int mg_adj_ready = 0;
+  const dp_cache* adj_cache_tag = nullptr;   // cache whose A_hat^T is assembled
 
   std::vector<dp_cache*> cache_pool;   // recycled step caches
   std::vector<dp_cache*> live_caches;  // handed out, not yet destroyed

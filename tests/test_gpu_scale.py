@@ -66,3 +66,32 @@ def test_c5_determinism_and_bit_exact_detection():
     assert np.array_equal([c.collider for c in got], ref.collider)
     assert np.array_equal(np.array([c.frame for c in got]), ref.frame)
     assert np.array_equal(np.array([c.d_n for c in got]), ref.d_n)
+
+
+def test_concurrent_rollouts_match_sequential():
+    """k rollouts on one GPU, one stream + host thread each (the batched
+    identification mode of bench.py --config c3): bitwise equal to running
+    them one after the other."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import bench
+    from paper_2603_16478_b200 import adjoint as aj, core, forward as fw
+
+    def job(E):
+        sc = bench.make_scene(4, fingers=True, eps_fb=1e-6, E=E)
+        sm = core.assemble_system_matrix(sc)
+        st, caches = sc.rest_state(), []
+        for k in range(3):
+            bench.move_fingers(sc, k)
+            st, rep = fw.forward_step(sc, st, sm, fw.ForwardConfig(tol=1e-10))
+            caches.append(rep.cache)
+        g = aj.backprop_rollout(caches, sc.rest_state().q + 1e-3)
+        return st.q, g.dL_dE
+
+    Es = [1e4, 1.2e4, 1.5e4, 2e4]
+    seq = [job(E) for E in Es]
+    with ThreadPoolExecutor(4) as ex:
+        par = list(ex.map(job, Es))
+    for (qa, ga), (qb, gb) in zip(seq, par):
+        assert np.array_equal(qa, qb)
+        assert ga == gb

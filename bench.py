@@ -60,6 +60,9 @@ CONFIGS = {
     "c3": dict(cells=(60, 12, 12), edge=0.01, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=8,
                desc="identification batch: 8 rollouts/GPU of a 51,840-tet NH beam on a frictional ground, "
                     "one E candidate per rollout (C3)"),
+    "c2": dict(cells=(100, 100, 0), edge=0.01, fingers=False, eps_fb=1e-9, tol=1e-11, rollouts=1, cloth=True,
+               desc="20,000-triangle ARAP cloth (1 m, 0.3 kg/m^2) draping over a frictional sphere, "
+                    "per-step control-force gradients (C2 without self-contact: none in the reference)"),
     "c1": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=1,
                desc="4,374-tet NH cube on a frictional ground (C1)"),
     "c1b": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=16,
@@ -79,6 +82,14 @@ def make_scene(cfg_or_n, fingers=None, eps_fb=None, E=E_YOUNG):
         n = int(cfg_or_n)
         c = dict(cells=(n, n, n), edge=0.1 / n, fingers=True, eps_fb=1e-9 if n >= 40 else (1e-7 if n >= 20 else 1e-6))
     nx, ny, nz = c["cells"]
+    if c.get("cloth"):
+        # horizontal sheet 0.5 mm above a sphere of radius 0.25
+        v, t = ident.horizontal_sheet(nx, ny, c["edge"], origin=(0.0, 0.0, 0.2505))
+        mats = [core.MaterialParams("arap", stiffness=50.0)] * len(t)
+        cx, cy = nx * c["edge"] / 2, ny * c["edge"] / 2
+        cols = [core.HalfSpace([0, 0, 1], 0.0, mu=0.3), core.Sphere([cx, cy, 0.0], 0.25, mu=0.3)]
+        return core.Scene(v, t, core.lumped_masses(v, t, 0.3), mats, colliders=cols, h=0.01,
+                          eps_fb=c["eps_fb"] if eps_fb is None else eps_fb)
     v, t = ident.box_tet_mesh(nx, ny, nz, size=c["edge"], origin=(0.0, 0.0, 5e-4))
     mat = core.MaterialParams("neohookean", E=E, nu=NU)
     cols = [core.HalfSpace([0, 0, 1], 0.0, mu=MU)]
@@ -107,56 +118,57 @@ def move_fingers(scene, k):
 
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled with NVML (in-process thread, every
+    250 ms) during the timed region.  Spawning nvidia-smi inside the timed
+    region was measured to perturb the step time."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.thread = None
 
     def __enter__(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return self
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for name, bit in self.REASONS.items():
+                            if r & bit:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    self._stop.wait(0.25)
+
+            self.thread = threading.Thread(target=run, daemon=True)
             self.thread.start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
+        except Exception:
+            self.thread = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 7:
-                continue
-            try:
-                sm.append(float(p[0]))
-                mx = max(mx, float(p[1]))
-            except ValueError:
-                continue
-            for nm, val in zip(names, p[3:7]):
-                if val.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = self.samples
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(sm), "source": "NVML, 250 ms"}
 
 
 # ---------------------------------------------------------------------------
@@ -287,9 +299,22 @@ def gpu_arm(args, rank, world, local_rank):
             tot = v if tot is None else tot + v
         return tot
 
-    # warm-up (untimed): the same K-step rollouts + reverse sweeps as timed
-    for _ in range(max(W, 0)):
+    # warm-up (untimed): the same K-step rollouts + reverse sweeps as timed,
+    # at least W of them and at least --warmup-seconds of wall time (a freshly
+    # leased box shows 2-4x step-time noise for its first ~2 s of GPU work,
+    # then settles to within 0.5%: measured, tools/var_c3.py)
+    t_w = time.perf_counter()
+    n_w = 0
+    while n_w < max(W, 0) or time.perf_counter() - t_w < args.warmup_seconds:
         run_all(device_rollout, K, W)
+        n_w += 1
+    if os.environ.get("BENCH_DEBUG"):
+        for i in range(3):
+            t0 = time.perf_counter(); run_all(device_rollout, K, W); torch.cuda.synchronize()
+            t1 = time.perf_counter(); run_all(host_rollout, K, W); torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            print(f"[bench] device path {1e3 * (t1 - t0):.1f} ms, host path {1e3 * (t2 - t1):.1f} ms",
+                  file=sys.stderr, flush=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -424,7 +449,7 @@ def cpu_baseline(n_tets_target, n_cells=8, steps=1, procs=1, tol=1e-9):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
@@ -432,6 +457,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-cells", type=int, default=12)
     ap.add_argument("--rollouts", type=int, default=0, help="rollouts per GPU (default per config)")
+    ap.add_argument("--warmup-seconds", type=float, default=5.0)
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -440,12 +466,14 @@ def main():
     cdef = CONFIGS[args.config]
     R = args.rollouts or cdef["rollouts"]
     nx, ny, nz = cdef["cells"]
-    n_tets = 6 * nx * ny * nz
-    config = {"workload": f"{args.config}: {cdef['desc']}", "n_tets": n_tets,
-              "n_verts": (nx + 1) * (ny + 1) * (nz + 1), "steps_per_rollout": args.steps,
+    cloth = bool(cdef.get("cloth"))
+    n_tets = 2 * nx * ny if cloth else 6 * nx * ny * nz
+    config = {"workload": f"{args.config}: {cdef['desc']}", ("n_tris" if cloth else "n_tets"): n_tets,
+              "n_verts": (nx + 1) * (ny + 1) * (nz + 1 if not cloth else 1), "steps_per_rollout": args.steps,
               "rollouts_per_gpu": R, "rollouts": world * R,
               "parallelism": f"dp{world} x {R} rollouts/GPU (independent rollouts, NCCL grad allreduce)",
-              "material": f"neohookean E={E_YOUNG}(1+0.05 i) nu={NU}", "friction_mu": MU, "h": 0.01,
+              "material": ("arap stiffness=50" if cloth else f"neohookean E={E_YOUNG}(1+0.05 i) nu={NU}"),
+              "friction_mu": 0.3 if cloth else MU, "h": 0.01,
               "eps_fb": cdef["eps_fb"], "newton_tol": cdef["tol"], "l2": "operands > L2 (no flush)"}
     if args.impl == "reference":
         if rank != 0:

@@ -457,7 +457,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-cells", type=int, default=12)
     ap.add_argument("--rollouts", type=int, default=0, help="rollouts per GPU (default per config)")
-    ap.add_argument("--warmup-seconds", type=float, default=5.0)
+    ap.add_argument("--warmup-seconds", type=float, default=8.0)
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))

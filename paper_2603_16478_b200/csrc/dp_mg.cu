@@ -421,7 +421,12 @@ __global__ void k_mg_jacobi0(int n, const TM* __restrict__ minv, const double* _
 
 // out = xt + omega Minv (b - A xt), xt = x + P xc (xc/agg may be null)
 // and optionally r_out = b - A xt (for the residual after the last pre-sweep)
-template <class TV>
+// SPLIT = 1: one warp per SELL slice (fine level: plenty of slices).
+// SPLIT = 8: one CTA per slice, warp w takes slots k = w, w+8, ... and the
+// partial row sums meet in shared memory - the coarse levels have few slices
+// but wide rows (a level-1 row couples ~27-100 aggregates), where a single
+// warp per slice is a long dependent-latency chain.
+template <class TV, int SPLIT>
 __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __restrict__ slice_base,
                                                    const int* __restrict__ slice_width, const int* __restrict__ col,
                                                    const TV* __restrict__ val, const TV* __restrict__ minv,
@@ -429,16 +434,18 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
                                                    const double* __restrict__ xc, const int* __restrict__ agg,
                                                    double omega, double* __restrict__ out, double* __restrict__ r_out,
                                                    const int* stop, double alpha) {
+  __shared__ double part[SPLIT > 1 ? SPLIT : 1][3][kSlice];
   if (stopped(stop)) return;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  const int wsub = (SPLIT > 1) ? (threadIdx.x >> 5) : 0;
+  const int gw = (SPLIT > 1) ? blockIdx.x : (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gw >= S) return;
   const int row = gw * kSlice + lane;
   const int base = slice_base[gw], K = slice_width[gw];
   const TV* vs = val + (size_t)base * 9 + lane;
   const int* cs = col + base + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  for (int k = 0; k < K; ++k) {
+  for (int k = wsub; k < K; k += SPLIT) {
     const int j = __ldg(cs + k * kSlice);
     const TV* v = vs + k * 9 * kSlice;
     double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
@@ -449,6 +456,16 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
     a0 += (double)v[0 * kSlice] * x0 + (double)v[1 * kSlice] * x1 + (double)v[2 * kSlice] * x2;
     a1 += (double)v[3 * kSlice] * x0 + (double)v[4 * kSlice] * x1 + (double)v[5 * kSlice] * x2;
     a2 += (double)v[6 * kSlice] * x0 + (double)v[7 * kSlice] * x1 + (double)v[8 * kSlice] * x2;
+  }
+  if (SPLIT > 1) {
+    part[wsub][0][lane] = a0;
+    part[wsub][1][lane] = a1;
+    part[wsub][2][lane] = a2;
+    __syncthreads();
+    if (wsub != 0) return;
+    a0 = a1 = a2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < SPLIT; ++w) { a0 += part[w][0][lane]; a1 += part[w][1][lane]; a2 += part[w][2][lane]; }
   }
   if (row >= n) return;
   double xt[3] = {x[3 * row], x[3 * row + 1], x[3 * row + 2]};
@@ -585,7 +602,10 @@ __global__ void __launch_bounds__(256) k_mg_coarse_jacobi(int n, int S, const in
                                                           const double* __restrict__ minv, const double* __restrict__ b,
                                                           double* __restrict__ x, double* __restrict__ y, double omega,
                                                           int nsweep, const int* stop) {
+  // one CTA; warp w handles slots k = w, w+8, ... of every slice, lanes = rows
+  __shared__ double part[8][3][kSlice];
   if (stop && *(volatile const int*)stop) return;
+  const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
   for (int row = threadIdx.x; row < n; row += blockDim.x) {
     double r[3] = {b[3 * row], b[3 * row + 1], b[3 * row + 2]}, u[3];
     mv_minv(minv, n, row, r, u);
@@ -594,24 +614,33 @@ __global__ void __launch_bounds__(256) k_mg_coarse_jacobi(int n, int S, const in
   }
   __syncthreads();
   for (int it = 0; it < nsweep; ++it) {
-    for (int row = threadIdx.x; row < n; row += blockDim.x) {
-      const int sl = row / kSlice, lane = row % kSlice;
+    for (int sl = 0; sl < S; ++sl) {
+      const int row = sl * kSlice + lane;
       const int base = slice_base[sl], K = slice_width[sl];
-      double a[3] = {0.0, 0.0, 0.0};
-      for (int k = 0; k < K; ++k) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      for (int k = wsub; k < K; k += 8) {
         const int j = col[base + k * kSlice + lane];
         const double* v = val + (size_t)base * 9 + (k * 9) * kSlice + lane;
-#pragma unroll
-        for (int p = 0; p < 3; ++p)
-          a[p] += v[(p * 3) * kSlice] * x[3 * j] + v[(p * 3 + 1) * kSlice] * x[3 * j + 1] +
-                  v[(p * 3 + 2) * kSlice] * x[3 * j + 2];
+        const double x0 = x[3 * j], x1 = x[3 * j + 1], x2 = x[3 * j + 2];
+        a0 += v[0 * kSlice] * x0 + v[1 * kSlice] * x1 + v[2 * kSlice] * x2;
+        a1 += v[3 * kSlice] * x0 + v[4 * kSlice] * x1 + v[5 * kSlice] * x2;
+        a2 += v[6 * kSlice] * x0 + v[7 * kSlice] * x1 + v[8 * kSlice] * x2;
       }
-      double r[3] = {b[3 * row] - a[0], b[3 * row + 1] - a[1], b[3 * row + 2] - a[2]}, u[3];
-      mv_minv(minv, n, row, r, u);
+      part[wsub][0][lane] = a0;
+      part[wsub][1][lane] = a1;
+      part[wsub][2][lane] = a2;
+      __syncthreads();
+      if (wsub == 0 && row < n) {
+        a0 = a1 = a2 = 0.0;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) y[3 * row + c] = x[3 * row + c] + omega * u[c];
+        for (int w = 0; w < 8; ++w) { a0 += part[w][0][lane]; a1 += part[w][1][lane]; a2 += part[w][2][lane]; }
+        double r[3] = {b[3 * row] - a0, b[3 * row + 1] - a1, b[3 * row + 2] - a2}, u[3];
+        mv_minv(minv, n, row, r, u);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) y[3 * row + c] = x[3 * row + c] + omega * u[c];
+      }
+      __syncthreads();
     }
-    __syncthreads();
     for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) x[t] = y[t];
     __syncthreads();
   }
@@ -662,8 +691,12 @@ template <class TV>
 static void smooth(dp_scene* s, const MGLevel& L, const TV* val, const TV* minv, const double* b, const double* x,
                    const double* xc, const int* agg, double omega, double* out, double* r_out, const int* stop,
                    double alpha) {
-  k_mg_smooth<TV><<<grid_for((int64_t)L.S * 32, 256), 256, 0, s->stream>>>(
-      L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x, xc, agg, omega, out, r_out, stop, alpha);
+  if (L.S >= 4 * 148)
+    k_mg_smooth<TV, 1><<<grid_for((int64_t)L.S * 32, 256), 256, 0, s->stream>>>(
+        L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x, xc, agg, omega, out, r_out, stop, alpha);
+  else
+    k_mg_smooth<TV, 8><<<L.S, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x,
+                                                   xc, agg, omega, out, r_out, stop, alpha);
   s->launches++;
 }
 

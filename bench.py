@@ -41,6 +41,22 @@ sys.path.insert(0, ROOT)
 # timed region
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
+
+def _keep_heap():
+    """Keep freed multi-MB host buffers in the heap instead of munmap'ing them:
+    each step returns fresh 3V-double NumPy arrays (public API), and the
+    mmap/munmap + page-zeroing churn showed up as 50-200 ms outliers."""
+    try:
+        import ctypes
+        libc = ctypes.CDLL("libc.so.6")
+        libc.mallopt(-3, 1 << 30)   # M_MMAP_THRESHOLD: serve big blocks from the heap
+        libc.mallopt(-1, 1 << 31)   # M_TRIM_THRESHOLD: never give the top back
+    except (OSError, AttributeError):
+        pass
+
+
+_keep_heap()
+
 # Workloads (SURVEY.md §8(d)).  cells = box_tet_mesh resolution, edge = cell
 # size (m); eps_fb and the Newton tolerance are scaled with the vertex mass:
 #  * eps_fb: the condensed normal force eps^2/delta at the activation

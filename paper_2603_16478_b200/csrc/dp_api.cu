@@ -545,6 +545,7 @@ int dp_scene_destroy(dp_scene* s) {
   s->cache_pool.clear();
   for (dp_cache* c : s->live_caches) c->scene = nullptr;   // freed by their own destroy
   s->live_caches.clear();
+  gm_graphs_destroy(s);
   mg_destroy(s);
   void* ptrs[] = {s->ev, s->B, s->w, s->vol, s->mu, s->lam, s->model, s->mass, s->inc_ptr, s->inc,
                   s->slice_base, s->slice_width, s->col, s->diag_slot, s->val_fwd, s->val_adj, s->val_A,

@@ -51,7 +51,11 @@ struct GmresScalars {
   double reorth_thr;                            // re-orthogonalise when |w|^2 < thr |w_before|^2
   int done;                                     // 1 inner stop, 2 lucky breakdown
   int reorth;
-  int used;
+  int used;                                     // columns finished in this cycle
+  int j;                                        // current column (device-driven loop)
+  int m;                                        // restart length of this cycle
+  int maxit;                                    // iteration budget of this cycle
+  int active;                                   // 0 once j == m or the budget is spent
   int pad;
 };
 
@@ -202,6 +206,7 @@ struct dp_scene {
 
   std::vector<dp_cache*> cache_pool;   // recycled step caches
   std::vector<dp_cache*> live_caches;  // handed out, not yet destroyed
+  std::vector<std::pair<uint64_t, void*>> gm_graphs;   // instantiated GMRES cycle graphs
 };
 
 namespace dp {
@@ -265,5 +270,6 @@ int mg_levels(const dp_scene* s);
 int mg_level_rows(const dp_scene* s, int l);
 void mg_set_params(dp_scene* s, double omega, int nu);
 void mg_set_symmetric(dp_scene* s, int on);
+void gm_graphs_destroy(dp_scene* s);
 
 }  // namespace dp

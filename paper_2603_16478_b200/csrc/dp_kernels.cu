@@ -455,9 +455,13 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
 #pragma unroll
     for (int c = 0; c < 9; ++c) vs[(k * 9 + c) * kSlice + lane] = b[c];
     if (val32) {
-      float* v32 = val32 + (size_t)base * 9;
-#pragma unroll
-      for (int c = 0; c < 9; ++c) v32[(k * 9 + c) * kSlice + lane] = (float)b[c];
+      // FP32 copy for the multigrid smoother: 12 floats per slot (9 + pad),
+      // slot-major, so a lane reads its block as three 16-byte loads and a
+      // warp reads 1.5 KB contiguous
+      float4* v4 = reinterpret_cast<float4*>(val32 + (size_t)slot * 12);
+      v4[0] = make_float4((float)b[0], (float)b[1], (float)b[2], (float)b[3]);
+      v4[1] = make_float4((float)b[4], (float)b[5], (float)b[6], (float)b[7]);
+      v4[2] = make_float4((float)b[8], 0.f, 0.f, 0.f);
     }
   }
 }
@@ -825,49 +829,36 @@ int cg_solve(dp_scene* s, const double* val, const double* b, double* x, double 
 }
 
 // ---------------------------------------------------------------------------
-// GMRES(m), left block-Jacobi preconditioning, classical Gram-Schmidt with a
-// conditional second pass (re-orthogonalise when |w| drops by more than 2x),
-// Givens rotations on device (gmres, linsolve.py:108-197).  The host drives
-// the column index j; kernels exit early once `done` is set.
+// GMRES(m) (gmres, linsolve.py:108-197), device-driven: the column index j,
+// the Hessenberg matrix, the Givens rotations and the stop decision live in
+// GmresScalars on the device.  Every column kernel reads j from there, and
+// k_gm_loopctl advances it and sets the condition of a CUDA-graph WHILE node,
+// so a whole restart cycle (up to 50 columns, incl. the multigrid V-cycles)
+// is ONE graph launch with no host round trip.  Classical Gram-Schmidt fused
+// into the SpMV pass, conditional second pass for tight solves.
 
 constexpr int kGT = 256;
 constexpr int kGM1 = kMaxRestart + 1;
 
-// w = Minv (A v)
-__global__ void __launch_bounds__(256) k_gm_apply(int V, int S, const int* __restrict__ slice_base,
-                                                  const int* __restrict__ slice_width, const int* __restrict__ col,
-                                                  const double* __restrict__ val, const double* __restrict__ minv,
-                                                  const double* __restrict__ v, double* __restrict__ w,
-                                                  const GmresScalars* gs) {
-  if (ldflag(&gs->done)) return;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (gw >= S) return;
-  double a[3];
-  spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, v, a);
-  const int row = gw * kSlice + lane;
-  if (row < V) {
-    double u[3];
-    minv_apply(minv, V, row, a, u);
-    w[3 * row] = u[0]; w[3 * row + 1] = u[1]; w[3 * row + 2] = u[2];
-  }
+__device__ __forceinline__ bool gm_idle(const GmresScalars* gs) {
+  return ldflag(&gs->done) || !ldflag(&gs->active);
 }
 
-// Fused GMRES column kernel (pass 0), one warp per SELL slice:
+// Left block-Jacobi column kernel, one warp per SELL slice:
 //   v_j = w_prev / hn            (own rows, written to the basis)
 //   w   = Minv A v_j             (SpMV on the gathered w_prev / hn)
 //   coef_i = (w, v_i), i <= j and |w|^2   (block partials, last block folds)
-// Replaces apply + normalize + a separate dot pass: the basis rows of this
-// slice are read once, w is written once.
 __global__ void __launch_bounds__(256) k_gm_spmvdot(int V, int S, const int* __restrict__ slice_base,
                                                     const int* __restrict__ slice_width, const int* __restrict__ col,
                                                     const double* __restrict__ val, const double* __restrict__ minv,
-                                                    const double* __restrict__ wprev, double* __restrict__ vj,
-                                                    double* __restrict__ wnew, const double* __restrict__ Vb, size_t ld,
-                                                    int j, double* partial, unsigned int* counter, GmresScalars* gs) {
+                                                    double* W0, double* W1, double* Vb, size_t ld, double* partial,
+                                                    unsigned int* counter, GmresScalars* gs) {
   __shared__ double sh[8][kGM1 + 1];
-  __shared__ double sred[32];
-  if (ldflag(&gs->done)) return;
+  if (gm_idle(gs)) return;
+  const int j = gs->j;
+  const double* wprev = (j & 1) ? W1 : W0;
+  double* wnew = (j & 1) ? W0 : W1;
+  double* vj = Vb + (size_t)j * ld;
   const double inv = 1.0 / gs->hn;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * 8 + warp;
@@ -889,8 +880,6 @@ __global__ void __launch_bounds__(256) k_gm_spmvdot(int V, int S, const int* __r
     }
   }
   const bool live = (gw < S) && (row < V);
-  // dots in groups of 8 basis vectors: the 8 row loads are independent, so
-  // their latencies overlap before the shuffle reductions
   for (int i0 = 0; i0 <= j + 1; i0 += 8) {
     double d[8];
 #pragma unroll
@@ -937,27 +926,25 @@ __global__ void __launch_bounds__(256) k_gm_spmvdot(int V, int S, const int* __r
   }
 }
 
-// Re-orthogonalisation dots (pass 1 only, when flagged): coef_i = (w, v_i),
-// i <= j, one read of the basis; accumulators in register chunks of 8.
-__global__ void __launch_bounds__(kGT) k_gm_dots(int n, int j, const double* __restrict__ Vb, size_t ld,
-                                                 const double* __restrict__ w, double* partial, unsigned int* counter,
+// coef_i = (w, v_i), i <= j (+ |w|^2 on the first pass), one read of the basis.
+// first = 0: re-orthogonalisation pass (only when flagged), added to H.
+__global__ void __launch_bounds__(kGT) k_gm_dots(int n, const double* __restrict__ Vb, size_t ld, double* W0,
+                                                 double* W1, double* partial, unsigned int* counter,
                                                  GmresScalars* gs, int first) {
   __shared__ double sh[kGT / 32][kGM1 + 1];
-  __shared__ double sred[32];
-  if (ldflag(&gs->done)) return;
+  if (gm_idle(gs)) return;
   if (!first && !ldflag(&gs->reorth)) return;
+  const int j = gs->j;
+  const double* w = ((j + 1) & 1) ? W1 : W0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nd = first ? j + 2 : j + 1;   // first pass also |w|^2
+  const int nd = first ? j + 2 : j + 1;
   for (int i0 = 0; i0 < nd; i0 += 8) {
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int k = blockIdx.x * kGT + threadIdx.x; k < n; k += gridDim.x * kGT) {
       const double wk = w[k];
       double vv[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const int i = min(i0 + t, j);    // clamp: loads stay in range and independent
-        vv[t] = Vb[(size_t)i * ld + k];
-      }
+      for (int t = 0; t < 8; ++t) vv[t] = Vb[(size_t)min(i0 + t, j) * ld + k];
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[t] += wk * ((i0 + t <= j) ? vv[t] : wk);
     }
@@ -990,13 +977,16 @@ __global__ void __launch_bounds__(kGT) k_gm_dots(int n, int j, const double* __r
   }
 }
 
-// MG path, column kernel: v_j = w_prev / hn (own rows), t = A v_j
+// left multigrid column kernel (host-driven path only): v_j = w/hn, t = A v_j
 __global__ void __launch_bounds__(256) k_gm_spmvnorm(int V, int S, const int* __restrict__ slice_base,
                                                      const int* __restrict__ slice_width, const int* __restrict__ col,
-                                                     const double* __restrict__ val, const double* __restrict__ wprev,
-                                                     double* __restrict__ vj, double* __restrict__ t,
+                                                     const double* __restrict__ val, double* W0, double* W1,
+                                                     double* Vb, size_t ld, double* __restrict__ t,
                                                      const GmresScalars* gs) {
-  if (ldflag(&gs->done)) return;
+  if (gm_idle(gs)) return;
+  const int j = gs->j;
+  const double* wprev = (j & 1) ? W1 : W0;
+  double* vj = Vb + (size_t)j * ld;
   const double inv = 1.0 / gs->hn;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (gw >= S) return;
@@ -1037,14 +1027,16 @@ __device__ void gm_finish_column(GmresScalars* gs, int j, double wn2) {
 
 // w -= sum_i coef_i v_i ; |w|^2 ; the last block finishes column j unless a
 // second orthogonalisation pass is needed.
-__global__ void __launch_bounds__(kGT) k_gm_update(int n, int j, int pass, const double* __restrict__ Vb, size_t ld,
-                                                   double* w, double* partial, unsigned int* counter,
+__global__ void __launch_bounds__(kGT) k_gm_update(int n, int pass, const double* __restrict__ Vb, size_t ld,
+                                                   double* W0, double* W1, double* partial, unsigned int* counter,
                                                    GmresScalars* gs) {
   __shared__ double sh[32];
   __shared__ double coef[kGM1];
   __shared__ double out[1];
-  if (ldflag(&gs->done)) return;
+  if (gm_idle(gs)) return;
   if (pass == 1 && !ldflag(&gs->reorth)) return;
+  const int j = gs->j;
+  double* w = ((j + 1) & 1) ? W1 : W0;
   for (int i = threadIdx.x; i <= j; i += kGT) coef[i] = gs->coef[i];
   __syncthreads();
   double acc = 0.0;
@@ -1077,18 +1069,24 @@ __global__ void __launch_bounds__(kGT) k_gm_update(int n, int j, int pass, const
   }
 }
 
-// v_{j+1} = w / hn
-__global__ void k_gm_normalize(int n, const double* __restrict__ w, double* __restrict__ vnext, const GmresScalars* gs) {
-  if (ldflag(&gs->done)) return;
-  const double inv = 1.0 / gs->hn;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) vnext[k] = w[k] * inv;
+// end of a column: advance j and decide whether the cycle continues; in the
+// graph path this sets the WHILE node's condition.
+__global__ void k_gm_loopctl(GmresScalars* gs, cudaGraphConditionalHandle handle, int use_cond) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned int cont = 0;
+  if (!gs->done && gs->active) {
+    gs->j += 1;
+    cont = (gs->j < gs->m && gs->used < gs->maxit) ? 1u : 0u;
+    if (!cont) gs->active = 0;
+  }
+  if (use_cond) cudaGraphSetConditional(handle, cont);
 }
 
-// cycle start: v0 = Minv r (unnormalised) and |v0|^2 -> beta, g, thresholds
+// cycle start: v0 = (Minv) r (unnormalised) and |v0|^2 -> beta, g, thresholds
 __global__ void __launch_bounds__(kVT) k_gm_start(double reorth_thr, int V, const double* __restrict__ minv,
                                                   const double* __restrict__ r,
                                                   double* __restrict__ v0, double* partial, unsigned int* counter,
-                                                  GmresScalars* gs, double tol, int set_nmb) {
+                                                  GmresScalars* gs, double tol, int set_nmb, int m, int maxit) {
   __shared__ double sh[32];
   __shared__ double out[1];
   const int i = blockIdx.x * kVT + threadIdx.x;
@@ -1107,7 +1105,7 @@ __global__ void __launch_bounds__(kVT) k_gm_start(double reorth_thr, int V, cons
       *counter = 0;
       const double beta = sqrt(out[0]);
       if (set_nmb) {
-        gs->nmb = beta != 0.0 ? beta : 1.0;   // |M^-1 b| (linsolve.py:180)
+        gs->nmb = beta != 0.0 ? beta : 1.0;   // |(M^-1) b| (linsolve.py:180)
       } else {
         gs->beta = beta;
         for (int k = 0; k <= kMaxRestart; ++k) gs->g[k] = 0.0;
@@ -1121,12 +1119,16 @@ __global__ void __launch_bounds__(kVT) k_gm_start(double reorth_thr, int V, cons
         gs->reorth_thr = (tol < 1e-7) ? reorth_thr : 0.0;
         gs->used = 0;
         gs->est = beta / gs->nmb;
+        gs->j = 0;
+        gs->m = m;
+        gs->maxit = maxit;
+        gs->active = (maxit > 0) ? 1 : 0;
       }
     }
   }
 }
 
-// x += sum_i y_i v_i
+// x += sum_i y_i v_i   (or x = sum when accumulate == 0)
 __global__ void k_gm_combine(int n, int used, const double* __restrict__ y, const double* __restrict__ Vb, size_t ld,
                              double* __restrict__ x, int accumulate) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -1136,17 +1138,25 @@ __global__ void k_gm_combine(int n, int used, const double* __restrict__ y, cons
   }
 }
 
-// Right-preconditioned GMRES column, step 1: v_j = w_prev / hn, z = Minv v_j
-// (block-Jacobi; with multigrid only the normalisation, z comes from a V-cycle)
-__global__ void k_gm_prec(int V, const double* __restrict__ wprev, double* __restrict__ vj,
-                          const double* __restrict__ minv, double* __restrict__ z, const GmresScalars* gs) {
-  if (ldflag(&gs->done)) return;
+// Right-preconditioned column, step 1: v_j = w_prev / hn; z = Minv v_j
+// (block-Jacobi) or, with multigrid, a copy of v_j into the V-cycle's fixed
+// input buffer.
+__global__ void k_gm_prec(int V, double* W0, double* W1, double* Vb, size_t ld, const double* __restrict__ minv,
+                          double* __restrict__ z, double* __restrict__ vcopy, const GmresScalars* gs) {
+  if (gm_idle(gs)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= V) return;
+  const int j = gs->j;
+  const double* wprev = (j & 1) ? W1 : W0;
+  double* vj = Vb + (size_t)j * ld;
   const double inv = 1.0 / gs->hn;
   double v[3];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) { v[c] = wprev[3 * i + c] * inv; vj[3 * i + c] = v[c]; }
+  for (int c = 0; c < 3; ++c) {
+    v[c] = wprev[3 * i + c] * inv;
+    vj[3 * i + c] = v[c];
+    if (vcopy) vcopy[3 * i + c] = v[c];
+  }
   if (minv) {
     double u[3];
     minv_apply(minv, V, i, v, u);
@@ -1160,11 +1170,13 @@ __global__ void k_gm_prec(int V, const double* __restrict__ wprev, double* __res
 __global__ void __launch_bounds__(256) k_gm_spmvdot_r(int V, int S, const int* __restrict__ slice_base,
                                                       const int* __restrict__ slice_width,
                                                       const int* __restrict__ col, const double* __restrict__ val,
-                                                      const double* __restrict__ z, double* __restrict__ wnew,
-                                                      const double* __restrict__ Vb, size_t ld, int j,
-                                                      double* partial, unsigned int* counter, GmresScalars* gs) {
+                                                      const double* __restrict__ z, double* W0, double* W1,
+                                                      const double* __restrict__ Vb, size_t ld, double* partial,
+                                                      unsigned int* counter, GmresScalars* gs) {
   __shared__ double sh[8][kGM1 + 1];
-  if (ldflag(&gs->done)) return;
+  if (gm_idle(gs)) return;
+  const int j = gs->j;
+  double* wnew = ((j + 1) & 1) ? W1 : W0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * 8 + warp;
   const int row = gw * kSlice + lane;
@@ -1234,6 +1246,7 @@ __global__ void k_minv_axpy(int V, const double* __restrict__ minv, const double
 
 // re-orthogonalise (tight solves only) when |w|^2 drops below this fraction
 static const double g_reorth_thr = getenv("DP_REORTH") ? atof(getenv("DP_REORTH")) : 0.01;
+static const int g_use_graphs = getenv("DP_GRAPHS") ? atoi(getenv("DP_GRAPHS")) : 1;
 
 static int gm_grid(int n) {
   // one element per thread: every basis load of a thread is independent
@@ -1241,9 +1254,122 @@ static int gm_grid(int n) {
   return grid_for(n, kGT);
 }
 
-// Restarted GMRES(m) with RIGHT preconditioning (block-Jacobi or the
-// multigrid V-cycle): the Arnoldi residual estimate is the true residual, so
-// the inner stop test and the forcing term of the inexact Newton use the same
+__global__ void k_gm_copy_wnew(int n, const double* __restrict__ src, double* W0, double* W1,
+                               const GmresScalars* gs) {
+  if (gm_idle(gs)) return;
+  double* wn = ((gs->j + 1) & 1) ? W1 : W0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) wn[k] = src[k];
+}
+
+// Kernels of one GMRES column (j read on device).  Returns the number of
+// kernel launches issued.
+static int gm_column(dp_scene* s, const double* val, int use_mg, int left, bool tight, cudaGraphConditionalHandle h,
+                     int use_cond) {
+  const int V = s->V, n = 3 * V;
+  const size_t ld = (size_t)n;
+  const int nbs = grid_for((int64_t)s->S * 32, 256);
+  const int nbg = gm_grid(n);
+  double* Vb = s->gm_V;
+  double* z = s->ku;
+  int k = 0;
+  if (left && !use_mg) {
+    k_gm_spmvdot<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, s->minv, s->kw,
+                                             s->kp, Vb, ld, s->red.partial, s->red.counter, s->gsc);
+    k += 1;
+  } else if (left) {
+    k_gm_spmvnorm<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, s->kw, s->kp, Vb,
+                                              ld, z, s->gsc);
+    // the V-cycle output must be the j-dependent w_new: copy through a fixed buffer
+    mg_apply(s, val, z, s->q_try, &s->gsc->done);
+    k_gm_copy_wnew<<<grid_for(n, 256), 256, 0, s->stream>>>(n, s->q_try, s->kw, s->kp, s->gsc);
+    k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, Vb, ld, s->kw, s->kp, s->red.partial, s->red.counter, s->gsc, 1);
+    k += 3;
+  } else {
+    k_gm_prec<<<grid_for(V, 256), 256, 0, s->stream>>>(V, s->kw, s->kp, Vb, ld, use_mg ? nullptr : s->minv, z,
+                                                       use_mg ? s->tmp : nullptr, s->gsc);
+    if (use_mg) mg_apply(s, val, s->tmp, z, &s->gsc->done);
+    k_gm_spmvdot_r<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, z, s->kw,
+                                               s->kp, Vb, ld, s->red.partial, s->red.counter, s->gsc);
+    k += 2;
+  }
+  k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, 0, Vb, ld, s->kw, s->kp, s->red.partial, s->red.counter, s->gsc);
+  k += 1;
+  if (tight) {   // conditional second Gram-Schmidt pass (kernels exit unless flagged)
+    k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, Vb, ld, s->kw, s->kp, s->red.partial, s->red.counter, s->gsc, 0);
+    k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, 1, Vb, ld, s->kw, s->kp, s->red.partial, s->red.counter, s->gsc);
+    k += 2;
+  }
+  k_gm_loopctl<<<1, 32, 0, s->stream>>>(s->gsc, h, use_cond);
+  return k + 1;
+}
+
+// One restart cycle as a CUDA graph: a WHILE node whose body is one column.
+// Cached per (operator, preconditioner side/type, tightness).
+struct GmGraph {
+  cudaGraphExec_t exec = nullptr;
+  int nodes = 0;
+};
+
+static GmGraph* gm_graph(dp_scene* s, const double* val, int use_mg, int left, bool tight) {
+  const uint64_t key = (uint64_t)(uintptr_t)val ^ ((uint64_t)use_mg << 1) ^ ((uint64_t)left << 2) ^
+                       ((uint64_t)tight << 3);
+  for (auto& e : s->gm_graphs)
+    if (e.first == key) return (GmGraph*)e.second;
+  cudaGraph_t g = nullptr;
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return nullptr;
+  cudaGraphConditionalHandle h;
+  if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return nullptr;
+  }
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, nullptr, 0, &cp) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return nullptr;
+  }
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  int nodes = 0;
+  const int64_t launches0 = s->launches;
+  if (cudaStreamBeginCaptureToGraph(s->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+      cudaSuccess) {
+    cudaGraphDestroy(g);
+    return nullptr;
+  }
+  nodes = gm_column(s, val, use_mg, left, tight, h, 1);
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(s->stream, &captured);
+  nodes += (int)(s->launches - launches0);   // V-cycle kernels count themselves
+  s->launches = launches0;
+  GmGraph* gg = new GmGraph();
+  if (ce != cudaSuccess || cudaGraphInstantiate(&gg->exec, g, 0) != cudaSuccess) {
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    delete gg;
+    return nullptr;
+  }
+  cudaGraphDestroy(g);
+  gg->nodes = nodes;
+  s->gm_graphs.push_back({key, (void*)gg});
+  return gg;
+}
+
+void gm_graphs_destroy(dp_scene* s) {
+  for (auto& e : s->gm_graphs) {
+    GmGraph* gg = (GmGraph*)e.second;
+    if (gg->exec) cudaGraphExecDestroy(gg->exec);
+    delete gg;
+  }
+  s->gm_graphs.clear();
+}
+
+// Restarted GMRES(m), right (block-Jacobi or multigrid V-cycle) or left
+// preconditioning.  With right preconditioning the Arnoldi estimate is the
+// true residual, so the inner stop test and the Newton forcing use the same
 // norm as the recomputed residual (linsolve.py:108-197 uses left
 // preconditioning; the converged solution is the same).  x = 0 initially.
 // Returns 0 converged, 1 not converged.
@@ -1255,7 +1381,6 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   if (restart < 1) restart = 1;
   const size_t ld = (size_t)n;
   const int nbv = grid_for(V, kVT);
-  const int nbs = grid_for((int64_t)s->S * 32, 256);
   const int nbg = gm_grid(n);
   double* Vb = s->gm_V;
   double* r = s->kr;
@@ -1270,74 +1395,55 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   // nmb = |b| (right) or |M^-1 b| (left, the reference's normalisation)
   if (left && use_mg) {
     mg_apply(s, val, b, z, nullptr);
-    k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, z, s->kw, s->red.partial, s->red.counter, s->gsc, rtol, 1);
+    k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, z, s->kw, s->red.partial, s->red.counter,
+                                           s->gsc, rtol, 1, 0, 0);
   } else {
-    k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, left ? s->minv : nullptr, b, s->kw, s->red.partial, s->red.counter,
-                                           s->gsc, rtol, 1);
+    k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, left ? s->minv : nullptr, b, s->kw, s->red.partial,
+                                           s->red.counter, s->gsc, rtol, 1, 0, 0);
   }
   s->launches++;
+  GmGraph* gg = (g_use_graphs && !(left && use_mg)) ? gm_graph(s, val, use_mg, left, tight) : nullptr;
   int total = 0;
   double rel = 1.0;
   while (total < max_iter) {
     rel = true_relres(s, val, b, x, r, bnorm);
     if (rel <= rtol) break;
     const double cycle_start = rel;
-    double* Wb[2] = {s->kw, s->kp};   // double-buffered unnormalised basis vector
+    const int budget = max_iter - total;
     if (left && use_mg) {
       mg_apply(s, val, r, z, nullptr);
-      k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, z, Wb[0], s->red.partial, s->red.counter, s->gsc, rtol, 0);
+      k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, z, s->kw, s->red.partial, s->red.counter,
+                                             s->gsc, rtol, 0, restart, budget);
     } else {
-      k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, left ? s->minv : nullptr, r, Wb[0], s->red.partial, s->red.counter,
-                                             s->gsc, rtol, 0);
+      k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, left ? s->minv : nullptr, r, s->kw, s->red.partial,
+                                             s->red.counter, s->gsc, rtol, 0, restart, budget);
     }
     s->launches++;
-    int j = 0;
-    bool stop = false;
-    while (j < restart && total < max_iter && !stop) {
-      int chunk = 8;
-      if (j + chunk > restart) chunk = restart - j;
-      if (total + chunk > max_iter) chunk = max_iter - total;
-      for (int c = 0; c < chunk; ++c, ++j) {
-        double* wp = Wb[j & 1];
-        double* wn = Wb[(j + 1) & 1];
-        double* vj = Vb + (size_t)j * ld;
-        if (left && !use_mg) {
-          // fused: v_j = w/hn, w = Minv A v_j, coef = V^T w, |w|^2
-          k_gm_spmvdot<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, s->minv,
-                                                   wp, vj, wn, Vb, ld, j, s->red.partial, s->red.counter, s->gsc);
-        } else if (left) {
-          // v_j = w/hn, t = A v_j ; w = B t (V-cycle) ; coef = V^T w, |w|^2
-          k_gm_spmvnorm<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, wp, vj,
-                                                    z, s->gsc);
-          mg_apply(s, val, z, wn, &s->gsc->done);
-          k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc, 1);
-          s->launches += 1;
-        } else {
-          k_gm_prec<<<grid_for(V, 256), 256, 0, s->stream>>>(V, wp, vj, use_mg ? nullptr : s->minv, z, s->gsc);
-          if (use_mg) mg_apply(s, val, vj, z, &s->gsc->done);
-          k_gm_spmvdot_r<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, z, wn,
-                                                     Vb, ld, j, s->red.partial, s->red.counter, s->gsc);
-          s->launches += 1;
-        }
-        k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, j, 0, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc);
-        s->launches += 2;
-        if (tight) {   // conditional second Gram-Schmidt pass (kernels exit unless flagged)
-          k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, j, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc, 0);
-          k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, j, 1, Vb, ld, wn, s->red.partial, s->red.counter, s->gsc);
-          s->launches += 2;
-        }
-      }
+    if (gg) {
+      // the whole cycle on the device: one graph launch, one sync
+      cudaGraphLaunch(gg->exec, s->stream);
       cudaMemcpyAsync(s->h_gsc, s->gsc, sizeof(GmresScalars), cudaMemcpyDeviceToHost, s->stream);
       cudaStreamSynchronize(s->stream);
-      if (s->h_gsc->done) stop = true;
-      total = *iters + s->h_gsc->used;
+      s->launches += (int64_t)gg->nodes * std::max(1, s->h_gsc->used);
+    } else {
+      // host-driven columns, polled every 8
+      bool stop = false;
+      int launched = 0;
+      while (!stop && launched < restart && launched < budget) {
+        int chunk = std::min(8, std::min(restart, budget) - launched);
+        for (int c = 0; c < chunk; ++c) s->launches += gm_column(s, val, use_mg, left, tight, 0, 0);
+        launched += chunk;
+        cudaMemcpyAsync(s->h_gsc, s->gsc, sizeof(GmresScalars), cudaMemcpyDeviceToHost, s->stream);
+        cudaStreamSynchronize(s->stream);
+        stop = s->h_gsc->done || !s->h_gsc->active;
+      }
     }
     const GmresScalars* hg = s->h_gsc;
     const int used = hg->used;
     *iters += used;
     total = *iters;
     if (used > 0) {
-      // back substitution H[:used,:used] y = g[:used]; x += M^-1 (V y)
+      // back substitution H[:used,:used] y = g[:used]; x += (M^-1) V y
       double y[kMaxRestart];
       for (int i = used - 1; i >= 0; --i) {
         double acc = hg->g[i];

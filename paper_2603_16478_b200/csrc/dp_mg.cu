@@ -170,7 +170,7 @@ int mg_setup(dp_scene* s) {
   // mixed-precision preconditioner: the fine-level V-cycle reads FP32 copies
   // of the operator (written by k_assemble); the Krylov method itself runs on
   // the FP64 operator, so the solution accuracy is unaffected
-  rc |= al(mg, &s->val32, (size_t)s->NS * 9);
+  rc |= al(mg, &s->val32, (size_t)s->NS * 12);   // packed 12 floats per slot (float4 x 3)
   rc |= al(mg, &s->minv32, (size_t)s->V * 9);
   rc |= al(mg, &L0.x, (size_t)3 * s->V);
   rc |= al(mg, &L0.r, (size_t)3 * s->V);
@@ -188,7 +188,10 @@ int mg_setup(dp_scene* s) {
     }
   }
   HostPattern cur = fine;
-  std::vector<int64_t> cur_addr = fine_addr;
+  // level 1 gathers from the packed FP32 fine copy: address = slot * 12
+  std::vector<int64_t> cur_addr(s->nnzb);
+  for (int64_t k = 0; k < s->nnzb; ++k) cur_addr[k] = s->h_block_slot[k] * 12;
+  (void)fine_addr;
   while (cur.n > kCoarseMax && !rc) {
     std::vector<int> agg;
     const int na = aggregate(cur, agg);
@@ -359,7 +362,7 @@ __device__ __forceinline__ void inv3(const double a[9], double o[9]) {
 // coarse operator: val_c[slot] = sum of the fine blocks in its gather list
 // (one warp per coarse slot, lanes over contributions); block-Jacobi inverse
 // of the diagonal slots.
-template <class TF>
+template <class TF, int CSTRIDE>
 __global__ void __launch_bounds__(256) k_mg_galerkin(int n, int S, const int* __restrict__ slice_base,
                                                      const int* __restrict__ slice_width,
                                                      const int* __restrict__ diag_slot,
@@ -374,7 +377,7 @@ __global__ void __launch_bounds__(256) k_mg_galerkin(int n, int S, const int* __
   for (int t = gal_ptr[slot] + lane; t < gal_ptr[slot + 1]; t += 32) {
     const TF* src = valf + gal[t];
 #pragma unroll
-    for (int c = 0; c < 9; ++c) b[c] += (double)src[c * kSlice];
+    for (int c = 0; c < 9; ++c) b[c] += (double)src[c * CSTRIDE];
   }
 #pragma unroll
   for (int c = 0; c < 9; ++c) b[c] = warp_allsum(b[c]);
@@ -447,15 +450,26 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (int k = wsub; k < K; k += SPLIT) {
     const int j = __ldg(cs + k * kSlice);
-    const TV* v = vs + k * 9 * kSlice;
+    double m[9];
+    if (sizeof(TV) == 4) {
+      // packed FP32 fine level: 3 x 16-byte loads per block
+      const float4* p4 = reinterpret_cast<const float4*>(val) + (size_t)(base + k * kSlice + lane) * 3;
+      const float4 q0 = __ldg(p4), q1 = __ldg(p4 + 1), q2 = __ldg(p4 + 2);
+      m[0] = q0.x; m[1] = q0.y; m[2] = q0.z; m[3] = q0.w;
+      m[4] = q1.x; m[5] = q1.y; m[6] = q1.z; m[7] = q1.w; m[8] = q2.x;
+    } else {
+      const TV* v = vs + k * 9 * kSlice;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) m[c] = (double)v[c * kSlice];
+    }
     double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
     if (xc) {
       const int J = __ldg(agg + j);
       x0 += alpha * __ldg(xc + 3 * J); x1 += alpha * __ldg(xc + 3 * J + 1); x2 += alpha * __ldg(xc + 3 * J + 2);
     }
-    a0 += (double)v[0 * kSlice] * x0 + (double)v[1 * kSlice] * x1 + (double)v[2 * kSlice] * x2;
-    a1 += (double)v[3 * kSlice] * x0 + (double)v[4 * kSlice] * x1 + (double)v[5 * kSlice] * x2;
-    a2 += (double)v[6 * kSlice] * x0 + (double)v[7 * kSlice] * x1 + (double)v[8 * kSlice] * x2;
+    a0 += m[0] * x0 + m[1] * x1 + m[2] * x2;
+    a1 += m[3] * x0 + m[4] * x1 + m[5] * x2;
+    a2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
   }
   if (SPLIT > 1) {
     part[wsub][0][lane] = a0;
@@ -670,11 +684,11 @@ void mg_assemble(dp_scene* s, const double* val) {
   for (size_t l = 1; l < mg->lv.size(); ++l) {
     MGLevel& L = mg->lv[l];
     if (l == 1)
-      k_mg_galerkin<float><<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
+      k_mg_galerkin<float, 1><<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
           L.n, L.S, L.slice_base, L.slice_width, L.diag_slot, L.gal_ptr, L.gal, s->val32, L.val, L.minv, L.slot_row,
           L.NS);
     else
-      k_mg_galerkin<double><<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
+      k_mg_galerkin<double, kSlice><<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
           L.n, L.S, L.slice_base, L.slice_width, L.diag_slot, L.gal_ptr, L.gal, vf, L.val, L.minv, L.slot_row, L.NS);
     vf = L.val;
     s->launches++;

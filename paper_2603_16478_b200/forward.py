@@ -160,15 +160,25 @@ class ForwardReport:
 
 class StepCache:
     """forward.py:47-60.  State vectors are device-resident; reading a field
-    downloads it once."""
+    downloads it once.  ``fext`` (scene.external_force() at step time) is
+    computed on first access from a snapshot of the scene's fext/gravity."""
 
     def __init__(self, scene, sysmat, dc, fext, report):
         self.scene = scene
         self.sysmat = sysmat
         self._dc = dc
-        self.fext = fext
+        self._fext_src = fext
+        self._fext = None
         self.report = report
         self._states = None
+
+    @property
+    def fext(self):
+        if self._fext is None and self._fext_src is not None:
+            f, g, m = self._fext_src
+            grav = m.repeat(3) * np.tile(g, m.size)
+            self._fext = grav if f is None else f + grav
+        return self._fext
 
     def _st(self):
         if self._states is None:
@@ -232,12 +242,9 @@ def forward_step(scene, state, sysmat, cfg=None, device_io=None):
     report.line_search_trials = int(rep_c.line_search_trials)
     report.n_contacts = int(rep_c.n_contacts)
     step_index = getattr(state, "step_index", 0) + 1 if state is not None else 0
-    if device_io is None:
-        new_state = core.SimState(q1, v1, step_index)
-        fext = scene.external_force()
-    else:
-        new_state = None
-        fext = None
+    # snapshot for StepCache.fext (scene.external_force() at this step)
+    fext = (None if scene.fext is None else scene.fext.copy(), scene.gravity.copy(), scene.masses)
+    new_state = core.SimState(q1, v1, step_index) if device_io is None else None
     report.cache = StepCache(scene, sysmat, dc, fext, report)
     return new_state, report
 

@@ -205,7 +205,7 @@ void dp_forward_cfg_default(dp_forward_cfg* c) {
   c->max_line_search = 40;
   c->pullback_margin = 1e-6;
   c->lin_rtol_max = 1e-3;
-  c->lin_rtol_min = 1e-12;
+  c->lin_rtol_min = 1e-3;
   c->lin_max_iter = 5000;
   c->gmres_restart = 50;
 }
@@ -822,6 +822,32 @@ static void evaluate(dp_scene* s, const double* q, double* r, int jac) {
   launch_residual(s, q, s->q_hat, r, s->esc);
 }
 
+// DP_DEBUG >= 3: the largest residual rows and their contact state
+static void debug_top_residuals(dp_scene* s, const double* r, const double* q, int it) {
+  const int V = s->V, C = s->h_esc->n_contacts;
+  std::vector<double> hr((size_t)3 * V), hd((size_t)3 * C), hq((size_t)3 * V);
+  std::vector<int> hv(C);
+  cudaMemcpy(hr.data(), r, hr.size() * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(hq.data(), q, hq.size() * 8, cudaMemcpyDeviceToHost);
+  if (C) {
+    cudaMemcpy(hv.data(), s->c_vertex, C * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hd.data(), s->c_delta, hd.size() * 8, cudaMemcpyDeviceToHost);
+  }
+  std::vector<int> idx(hr.size());
+  for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
+  std::partial_sort(idx.begin(), idx.begin() + 6, idx.end(),
+                    [&](int a, int b) { return std::fabs(hr[a]) > std::fabs(hr[b]); });
+  for (int k = 0; k < 6; ++k) {
+    const int i = idx[k], v = i / 3;
+    int c = -1;
+    for (int j = 0; j < C; ++j)
+      if (hv[j] == v) { c = j; break; }
+    fprintf(stderr, "[dp]     it=%d top%d v=%d comp=%d r=%.3e contact=%d", it, k, v, i % 3, hr[i], c);
+    if (c >= 0) fprintf(stderr, " delta=(%.3e %.3e %.3e)", hd[3 * c], hd[3 * c + 1], hd[3 * c + 2]);
+    fprintf(stderr, " q=(%.6f %.6f %.6f)\n", hq[3 * v], hq[3 * v + 1], hq[3 * v + 2]);
+  }
+}
+
 __global__ void k_neg(int n, const double* a, double* o) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) o[i] = -a[i];
 }
@@ -866,6 +892,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     if ((rc = sync_esc(s))) return rc;
     const EvalScalars E = *s->h_esc;
     if (g_debug) fprintf(stderr, "[dp]   detect+eval(jac) %.2fms\n", 1e3 * (now_s() - t_it0));
+    if (g_debug >= 3) debug_top_residuals(s, s->r, q, it);
     if (it == 0) scale = std::max(1.0, E.scale_max);
     n_contacts = E.n_contacts;
     asym = E.asym;

@@ -38,7 +38,7 @@ class ForwardConfig:
     max_line_search: int = 40
     pullback_margin: float = 1e-6
     lin_rtol_max: float = 1e-3
-    lin_rtol_min: float = 1e-12
+    lin_rtol_min: float = 1e-3
     lin_max_iter: int = 5000
     gmres_restart: int = 50
 

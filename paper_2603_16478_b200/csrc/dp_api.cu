@@ -161,6 +161,7 @@ using namespace dp;
 static const int g_debug = getenv("DP_DEBUG") ? atoi(getenv("DP_DEBUG")) : 0;
 // after a line search that had to cut the step below 1/16 the Newton model is
 // poor (friction-cone / activation kinks): a cheap direction is enough
+static const int g_ls_norm = getenv("DP_LS_NORM") ? atoi(getenv("DP_LS_NORM")) : 0;
 static const double g_eta_plateau = getenv("DP_ETA_PLATEAU") ? atof(getenv("DP_ETA_PLATEAU")) : 0.0;
 static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -969,7 +970,8 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
         const int st = T.status;
         const bool value_error = (st & (ST_INVERTED | ST_NONFINITE | ST_PENETRATION)) != 0;
         if (!value_error && (st & ST_NH_STALL)) return raise_status(ST_NH_STALL);
-        if (!value_error && T.rmax < E.rmax) {
+        const bool decrease = g_ls_norm == 2 ? (T.rnorm2 < E.rnorm2) : (T.rmax < E.rmax);
+        if (!value_error && decrease) {
           std::swap(q, q_try);
           accepted = true;
           break;

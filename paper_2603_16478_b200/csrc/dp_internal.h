@@ -140,6 +140,7 @@ struct dp_scene {
   int *contrib_ptr = nullptr, *contrib = nullptr;
   double* minv = nullptr;          // block-Jacobi inverses [9][V]
   float* val32 = nullptr;          // FP32 copy of the last assembled operator (multigrid fine level)
+  const double* val32_src = nullptr;   // operator val32 was last written from
   float* minv32 = nullptr;         // FP32 block-Jacobi inverses (multigrid smoother)
 
   // element outputs

@@ -476,6 +476,7 @@ void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat)
                                        has_c ? s->c_count : nullptr, s->c_off, s->c_blk, amat ? 0 : 1,
                                        s->h * s->h, val, s->minv, amat ? nullptr : s->val32,
                                        amat ? nullptr : s->minv32);
+  if (!amat && s->val32) s->val32_src = val;   // the FP32 copy now mirrors `val`
   s->launches++;
 }
 
@@ -928,23 +929,24 @@ __global__ void __launch_bounds__(256) k_gm_spmvdot(int V, int S, const int* __r
 
 // coef_i = (w, v_i), i <= j (+ |w|^2 on the first pass), one read of the basis.
 // first = 0: re-orthogonalisation pass (only when flagged), added to H.
-__global__ void __launch_bounds__(kGT) k_gm_dots(int n, const double* __restrict__ Vb, size_t ld, double* W0,
-                                                 double* W1, double* partial, unsigned int* counter,
+template <typename TB>
+__global__ void __launch_bounds__(kGT) k_gm_dots(int n, const TB* __restrict__ Vb, size_t ld, TB* W0,
+                                                 TB* W1, double* partial, unsigned int* counter,
                                                  GmresScalars* gs, int first) {
   __shared__ double sh[kGT / 32][kGM1 + 1];
   if (gm_idle(gs)) return;
   if (!first && !ldflag(&gs->reorth)) return;
   const int j = gs->j;
-  const double* w = ((j + 1) & 1) ? W1 : W0;
+  const TB* w = ((j + 1) & 1) ? W1 : W0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nd = first ? j + 2 : j + 1;
   for (int i0 = 0; i0 < nd; i0 += 8) {
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int k = blockIdx.x * kGT + threadIdx.x; k < n; k += gridDim.x * kGT) {
-      const double wk = w[k];
+      const double wk = (double)w[k];
       double vv[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) vv[t] = Vb[(size_t)min(i0 + t, j) * ld + k];
+      for (int t = 0; t < 8; ++t) vv[t] = (double)Vb[(size_t)min(i0 + t, j) * ld + k];
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[t] += wk * ((i0 + t <= j) ? vv[t] : wk);
     }
@@ -1027,8 +1029,9 @@ __device__ void gm_finish_column(GmresScalars* gs, int j, double wn2) {
 
 // w -= sum_i coef_i v_i ; |w|^2 ; the last block finishes column j unless a
 // second orthogonalisation pass is needed.
-__global__ void __launch_bounds__(kGT) k_gm_update(int n, int pass, const double* __restrict__ Vb, size_t ld,
-                                                   double* W0, double* W1, double* partial, unsigned int* counter,
+template <typename TB>
+__global__ void __launch_bounds__(kGT) k_gm_update(int n, int pass, const TB* __restrict__ Vb, size_t ld,
+                                                   TB* W0, TB* W1, double* partial, unsigned int* counter,
                                                    GmresScalars* gs) {
   __shared__ double sh[32];
   __shared__ double coef[kGM1];
@@ -1036,21 +1039,22 @@ __global__ void __launch_bounds__(kGT) k_gm_update(int n, int pass, const double
   if (gm_idle(gs)) return;
   if (pass == 1 && !ldflag(&gs->reorth)) return;
   const int j = gs->j;
-  double* w = ((j + 1) & 1) ? W1 : W0;
+  TB* w = ((j + 1) & 1) ? W1 : W0;
   for (int i = threadIdx.x; i <= j; i += kGT) coef[i] = gs->coef[i];
   __syncthreads();
   double acc = 0.0;
   for (int k = blockIdx.x * kGT + threadIdx.x; k < n; k += gridDim.x * kGT) {
-    double v = w[k];
+    double v = (double)w[k];
     int i = 0;
     for (; i + 4 <= j + 1; i += 4) {
-      const double a0 = Vb[(size_t)i * ld + k], a1 = Vb[(size_t)(i + 1) * ld + k];
-      const double a2 = Vb[(size_t)(i + 2) * ld + k], a3 = Vb[(size_t)(i + 3) * ld + k];
+      const double a0 = (double)Vb[(size_t)i * ld + k], a1 = (double)Vb[(size_t)(i + 1) * ld + k];
+      const double a2 = (double)Vb[(size_t)(i + 2) * ld + k], a3 = (double)Vb[(size_t)(i + 3) * ld + k];
       v -= coef[i] * a0 + coef[i + 1] * a1 + coef[i + 2] * a2 + coef[i + 3] * a3;
     }
-    for (; i <= j; ++i) v -= coef[i] * Vb[(size_t)i * ld + k];
-    w[k] = v;
-    acc += v * v;
+    for (; i <= j; ++i) v -= coef[i] * (double)Vb[(size_t)i * ld + k];
+    const TB vs = (TB)v;
+    w[k] = vs;
+    acc += (double)vs * (double)vs;
   }
   double t = block_sum<kGT>(acc, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
@@ -1083,9 +1087,10 @@ __global__ void k_gm_loopctl(GmresScalars* gs, cudaGraphConditionalHandle handle
 }
 
 // cycle start: v0 = (Minv) r (unnormalised) and |v0|^2 -> beta, g, thresholds
+template <typename TB>
 __global__ void __launch_bounds__(kVT) k_gm_start(double reorth_thr, int V, const double* __restrict__ minv,
                                                   const double* __restrict__ r,
-                                                  double* __restrict__ v0, double* partial, unsigned int* counter,
+                                                  TB* __restrict__ v0, double* partial, unsigned int* counter,
                                                   GmresScalars* gs, double tol, int set_nmb, int m, int maxit) {
   __shared__ double sh[32];
   __shared__ double out[1];
@@ -1095,7 +1100,11 @@ __global__ void __launch_bounds__(kVT) k_gm_start(double reorth_thr, int V, cons
     double rv[3] = {r[3 * i], r[3 * i + 1], r[3 * i + 2]}, u[3] = {rv[0], rv[1], rv[2]};
     if (minv) minv_apply(minv, V, i, rv, u);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { v0[3 * i + c] = u[c]; acc += u[c] * u[c]; }
+    for (int c = 0; c < 3; ++c) {
+      const TB us = (TB)u[c];
+      if (v0) v0[3 * i + c] = us;
+      acc += (double)us * (double)us;
+    }
   }
   double t = block_sum<kVT>(acc, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
@@ -1129,11 +1138,12 @@ __global__ void __launch_bounds__(kVT) k_gm_start(double reorth_thr, int V, cons
 }
 
 // x += sum_i y_i v_i   (or x = sum when accumulate == 0)
-__global__ void k_gm_combine(int n, int used, const double* __restrict__ y, const double* __restrict__ Vb, size_t ld,
+template <typename TB>
+__global__ void k_gm_combine(int n, int used, const double* __restrict__ y, const TB* __restrict__ Vb, size_t ld,
                              double* __restrict__ x, int accumulate) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     double acc = 0.0;
-    for (int i = 0; i < used; ++i) acc += y[i] * Vb[(size_t)i * ld + k];
+    for (int i = 0; i < used; ++i) acc += y[i] * (double)Vb[(size_t)i * ld + k];
     x[k] = accumulate ? x[k] + acc : acc;
   }
 }
@@ -1141,20 +1151,22 @@ __global__ void k_gm_combine(int n, int used, const double* __restrict__ y, cons
 // Right-preconditioned column, step 1: v_j = w_prev / hn; z = Minv v_j
 // (block-Jacobi) or, with multigrid, a copy of v_j into the V-cycle's fixed
 // input buffer.
-__global__ void k_gm_prec(int V, double* W0, double* W1, double* Vb, size_t ld, const double* __restrict__ minv,
+template <typename TB>
+__global__ void k_gm_prec(int V, TB* W0, TB* W1, TB* Vb, size_t ld, const double* __restrict__ minv,
                           double* __restrict__ z, double* __restrict__ vcopy, const GmresScalars* gs) {
   if (gm_idle(gs)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= V) return;
   const int j = gs->j;
-  const double* wprev = (j & 1) ? W1 : W0;
-  double* vj = Vb + (size_t)j * ld;
+  const TB* wprev = (j & 1) ? W1 : W0;
+  TB* vj = Vb + (size_t)j * ld;
   const double inv = 1.0 / gs->hn;
   double v[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    v[c] = wprev[3 * i + c] * inv;
-    vj[3 * i + c] = v[c];
+    const TB vs = (TB)((double)wprev[3 * i + c] * inv);
+    v[c] = (double)vs;
+    vj[3 * i + c] = vs;
     if (vcopy) vcopy[3 * i + c] = v[c];
   }
   if (minv) {
@@ -1167,24 +1179,53 @@ __global__ void k_gm_prec(int V, double* W0, double* W1, double* Vb, size_t ld, 
 
 // step 2 (one warp per SELL slice): w = A z, coef_i = (w, v_i) for i <= j,
 // |w|^2; last block folds into the Hessenberg column.
+// SpMV row with the packed FP32 copy of the operator (12 floats per slot)
+__device__ __forceinline__ void spmv_row32(int slice, int lane, const int* __restrict__ slice_base,
+                                           const int* __restrict__ slice_width, const int* __restrict__ col,
+                                           const float* __restrict__ val, const double* __restrict__ x, double y[3]) {
+  const int base = slice_base[slice];
+  const int K = slice_width[slice];
+  const int* cs = col + base + lane;
+  const float4* p4 = reinterpret_cast<const float4*>(val) + (size_t)(base + lane) * 3;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < K; ++k) {
+    const int j = __ldg(cs + k * kSlice);
+    const float4* p = p4 + (size_t)k * kSlice * 3;
+    const float4 q0 = __ldcs(p), q1 = __ldcs(p + 1), q2 = __ldcs(p + 2);
+    const double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
+    a0 += (double)q0.x * x0 + (double)q0.y * x1 + (double)q0.z * x2;
+    a1 += (double)q0.w * x0 + (double)q1.x * x1 + (double)q1.y * x2;
+    a2 += (double)q1.z * x0 + (double)q1.w * x1 + (double)q2.x * x2;
+  }
+  y[0] = a0; y[1] = a1; y[2] = a2;
+}
+
+template <typename TB, typename TV>
 __global__ void __launch_bounds__(256) k_gm_spmvdot_r(int V, int S, const int* __restrict__ slice_base,
                                                       const int* __restrict__ slice_width,
-                                                      const int* __restrict__ col, const double* __restrict__ val,
-                                                      const double* __restrict__ z, double* W0, double* W1,
-                                                      const double* __restrict__ Vb, size_t ld, double* partial,
+                                                      const int* __restrict__ col, const TV* __restrict__ val,
+                                                      const double* __restrict__ z, TB* W0, TB* W1,
+                                                      const TB* __restrict__ Vb, size_t ld, double* partial,
                                                       unsigned int* counter, GmresScalars* gs) {
   __shared__ double sh[8][kGM1 + 1];
   if (gm_idle(gs)) return;
   const int j = gs->j;
-  double* wnew = ((j + 1) & 1) ? W1 : W0;
+  TB* wnew = ((j + 1) & 1) ? W1 : W0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * 8 + warp;
   const int row = gw * kSlice + lane;
   double u[3] = {0.0, 0.0, 0.0};
   if (gw < S) {
-    spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, z, u);
+    if constexpr (sizeof(TV) == 4) spmv_row32(gw, lane, slice_base, slice_width, col, val, z, u);
+    else spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, z, u);
     if (row < V) {
-      wnew[3 * row] = u[0]; wnew[3 * row + 1] = u[1]; wnew[3 * row + 2] = u[2];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const TB us = (TB)u[c];
+        wnew[3 * row + c] = us;
+        u[c] = (double)us;
+      }
     } else {
       u[0] = u[1] = u[2] = 0.0;
     }
@@ -1198,8 +1239,8 @@ __global__ void __launch_bounds__(256) k_gm_spmvdot_r(int V, int S, const int* _
       double v = 0.0;
       if (live && i <= j + 1) {
         if (i <= j) {
-          const double* vi = Vb + (size_t)i * ld + 3 * (size_t)row;
-          v = u[0] * vi[0] + u[1] * vi[1] + u[2] * vi[2];
+          const TB* vi = Vb + (size_t)i * ld + 3 * (size_t)row;
+          v = u[0] * (double)vi[0] + u[1] * (double)vi[1] + u[2] * (double)vi[2];
         } else {
           v = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
         }
@@ -1247,6 +1288,7 @@ __global__ void k_minv_axpy(int V, const double* __restrict__ minv, const double
 // re-orthogonalise (tight solves only) when |w|^2 drops below this fraction
 static const double g_reorth_thr = getenv("DP_REORTH") ? atof(getenv("DP_REORTH")) : 0.01;
 static const int g_use_graphs = getenv("DP_GRAPHS") ? atoi(getenv("DP_GRAPHS")) : 1;
+static const int g_gm_fp32 = getenv("DP_GM_FP32") ? atoi(getenv("DP_GM_FP32")) : 0;
 
 static int gm_grid(int n) {
   // one element per thread: every basis load of a thread is independent
@@ -1263,8 +1305,8 @@ __global__ void k_gm_copy_wnew(int n, const double* __restrict__ src, double* W0
 
 // Kernels of one GMRES column (j read on device).  Returns the number of
 // kernel launches issued.
-static int gm_column(dp_scene* s, const double* val, int use_mg, int left, bool tight, cudaGraphConditionalHandle h,
-                     int use_cond) {
+static int gm_column(dp_scene* s, const double* val, int use_mg, int left, bool tight, bool lowp,
+                     cudaGraphConditionalHandle h, int use_cond) {
   const int V = s->V, n = 3 * V;
   const size_t ld = (size_t)n;
   const int nbs = grid_for((int64_t)s->S * 32, 256);
@@ -1284,19 +1326,36 @@ static int gm_column(dp_scene* s, const double* val, int use_mg, int left, bool 
     k_gm_copy_wnew<<<grid_for(n, 256), 256, 0, s->stream>>>(n, s->q_try, s->kw, s->kp, s->gsc);
     k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, Vb, ld, s->kw, s->kp, s->red.partial, s->red.counter, s->gsc, 1);
     k += 3;
+  } else if (lowp) {
+    // FP32 Krylov basis and FP32 operator copy (inexact Newton solves with
+    // the V-cycle; the residual is recomputed in FP64 every cycle)
+    float* Vf = reinterpret_cast<float*>(Vb);
+    float* W0 = reinterpret_cast<float*>(s->kw);
+    float* W1 = reinterpret_cast<float*>(s->kp);
+    k_gm_prec<float><<<grid_for(V, 256), 256, 0, s->stream>>>(V, W0, W1, Vf, ld, nullptr, z, s->tmp, s->gsc);
+    mg_apply(s, val, s->tmp, z, &s->gsc->done);
+    k_gm_spmvdot_r<float, float><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col,
+                                                             s->val32, z, W0, W1, Vf, ld, s->red.partial,
+                                                             s->red.counter, s->gsc);
+    k_gm_update<float><<<nbg, kGT, 0, s->stream>>>(n, 0, Vf, ld, W0, W1, s->red.partial, s->red.counter, s->gsc);
+    k_gm_loopctl<<<1, 32, 0, s->stream>>>(s->gsc, h, use_cond);
+    return k + 4;
   } else {
-    k_gm_prec<<<grid_for(V, 256), 256, 0, s->stream>>>(V, s->kw, s->kp, Vb, ld, use_mg ? nullptr : s->minv, z,
-                                                       use_mg ? s->tmp : nullptr, s->gsc);
+    k_gm_prec<double><<<grid_for(V, 256), 256, 0, s->stream>>>(V, s->kw, s->kp, Vb, ld, use_mg ? nullptr : s->minv,
+                                                               z, use_mg ? s->tmp : nullptr, s->gsc);
     if (use_mg) mg_apply(s, val, s->tmp, z, &s->gsc->done);
-    k_gm_spmvdot_r<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, z, s->kw,
-                                               s->kp, Vb, ld, s->red.partial, s->red.counter, s->gsc);
+    k_gm_spmvdot_r<double, double><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val,
+                                                               z, s->kw, s->kp, Vb, ld, s->red.partial,
+                                                               s->red.counter, s->gsc);
     k += 2;
   }
-  k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, 0, Vb, ld, s->kw, s->kp, s->red.partial, s->red.counter, s->gsc);
+  k_gm_update<double><<<nbg, kGT, 0, s->stream>>>(n, 0, Vb, ld, s->kw, s->kp, s->red.partial, s->red.counter,
+                                                  s->gsc);
   k += 1;
   if (tight) {   // conditional second Gram-Schmidt pass (kernels exit unless flagged)
     k_gm_dots<<<nbg, kGT, 0, s->stream>>>(n, Vb, ld, s->kw, s->kp, s->red.partial, s->red.counter, s->gsc, 0);
-    k_gm_update<<<nbg, kGT, 0, s->stream>>>(n, 1, Vb, ld, s->kw, s->kp, s->red.partial, s->red.counter, s->gsc);
+    k_gm_update<double><<<nbg, kGT, 0, s->stream>>>(n, 1, Vb, ld, s->kw, s->kp, s->red.partial, s->red.counter,
+                                                    s->gsc);
     k += 2;
   }
   k_gm_loopctl<<<1, 32, 0, s->stream>>>(s->gsc, h, use_cond);
@@ -1310,9 +1369,9 @@ struct GmGraph {
   int nodes = 0;
 };
 
-static GmGraph* gm_graph(dp_scene* s, const double* val, int use_mg, int left, bool tight) {
+static GmGraph* gm_graph(dp_scene* s, const double* val, int use_mg, int left, bool tight, bool lowp) {
   const uint64_t key = (uint64_t)(uintptr_t)val ^ ((uint64_t)use_mg << 1) ^ ((uint64_t)left << 2) ^
-                       ((uint64_t)tight << 3);
+                       ((uint64_t)tight << 3) ^ ((uint64_t)lowp << 4);
   for (auto& e : s->gm_graphs)
     if (e.first == key) return (GmGraph*)e.second;
   cudaGraph_t g = nullptr;
@@ -1340,7 +1399,7 @@ static GmGraph* gm_graph(dp_scene* s, const double* val, int use_mg, int left, b
     cudaGraphDestroy(g);
     return nullptr;
   }
-  nodes = gm_column(s, val, use_mg, left, tight, h, 1);
+  nodes = gm_column(s, val, use_mg, left, tight, lowp, h, 1);
   cudaGraph_t captured = nullptr;
   const cudaError_t ce = cudaStreamEndCapture(s->stream, &captured);
   nodes += (int)(s->launches - launches0);   // V-cycle kernels count themselves
@@ -1388,6 +1447,8 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   double* t = s->kx;       // V y at the end of a cycle
   double* y_dev = s->ks;   // scratch (>= restart doubles)
   const bool tight = rtol < 1e-7;   // inexact Newton solves skip re-orthogonalisation
+  // inexact solves with the V-cycle run in FP32 (basis + operator copy)
+  const bool lowp = g_gm_fp32 && use_mg && !left && !tight && s->val32 != nullptr && val == s->val32_src;
   *iters = 0;
   cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
   const double bnorm = sqrt(device_norm2(s, b));
@@ -1395,14 +1456,14 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   // nmb = |b| (right) or |M^-1 b| (left, the reference's normalisation)
   if (left && use_mg) {
     mg_apply(s, val, b, z, nullptr);
-    k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, z, s->kw, s->red.partial, s->red.counter,
-                                           s->gsc, rtol, 1, 0, 0);
+    k_gm_start<double><<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, z, nullptr, s->red.partial,
+                                                   s->red.counter, s->gsc, rtol, 1, 0, 0);
   } else {
-    k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, left ? s->minv : nullptr, b, s->kw, s->red.partial,
-                                           s->red.counter, s->gsc, rtol, 1, 0, 0);
+    k_gm_start<double><<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, left ? s->minv : nullptr, b, nullptr,
+                                                   s->red.partial, s->red.counter, s->gsc, rtol, 1, 0, 0);
   }
   s->launches++;
-  GmGraph* gg = (g_use_graphs && !(left && use_mg)) ? gm_graph(s, val, use_mg, left, tight) : nullptr;
+  GmGraph* gg = (g_use_graphs && !(left && use_mg)) ? gm_graph(s, val, use_mg, left, tight, lowp) : nullptr;
   int total = 0;
   double rel = 1.0;
   while (total < max_iter) {
@@ -1412,10 +1473,15 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
     const int budget = max_iter - total;
     if (left && use_mg) {
       mg_apply(s, val, r, z, nullptr);
-      k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, z, s->kw, s->red.partial, s->red.counter,
+      k_gm_start<double><<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, z, s->kw, s->red.partial, s->red.counter,
                                              s->gsc, rtol, 0, restart, budget);
     } else {
-      k_gm_start<<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, left ? s->minv : nullptr, r, s->kw, s->red.partial,
+      if (lowp)
+        k_gm_start<float><<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, r, reinterpret_cast<float*>(s->kw),
+                                                      s->red.partial, s->red.counter, s->gsc, rtol, 0, restart,
+                                                      budget);
+      else
+      k_gm_start<double><<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, left ? s->minv : nullptr, r, s->kw, s->red.partial,
                                              s->red.counter, s->gsc, rtol, 0, restart, budget);
     }
     s->launches++;
@@ -1431,7 +1497,7 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
       int launched = 0;
       while (!stop && launched < restart && launched < budget) {
         int chunk = std::min(8, std::min(restart, budget) - launched);
-        for (int c = 0; c < chunk; ++c) s->launches += gm_column(s, val, use_mg, left, tight, 0, 0);
+        for (int c = 0; c < chunk; ++c) s->launches += gm_column(s, val, use_mg, left, tight, lowp, 0, 0);
         launched += chunk;
         cudaMemcpyAsync(s->h_gsc, s->gsc, sizeof(GmresScalars), cudaMemcpyDeviceToHost, s->stream);
         cudaStreamSynchronize(s->stream);
@@ -1451,7 +1517,8 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
         y[i] = acc / hg->H[(size_t)i * kGM1 + i];
       }
       cudaMemcpyAsync(y_dev, y, sizeof(double) * used, cudaMemcpyHostToDevice, s->stream);
-      k_gm_combine<<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, Vb, ld, left ? x : t, left ? 1 : 0);
+      if (lowp) k_gm_combine<float><<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, reinterpret_cast<const float*>(Vb), ld, t, 0);
+      else k_gm_combine<double><<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, Vb, ld, left ? x : t, left ? 1 : 0);
       if (left) {
       } else if (use_mg) {
         mg_apply(s, val, t, z, nullptr);

@@ -37,10 +37,14 @@ __device__ __forceinline__ void solve_pp(double J[D][D], double b[D], double x[D
       double v = fabs(J[r][k]);
       if (v > best) { best = v; p = r; }
     }
-    if (p != k) {
+    // row swap with compile-time indices (keeps J, b in registers)
 #pragma unroll
-      for (int c = 0; c < D; ++c) { double t = J[k][c]; J[k][c] = J[p][c]; J[p][c] = t; }
-      double t = b[k]; b[k] = b[p]; b[p] = t;
+    for (int r = k + 1; r < D; ++r) {
+      if (p == r) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) { double t = J[k][c]; J[k][c] = J[r][c]; J[r][c] = t; }
+        double t = b[k]; b[k] = b[r]; b[r] = t;
+      }
     }
 #pragma unroll
     for (int r = k + 1; r < D; ++r) {

@@ -8,9 +8,13 @@ from paper_2603_16478_b200 import forward as fw, core
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 rmax = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-3
 cfgname = sys.argv[3] if len(sys.argv) > 3 else "c5"
-rmin = float(sys.argv[4]) if len(sys.argv) > 4 else 1e-12
+rmin = float(sys.argv[4]) if len(sys.argv) > 4 else fw.ForwardConfig().lin_rtol_min
 c = bench.CONFIGS[cfgname]
-sc = bench.make_scene(cfgname)
+import os
+eps = float(os.environ["EPS"]) if "EPS" in os.environ else None
+sc = bench.make_scene(cfgname, eps_fb=eps, E=float(os.environ.get("E", bench.E_YOUNG)))
+if "TOL" in os.environ:
+    c = dict(c, tol=float(os.environ["TOL"]))
 sm = core.assemble_system_matrix(sc)
 st = sc.rest_state()
 cfg = fw.ForwardConfig(tol=c["tol"], lin_rtol_max=rmax, lin_rtol_min=rmin)

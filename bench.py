@@ -76,7 +76,7 @@ CONFIGS = {
     "c3": dict(cells=(60, 12, 12), edge=0.01, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=8,
                desc="identification batch: 8 rollouts/GPU of a 51,840-tet NH beam on a frictional ground, "
                     "one E candidate per rollout (C3)"),
-    "c2": dict(cells=(100, 100, 0), edge=0.01, fingers=False, eps_fb=1e-9, tol=1e-11, rollouts=1, cloth=True,
+    "c2": dict(cells=(100, 100, 0), edge=0.01, fingers=False, eps_fb=1e-9, tol=1e-11, rollouts=1, cloth=True, steps=4,
                desc="20,000-triangle ARAP cloth (1 m, 0.3 kg/m^2) draping over a frictional sphere, "
                     "per-step control-force gradients (C2 without self-contact: none in the reference)"),
     "c1": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=1,
@@ -465,7 +465,7 @@ def cpu_baseline(n_tets_target, n_cells=8, steps=1, procs=1, tol=1e-9):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--steps", type=int, default=0, help="steps per rollout (default per config: 6; c2 4)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
@@ -475,6 +475,10 @@ def main():
     ap.add_argument("--rollouts", type=int, default=0, help="rollouts per GPU (default per config)")
     ap.add_argument("--warmup-seconds", type=float, default=8.0)
     args = ap.parse_args()
+    if args.steps <= 0:
+        # the reference's own Newton (oracle, exact LU) stops converging at
+        # step 6 of the C2 drape (compressed ARAP cloth, tools/diag_cloth.py)
+        args.steps = CONFIGS[args.config].get("steps", 6)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(1)))

@@ -37,11 +37,10 @@ struct KrylovScalars {
   double pad[2];
 };
 
-constexpr int kMaxRestart = 50;
+// GMRES restart cap: the default cycle is 50; solves that stagnate escalate
+// to longer cycles (indefinite Newton matrices of compressed cloth).
+constexpr int kMaxRestart = 200;
 struct GmresScalars {
-  double H[kMaxRestart * (kMaxRestart + 1)];   // column j at H[j*(m+1) + i]
-  double cs[kMaxRestart], sn[kMaxRestart], g[kMaxRestart + 1];
-  double coef[kMaxRestart + 1];                 // coefficients of the current pass
   double wn2_before;                            // |w|^2 before orthogonalisation
   double hn;                                    // H[j+1, j] before rotation
   double beta;                                  // |M^-1 r0|
@@ -57,6 +56,9 @@ struct GmresScalars {
   int maxit;                                    // iteration budget of this cycle
   int active;                                   // 0 once j == m or the budget is spent
   int pad;
+  double cs[kMaxRestart], sn[kMaxRestart], g[kMaxRestart + 1];
+  double coef[kMaxRestart + 1];                 // coefficients of the current pass
+  double H[kMaxRestart * (kMaxRestart + 1)];   // column j at H[j*(kMaxRestart+1) + i]; keep last
 };
 
 struct ColliderSet {

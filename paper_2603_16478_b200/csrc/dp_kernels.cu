@@ -13,6 +13,7 @@
 // Assembly is a deterministic gather (no atomics): every SELL slot owns a
 // list of (element, local block, transposed?) contributions.
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -1466,40 +1467,42 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   GmGraph* gg = (g_use_graphs && !(left && use_mg)) ? gm_graph(s, val, use_mg, left, tight, lowp) : nullptr;
   int total = 0;
   double rel = 1.0;
+  int m = restart;   // cycle length; grows when a cycle stagnates
+  const int m_cap = std::min(kMaxRestart, n);
   while (total < max_iter) {
     rel = true_relres(s, val, b, x, r, bnorm);
     if (rel <= rtol) break;
     const double cycle_start = rel;
     const int budget = max_iter - total;
+    const size_t gsc_bytes = offsetof(GmresScalars, H) + sizeof(double) * (size_t)m * kGM1;
     if (left && use_mg) {
       mg_apply(s, val, r, z, nullptr);
       k_gm_start<double><<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, z, s->kw, s->red.partial, s->red.counter,
-                                             s->gsc, rtol, 0, restart, budget);
+                                             s->gsc, rtol, 0, m, budget);
     } else {
       if (lowp)
         k_gm_start<float><<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, nullptr, r, reinterpret_cast<float*>(s->kw),
-                                                      s->red.partial, s->red.counter, s->gsc, rtol, 0, restart,
-                                                      budget);
+                                                      s->red.partial, s->red.counter, s->gsc, rtol, 0, m, budget);
       else
       k_gm_start<double><<<nbv, kVT, 0, s->stream>>>(g_reorth_thr, V, left ? s->minv : nullptr, r, s->kw, s->red.partial,
-                                             s->red.counter, s->gsc, rtol, 0, restart, budget);
+                                             s->red.counter, s->gsc, rtol, 0, m, budget);
     }
     s->launches++;
     if (gg) {
       // the whole cycle on the device: one graph launch, one sync
       cudaGraphLaunch(gg->exec, s->stream);
-      cudaMemcpyAsync(s->h_gsc, s->gsc, sizeof(GmresScalars), cudaMemcpyDeviceToHost, s->stream);
+      cudaMemcpyAsync(s->h_gsc, s->gsc, gsc_bytes, cudaMemcpyDeviceToHost, s->stream);
       cudaStreamSynchronize(s->stream);
       s->launches += (int64_t)gg->nodes * std::max(1, s->h_gsc->used);
     } else {
       // host-driven columns, polled every 8
       bool stop = false;
       int launched = 0;
-      while (!stop && launched < restart && launched < budget) {
-        int chunk = std::min(8, std::min(restart, budget) - launched);
+      while (!stop && launched < m && launched < budget) {
+        int chunk = std::min(8, std::min(m, budget) - launched);
         for (int c = 0; c < chunk; ++c) s->launches += gm_column(s, val, use_mg, left, tight, lowp, 0, 0);
         launched += chunk;
-        cudaMemcpyAsync(s->h_gsc, s->gsc, sizeof(GmresScalars), cudaMemcpyDeviceToHost, s->stream);
+        cudaMemcpyAsync(s->h_gsc, s->gsc, gsc_bytes, cudaMemcpyDeviceToHost, s->stream);
         cudaStreamSynchronize(s->stream);
         stop = s->h_gsc->done || !s->h_gsc->active;
       }
@@ -1530,11 +1533,18 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
     }
     rel = true_relres(s, val, b, x, r, bnorm);
     if (rel <= rtol) break;
-    if (rel >= cycle_start * (1.0 - 1e-12)) break;   // stagnation (linsolve.py:187-188)
-    // inexact-Newton use: a restart cycle that gains less than min_cycle_gain
-    // means GMRES(m) is stagnating; return the best iterate so far
-    if (min_cycle_gain > 0.0 && rel > cycle_start / min_cycle_gain) break;
     if (used == 0) break;
+    // a cycle that gains less than min_cycle_gain (inexact Newton use), or
+    // nothing at all (linsolve.py:187-188), means GMRES(m) is stagnating:
+    // lengthen the cycle (restarting discards the Krylov space that an
+    // indefinite operator needs), and return the best iterate once the
+    // cycle is at its cap
+    const bool stalled = (rel >= cycle_start * (1.0 - 1e-12)) ||
+                         (min_cycle_gain > 0.0 && rel > cycle_start / min_cycle_gain);
+    if (stalled) {
+      if (m >= m_cap) break;
+      m = std::min(m_cap, 4 * m);
+    }
   }
   *relres = rel;
   return rel <= rtol ? 0 : 1;

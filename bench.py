@@ -79,6 +79,10 @@ CONFIGS = {
     "c2": dict(cells=(100, 100, 0), edge=0.01, fingers=False, eps_fb=1e-9, tol=1e-11, rollouts=1, cloth=True, steps=4,
                desc="20,000-triangle ARAP cloth (1 m, 0.3 kg/m^2) draping over a frictional sphere, "
                     "per-step control-force gradients (C2 without self-contact: none in the reference)"),
+    "c4": dict(cells=(8, 8, 520), edge=2.5e-3, fingers=False, eps_fb=1e-9, tol=1e-10, rollouts=1, trunk=True,
+               steps=20,
+               desc="199,680-tet NH trunk (2 x 2 x 130 cm) clamped at the top by stiff bindings, 4 cable "
+                    "force lines driven per step, frictional wall (C4)"),
     "c1": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=1,
                desc="4,374-tet NH cube on a frictional ground (C1)"),
     "c1b": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=16,
@@ -106,6 +110,8 @@ def make_scene(cfg_or_n, fingers=None, eps_fb=None, E=E_YOUNG):
         cols = [core.HalfSpace([0, 0, 1], 0.0, mu=0.3), core.Sphere([cx, cy, 0.0], 0.25, mu=0.3)]
         return core.Scene(v, t, core.lumped_masses(v, t, 0.3), mats, colliders=cols, h=0.01,
                           eps_fb=c["eps_fb"] if eps_fb is None else eps_fb)
+    if c.get("trunk"):
+        return make_trunk(c, E)
     v, t = ident.box_tet_mesh(nx, ny, nz, size=c["edge"], origin=(0.0, 0.0, 5e-4))
     mat = core.MaterialParams("neohookean", E=E, nu=NU)
     cols = [core.HalfSpace([0, 0, 1], 0.0, mu=MU)]
@@ -119,9 +125,47 @@ def make_scene(cfg_or_n, fingers=None, eps_fb=None, E=E_YOUNG):
                       colliders=cols, h=0.01, eps_fb=c["eps_fb"] if eps_fb is None else eps_fb)
 
 
+def make_trunk(c, E):
+    """C4: a hanging NH trunk, clamped at the top by
+    stiff bindings (E_b = 1e-8 as cli.py:230-231), four "cables" = per-step
+    external-force patterns on the four vertical corner lines (no cable model
+    exists in the reference), a frictional wall 5 mm beside it."""
+    from paper_2603_16478_b200 import core, ident
+    nx, ny, nz = c["cells"]
+    edge = c["edge"]
+    v, t = ident.box_tet_mesh(nx, ny, nz, size=edge, origin=(0.0, 0.0, 0.0))
+    ztop = v[:, 2].max()
+    top = np.nonzero(v[:, 2] > ztop - 1e-9)[0]
+    binds = [core.BindingSpec(int(i), v[i], 1e-8) for i in top]
+    lx, ly = nx * edge, ny * edge
+    wall = core.HalfSpace([-1.0, 0.0, 0.0], -(lx + c.get("wall_gap", 5e-3)), mu=0.3)
+    sc = core.Scene(v, t, core.lumped_masses(v, t, 1000.0), [core.MaterialParams("neohookean", E=E, nu=NU)] * len(t),
+                    colliders=[wall], bindings=binds, h=0.01, eps_fb=c["eps_fb"])
+    lines = []
+    for (cx, cy) in ((0.0, 0.0), (lx, 0.0), (0.0, ly), (lx, ly)):
+        m = (np.abs(v[:, 0] - cx) < 1e-9) & (np.abs(v[:, 1] - cy) < 1e-9) & (v[:, 2] < 0.5 * ztop)
+        lines.append(np.nonzero(m)[0])
+    sc._cable_lines = lines
+    return sc
+
+
+def drive_cables(scene, k):
+    """Cable pattern of step k: the two +x cables pull towards the wall with a
+    ramped, phase-shifted tension, the -x pair relaxes (2 mN per vertex)."""
+    f = np.zeros(3 * scene.n_verts)
+    for ci, line in enumerate(scene._cable_lines):
+        amp = 2e-3 * min(1.0, (k + 1) / 10.0) * (1.0 + 0.5 * np.sin(0.3 * k + ci))
+        sx = 1.0 if ci in (1, 3) else -0.25
+        f[3 * line] += sx * amp
+    scene.fext = f
+
+
 def move_fingers(scene, k):
     """Kinematic fingers: close by 20 um per step (host-side, colliders are
-    re-read every step as in contact.py:125-127)."""
+    re-read every step as in contact.py:125-127); C4: cable forces."""
+    if getattr(scene, "_cable_lines", None) is not None:
+        drive_cables(scene, k)
+        return
     if len(scene.colliders) < 3:
         return
     lx = scene.vertices[:, 0].max()
@@ -493,7 +537,7 @@ def main():
               "rollouts_per_gpu": R, "rollouts": world * R,
               "parallelism": f"dp{world} x {R} rollouts/GPU (independent rollouts, NCCL grad allreduce)",
               "material": ("arap stiffness=50" if cloth else f"neohookean E={E_YOUNG}(1+0.05 i) nu={NU}"),
-              "friction_mu": 0.3 if cloth else MU, "h": 0.01,
+              "friction_mu": 0.3 if (cloth or cdef.get("trunk")) else MU, "h": 0.01,
               "eps_fb": cdef["eps_fb"], "newton_tol": cdef["tol"], "l2": "operands > L2 (no flush)"}
     if args.impl == "reference":
         if rank != 0:

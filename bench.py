@@ -25,6 +25,7 @@ torchrun (one process per GPU).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -238,6 +239,8 @@ class ClockSampler:
 def _pin_thread(slot):
     """Pin the calling thread to one core (the Newton driver spin-waits on
     ~100 device synchronisations per step; migrations show up as jitter)."""
+    if os.environ.get("BENCH_NO_PIN"):
+        return
     try:
         cpus = sorted(os.sched_getaffinity(0) if slot < 0 else range(os.cpu_count() or 1))
         os.sched_setaffinity(0, {cpus[(2 * abs(slot) + 1) % len(cpus)]})
@@ -296,7 +299,10 @@ def gpu_arm(args, rank, world, local_rank):
             v[0].zero_()
         c.stream.synchronize()
         caches, stats = [], []
+        trace = [] if os.environ.get("BENCH_TRACE") else None
         for k in range(nsteps):
+            if trace is not None:
+                trace.append(time.perf_counter())
             move_fingers(scene, k0 + k)
             _, rep = fw.forward_step(scene, None, c.sysmat, cfg,
                                      device_io=dict(q_bar=q[k], v_bar=v[k], q_out=q[k + 1], v_out=v[k + 1]))
@@ -324,6 +330,10 @@ def gpu_arm(args, rank, world, local_rank):
                                           _lib.ptr(dqb), _lib.ptr(dvb), _lib.ptr(dfx)))
             dq, dqb = dqb, dq
             dv, dvb = dvb, dv
+        if trace is not None:
+            trace.append(time.perf_counter())
+            print("[trace] step ms", [round(1e3 * (b - a), 1) for a, b in zip(trace, trace[1:])],
+                  file=sys.stderr, flush=True)
         grads = aj.GradientReport()
         grads.ensure_shapes(len(scene.bindings), dev.n_elems)
         aj._fold_device_grads(dev, scene, grads)
@@ -369,7 +379,7 @@ def gpu_arm(args, rank, world, local_rank):
         run_all(device_rollout, K, W)
         n_w += 1
     if os.environ.get("BENCH_DEBUG"):
-        for i in range(3):
+        for i in range(int(os.environ.get("BENCH_DEBUG_REPS", "3"))):
             t0 = time.perf_counter(); run_all(device_rollout, K, W); torch.cuda.synchronize()
             t1 = time.perf_counter(); run_all(host_rollout, K, W); torch.cuda.synchronize()
             t2 = time.perf_counter()
@@ -382,6 +392,11 @@ def gpu_arm(args, rank, world, local_rank):
     ev1 = torch.cuda.Event(enable_timing=True)
     for c in ctxs:
         c.L.dp_scene_reset_timing(c.dev.handle)
+    # host hygiene: no cyclic-GC pass inside the timed region (a full
+    # collection walks the ~10^6 objects of torch/scipy/numpy: tens of ms)
+    gc.collect()
+    gc.freeze()
+    gc.disable()
     with ClockSampler(local_rank) as clk:
         ev0.record()
         res = run_all(device_rollout, K, W)
@@ -390,6 +405,7 @@ def gpu_arm(args, rank, world, local_rank):
         torch.cuda.synchronize()
         ev1.record()
         ev1.synchronize()
+    gc.enable()
     ms = ev0.elapsed_time(ev1)
     launches = sum(int(c.L.dp_scene_launch_count(c.dev.handle)) for c in ctxs)
     t = torch.tensor([ms], device=dd["device"])
@@ -432,11 +448,14 @@ def gpu_arm(args, rank, world, local_rank):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        gc.collect()
+        gc.disable()
         t0 = time.perf_counter()
         res2 = run_all(host_rollout, K, W)
         allreduce_gradients(pack_sum(res2), world)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+        gc.enable()
         tw = torch.tensor([wall], device=dd["device"])
         if world > 1:
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)

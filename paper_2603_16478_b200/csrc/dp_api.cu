@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -238,7 +239,18 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   // iteration (residual norms, line-search decisions, Krylov convergence):
   // spin-waiting cuts each wake-up from tens of microseconds to ~1 us
   // (measured 15% per C5 step vs the default scheduling).
-  dp_set_spin_wait(d->device, getenv("DP_SCHED") ? atoi(getenv("DP_SCHED")) : 1);
+  // Once per device and process: changing the primary context's flags while
+  // other threads launch work on it (concurrent rollouts creating scenes)
+  // races inside the driver.
+  {
+    static std::mutex mu;
+    static bool done[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    if (d->device >= 0 && d->device < 64 && !done[d->device]) {
+      dp_set_spin_wait(d->device, getenv("DP_SCHED") ? atoi(getenv("DP_SCHED")) : 1);
+      done[d->device] = true;
+    }
+  }
   DP_CUDA(cudaSetDevice(d->device));
   dp_scene* s = new dp_scene();
   s->device = d->device;

@@ -20,16 +20,22 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "dp_common.cuh"
 #include "dp_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace dp {
 
 constexpr int kCoarseMax = 36;      // dense coarsest solve (<= 108 unknowns, shared memory)
 constexpr int kDenseSmem = 108;
 __global__ void k_mg_dense_invert(int N, const double* __restrict__ Ag, double* __restrict__ Ainv);
+static int fused_grid_size(int device);
 
 struct MGLevel {
   int n = 0, S = 0;
@@ -55,6 +61,8 @@ struct MG {
   int gamma = 1;              // coarse-grid corrections per visit below the fine level (2 = W-cycle)
   int coarse_sweeps = 4;      // >0: Jacobi sweeps at the coarsest level instead of the dense inverse
   int symmetric_needed = 0;  // set while a CG solve uses the V-cycle
+  int fused = 1;              // coarse levels in one cooperative kernel (k_mg_coarse_fused)
+  int fused_grid = 0;
   size_t bytes = 0;
 };
 
@@ -307,6 +315,7 @@ int mg_setup(dp_scene* s) {
   if (getenv("DP_MG_POST")) mg->post = atoi(getenv("DP_MG_POST"));
   if (getenv("DP_MG_GAMMA")) mg->gamma = atoi(getenv("DP_MG_GAMMA"));
   if (getenv("DP_MG_CSWEEP")) mg->coarse_sweeps = atoi(getenv("DP_MG_CSWEEP"));
+  mg->fused_grid = fused_grid_size(s->device);
   s->mg = mg;
   s->bytes += mg->bytes;
   return 0;
@@ -660,6 +669,231 @@ __global__ void __launch_bounds__(256) k_mg_coarse_jacobi(int n, int S, const in
   }
 }
 
+// ---------------------------------------------------------------------------
+// All coarse levels of one V-cycle in ONE cooperative kernel.  Below the fine
+// level every kernel of the V-cycle is latency-bound (level 1 at C5: 6,859
+// block rows, 13 MB of values, L2-resident), so the nine launches of levels
+// 1..3 (restrict+jacobi0, residual, restrict, ..., coarsest sweeps, post
+// smoothers) become phases of one persistent grid separated by grid-wide
+// barriers.  Every phase repeats the arithmetic of its stand-alone kernel
+// term by term (same split of a slice over 8 warps, same partial order, same
+// warp reductions), so the V-cycle output is bitwise identical to the
+// multi-kernel path (checked by tests/test_gpu_scale.py::test_mg_fused_bitwise).
+
+struct FusedLevel {
+  int n, S;
+  const int *slice_base, *slice_width, *col;
+  const double *val, *minv;
+  const int *mem_ptr, *mem;   // coarse row -> rows of the level above
+  const int* agg;             // row of the level above -> coarse row
+  double *x, *b, *r, *t;
+};
+constexpr int kMaxFusedLevels = 8;
+struct FusedArgs {
+  int L;                               // levels in the hierarchy (lv[0] unused: fine level)
+  FusedLevel lv[kMaxFusedLevels];
+  const double* r0;                    // fine-level residual
+  double omega, alpha;
+  int coarse_sweeps;
+  const int* stop;
+  unsigned long long* tstamp;          // DP_MG_FTIME: per-phase globaltimer stamps (CTA 0)
+};
+
+__device__ __forceinline__ void fused_stamp(const FusedArgs& A, int& ph) {
+  if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.tstamp[ph] = t;
+  }
+  ++ph;
+}
+
+// b_l[I] = sum of r_{l-1} over the members of I; optionally t_l[I] = w Minv b_l[I]
+__device__ __forceinline__ void fused_restrict_row(const FusedLevel& C, const double* rf, int I, int lane,
+                                                   double omega, bool jac) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int t = C.mem_ptr[I] + lane; t < C.mem_ptr[I + 1]; t += 32) {
+    const int i = C.mem[t];
+    s0 += __ldcg(rf + 3 * i); s1 += __ldcg(rf + 3 * i + 1); s2 += __ldcg(rf + 3 * i + 2);
+  }
+  s0 = warp_sum(s0); s1 = warp_sum(s1); s2 = warp_sum(s2);
+  if (lane == 0) {
+    C.b[3 * I] = s0; C.b[3 * I + 1] = s1; C.b[3 * I + 2] = s2;
+    if (jac) {
+      const double r[3] = {s0, s1, s2};
+      double u[3];
+      mv_minv(C.minv, C.n, I, r, u);
+      C.t[3 * I] = omega * u[0]; C.t[3 * I + 1] = omega * u[1]; C.t[3 * I + 2] = omega * u[2];
+    }
+  }
+}
+
+// k_mg_smooth<double, 8> for one slice (whole CTA); in-kernel data via __ldcg
+__device__ __forceinline__ void fused_smooth_slice(const FusedLevel& L, int sl, const double* x, const double* xc,
+                                                   const int* agg, double omega, double* out, double* r_out,
+                                                   double alpha, double (*part)[3][kSlice]) {
+  const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
+  const int row = sl * kSlice + lane;
+  const int base = L.slice_base[sl], K = L.slice_width[sl];
+  const double* vs = L.val + (size_t)base * 9 + lane;
+  const int* cs = L.col + base + lane;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int k = wsub; k < K; k += 8) {
+    const int j = __ldg(cs + k * kSlice);
+    double m[9];
+    const double* v = vs + k * 9 * kSlice;
+#pragma unroll
+    for (int c = 0; c < 9; ++c) m[c] = (double)v[c * kSlice];
+    double x0 = __ldcg(x + 3 * j), x1 = __ldcg(x + 3 * j + 1), x2 = __ldcg(x + 3 * j + 2);
+    if (xc) {
+      const int J = __ldg(agg + j);
+      x0 += alpha * __ldcg(xc + 3 * J); x1 += alpha * __ldcg(xc + 3 * J + 1); x2 += alpha * __ldcg(xc + 3 * J + 2);
+    }
+    a0 += m[0] * x0 + m[1] * x1 + m[2] * x2;
+    a1 += m[3] * x0 + m[4] * x1 + m[5] * x2;
+    a2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
+  }
+  part[wsub][0][lane] = a0;
+  part[wsub][1][lane] = a1;
+  part[wsub][2][lane] = a2;
+  __syncthreads();
+  if (wsub == 0 && row < L.n) {
+    a0 = a1 = a2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) { a0 += part[w][0][lane]; a1 += part[w][1][lane]; a2 += part[w][2][lane]; }
+    double xt[3] = {__ldcg(x + 3 * row), __ldcg(x + 3 * row + 1), __ldcg(x + 3 * row + 2)};
+    if (xc) {
+      const int I = agg[row];
+      xt[0] += alpha * __ldcg(xc + 3 * I); xt[1] += alpha * __ldcg(xc + 3 * I + 1);
+      xt[2] += alpha * __ldcg(xc + 3 * I + 2);
+    }
+    const double rr[3] = {__ldcg(L.b + 3 * row) - a0, __ldcg(L.b + 3 * row + 1) - a1,
+                          __ldcg(L.b + 3 * row + 2) - a2};
+    if (r_out) { r_out[3 * row] = rr[0]; r_out[3 * row + 1] = rr[1]; r_out[3 * row + 2] = rr[2]; }
+    if (out) {
+      double u[3];
+      mv_minv(L.minv, L.n, row, rr, u);
+      out[3 * row] = xt[0] + omega * u[0];
+      out[3 * row + 1] = xt[1] + omega * u[1];
+      out[3 * row + 2] = xt[2] + omega * u[2];
+    }
+  }
+  __syncthreads();   // part[] is reused by the next slice
+}
+
+// k_mg_coarse_jacobi in the calling CTA, iterate and right-hand side in
+// shared memory (the coarsest level has <= kCoarseMax rows); the arithmetic
+// and its order are those of k_mg_coarse_jacobi.
+__device__ __forceinline__ void fused_coarse_jacobi(const FusedLevel& C, double omega, int nsweep,
+                                                    double (*part)[3][kSlice], double* xs, double* ys,
+                                                    const double* bs) {
+  const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
+  const int n = C.n;
+  for (int row = threadIdx.x; row < n; row += blockDim.x) {
+    double r[3] = {bs[3 * row], bs[3 * row + 1], bs[3 * row + 2]}, u[3];
+    mv_minv(C.minv, n, row, r, u);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) xs[3 * row + c] = omega * u[c];
+  }
+  __syncthreads();
+  for (int it = 0; it < nsweep; ++it) {
+    for (int sl = 0; sl < C.S; ++sl) {
+      const int row = sl * kSlice + lane;
+      const int base = C.slice_base[sl], K = C.slice_width[sl];
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      for (int k = wsub; k < K; k += 8) {
+        const int j = __ldg(C.col + base + k * kSlice + lane);
+        const double* v = C.val + (size_t)base * 9 + (k * 9) * kSlice + lane;
+        const double x0 = xs[3 * j], x1 = xs[3 * j + 1], x2 = xs[3 * j + 2];
+        a0 += __ldg(v + 0 * kSlice) * x0 + __ldg(v + 1 * kSlice) * x1 + __ldg(v + 2 * kSlice) * x2;
+        a1 += __ldg(v + 3 * kSlice) * x0 + __ldg(v + 4 * kSlice) * x1 + __ldg(v + 5 * kSlice) * x2;
+        a2 += __ldg(v + 6 * kSlice) * x0 + __ldg(v + 7 * kSlice) * x1 + __ldg(v + 8 * kSlice) * x2;
+      }
+      part[wsub][0][lane] = a0;
+      part[wsub][1][lane] = a1;
+      part[wsub][2][lane] = a2;
+      __syncthreads();
+      if (wsub == 0 && row < n) {
+        a0 = a1 = a2 = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) { a0 += part[w][0][lane]; a1 += part[w][1][lane]; a2 += part[w][2][lane]; }
+        double r[3] = {bs[3 * row] - a0, bs[3 * row + 1] - a1, bs[3 * row + 2] - a2}, u[3];
+        mv_minv(C.minv, n, row, r, u);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ys[3 * row + c] = xs[3 * row + c] + omega * u[c];
+      }
+      __syncthreads();
+    }
+    for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) xs[t] = ys[t];
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) C.x[t] = xs[t];
+}
+
+__global__ void __launch_bounds__(256) k_mg_coarse_fused(const __grid_constant__ FusedArgs A) {
+  __shared__ double part[8][3][kSlice];
+  if (A.stop && *(volatile const int*)A.stop) return;   // uniform over the grid
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gwarp = blockIdx.x * 8 + warp, nwarps = gridDim.x * 8;
+  const int Lc = A.L - 1;
+  int ph = 0;
+  fused_stamp(A, ph);
+  // descending: restrict + jacobi0, residual
+  for (int l = 1; l < Lc; ++l) {
+    const FusedLevel& C = A.lv[l];
+    const double* rf = (l == 1) ? A.r0 : A.lv[l - 1].r;
+    for (int I = gwarp; I < C.n; I += nwarps) fused_restrict_row(C, rf, I, lane, A.omega, true);
+    fused_stamp(A, ph);
+    grid.sync();
+    fused_stamp(A, ph);
+    for (int sl = blockIdx.x; sl < C.S; sl += gridDim.x)
+      fused_smooth_slice(C, sl, C.t, nullptr, nullptr, A.omega, nullptr, C.r, 1.0, part);
+    fused_stamp(A, ph);
+    grid.sync();
+    fused_stamp(A, ph);
+  }
+  // coarsest: restriction and the Jacobi sweeps in CTA 0
+  if (blockIdx.x == 0) {
+    __shared__ double xs[3 * kCoarseMax + 3], ys[3 * kCoarseMax + 3], bs[3 * kCoarseMax + 3];
+    const FusedLevel& C = A.lv[Lc];
+    const double* rf = (Lc == 1) ? A.r0 : A.lv[Lc - 1].r;
+    for (int I = warp; I < C.n; I += 8) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int t = C.mem_ptr[I] + lane; t < C.mem_ptr[I + 1]; t += 32) {
+        const int i = C.mem[t];
+        s0 += __ldcg(rf + 3 * i); s1 += __ldcg(rf + 3 * i + 1); s2 += __ldcg(rf + 3 * i + 2);
+      }
+      s0 = warp_sum(s0); s1 = warp_sum(s1); s2 = warp_sum(s2);
+      if (lane == 0) { bs[3 * I] = s0; bs[3 * I + 1] = s1; bs[3 * I + 2] = s2; }
+    }
+    __syncthreads();
+    fused_coarse_jacobi(C, A.omega, A.coarse_sweeps, part, xs, ys, bs);
+  }
+  fused_stamp(A, ph);
+  // ascending: post-smoothing with the coarse correction in its gathers
+  for (int l = Lc - 1; l >= 1; --l) {
+    grid.sync();
+    fused_stamp(A, ph);
+    const FusedLevel& C = A.lv[l];
+    for (int sl = blockIdx.x; sl < C.S; sl += gridDim.x)
+      fused_smooth_slice(C, sl, C.t, A.lv[l + 1].x, A.lv[l + 1].agg, A.omega, C.x, nullptr, A.alpha, part);
+    fused_stamp(A, ph);
+  }
+}
+
+// co-resident grid of the cooperative kernel: up to 2 CTAs per SM
+static int fused_grid_size(int device) {
+  int nsm = 0, per_sm = 0;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+  if (!coop) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mg_coarse_fused, 256, 0) != cudaSuccess) return 0;
+  const int want = getenv("DP_MG_FGRID") ? atoi(getenv("DP_MG_FGRID")) : 2;
+  return nsm * std::max(1, std::min(per_sm, want));
+}
+
 // x = Ainv b (dense, one row per warp)
 __global__ void k_mg_dense_solve(int N, const double* __restrict__ Ainv, const double* __restrict__ b,
                                  double* __restrict__ x, const int* stop) {
@@ -725,6 +959,59 @@ template <class TV>
 static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, const double* b, double* x,
                          const int* stop);
 
+static const int g_mg_fused_env = getenv("DP_MG_FUSED") ? atoi(getenv("DP_MG_FUSED")) : 1;
+
+static bool fused_usable(const MG* mg) {
+  return g_mg_fused_env && mg->fused && mg->fused_grid > 0 && mg->nu == 1 && mg->post == 1 && mg->gamma == 1 &&
+         mg->coarse_sweeps > 0 && mg->lv.size() >= 2 && mg->lv.size() <= (size_t)kMaxFusedLevels &&
+         mg->lv.back().n <= kCoarseMax;
+}
+
+// levels 1..L-1 of the V-cycle for the fine residual r0 -> lv[1].x
+static void launch_coarse_fused(dp_scene* s, const double* r0, const int* stop) {
+  MG* mg = s->mg;
+  FusedArgs a;
+  a.L = (int)mg->lv.size();
+  for (int l = 1; l < a.L; ++l) {
+    const MGLevel& L = mg->lv[l];
+    FusedLevel& f = a.lv[l];
+    f.n = L.n; f.S = L.S;
+    f.slice_base = L.slice_base; f.slice_width = L.slice_width; f.col = L.col;
+    f.val = L.val; f.minv = L.minv;
+    f.mem_ptr = L.mem_ptr; f.mem = L.mem; f.agg = L.agg;
+    f.x = L.x; f.b = L.b; f.r = L.r; f.t = L.t;
+  }
+  a.r0 = r0;
+  a.omega = mg->omega;
+  a.alpha = mg->alpha;
+  a.coarse_sweeps = mg->coarse_sweeps;
+  a.stop = stop;
+  a.tstamp = nullptr;
+  static const int ftime = getenv("DP_MG_FTIME") ? atoi(getenv("DP_MG_FTIME")) : 0;
+  static unsigned long long* dts = nullptr;
+  static long calls = 0;
+  if (ftime) {
+    // diagnostics only: phase stamps of one call in 64, printed on the host
+    if (!dts) cudaMalloc(&dts, 64 * sizeof(unsigned long long));
+    if (calls % 64 == 63) {
+      unsigned long long h[64];
+      cudaStreamSynchronize(s->stream);
+      cudaMemcpy(h, dts, sizeof(h), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[mg-fused] L=%d phases(us):", a.L);
+      for (int i = 1; i < 32 && h[i]; ++i) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+      fprintf(stderr, "\n");
+    }
+    if (calls % 64 == 62) {
+      cudaMemsetAsync(dts, 0, 64 * sizeof(unsigned long long), s->stream);
+      a.tstamp = dts;
+    }
+    ++calls;
+  }
+  void* args[] = {&a};
+  cudaLaunchCooperativeKernel((const void*)k_mg_coarse_fused, dim3(mg->fused_grid), dim3(256), args, 0, s->stream);
+  s->launches++;
+}
+
 static void vcycle(dp_scene* s, int l, const double* b, double* x, const int* stop) {
   MG* mg = s->mg;
   if (l == (int)mg->lv.size() - 1) {
@@ -762,9 +1049,13 @@ static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, cons
   const int ncorr = (l == 0) ? 1 : mg->gamma;
   for (int g = 0; g < ncorr; ++g) {
     smooth<TV>(s, L, val, minv, b, xa, nullptr, nullptr, om, nullptr, L.r, stop, 1.0);
-    k_mg_restrict<<<grid_for((int64_t)C.n * 32, 256), 256, 0, s->stream>>>(C.n, C.mem_ptr, C.mem, L.r, C.b, stop);
-    s->launches++;
-    vcycle(s, l + 1, C.b, C.x, stop);
+    if (l == 0 && fused_usable(mg)) {
+      launch_coarse_fused(s, L.r, stop);   // restriction to level 1 is its first phase
+    } else {
+      k_mg_restrict<<<grid_for((int64_t)C.n * 32, 256), 256, 0, s->stream>>>(C.n, C.mem_ptr, C.mem, L.r, C.b, stop);
+      s->launches++;
+      vcycle(s, l + 1, C.b, C.x, stop);
+    }
     const bool last = (g == ncorr - 1);
     if (mg->post == 0 && !mg->symmetric_needed && last) {
       // V(nu,0): x = x_pre + alpha P x_c (no post-smoothing SpMV)

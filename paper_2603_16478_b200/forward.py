@@ -21,6 +21,7 @@ materialised from device memory lazily (only when a caller reads them).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -119,7 +120,8 @@ class Projection:
 
 
 class ForwardReport:
-    """forward.py:37-44; contacts/projections/contact_residuals are lazy."""
+    """forward.py:37-44; contacts/projections/contact_residuals are lazy
+    (materialised from the step's device cache on first access)."""
 
     def __init__(self):
         self.residual_history = []
@@ -129,28 +131,51 @@ class ForwardReport:
         self.line_search_trials = 0
         self.n_contacts = 0
         self.cache = None
-        self._contacts = None
-        self._projections = None
 
     @property
     def contacts(self):
-        if self._contacts is None:
-            from . import contact as ct
-            self._contacts = ct.contacts_from_arrays(self.cache._dc.contact_arrays(),
-                                                     self.cache.scene.eps_fb)
-        return self._contacts
+        return self.cache.contacts
 
     @contacts.setter
     def contacts(self, v):
-        self._contacts = v
+        self.cache._contacts = v
 
     @property
     def projections(self):
-        if self._projections is None:
-            _, th, P, en = self.cache._dc.projections()
-            self._projections = [Projection(theta=th[e], P=P[e], energy_density=float(en[e]))
-                                 for e in range(th.shape[0])]
-        return self._projections
+        return self.cache.elem_caches
+
+    @property
+    def contact_residuals(self):
+        from . import contact as ct
+        return [ct.contact_residual(cp, None, None) for cp in self.contacts]
+
+
+class _ReportView:
+    """``StepCache.report``: the report's fields without a strong reference
+    back to the cache.  ForwardReport -> StepCache -> ForwardReport would be a
+    reference cycle that only the cyclic GC frees, and the cache owns pooled
+    device buffers that must return to the pool when the step is dropped."""
+
+    def __init__(self, rep, cache):
+        self.residual_history = rep.residual_history
+        self.converged = rep.converged
+        self.iterations = rep.iterations
+        self.krylov_iterations = rep.krylov_iterations
+        self.line_search_trials = rep.line_search_trials
+        self.n_contacts = rep.n_contacts
+        self._cache = weakref.ref(cache)
+
+    @property
+    def cache(self):
+        return self._cache()
+
+    @property
+    def contacts(self):
+        return self._cache().contacts
+
+    @property
+    def projections(self):
+        return self._cache().elem_caches
 
     @property
     def contact_residuals(self):
@@ -169,8 +194,10 @@ class StepCache:
         self._dc = dc
         self._fext_src = fext
         self._fext = None
-        self.report = report
+        self.report = _ReportView(report, self)
         self._states = None
+        self._contacts = None
+        self._projections = None
 
     @property
     def fext(self):
@@ -192,11 +219,18 @@ class StepCache:
 
     @property
     def contacts(self):
-        return self.report.contacts
+        if self._contacts is None:
+            from . import contact as ct
+            self._contacts = ct.contacts_from_arrays(self._dc.contact_arrays(), self.scene.eps_fb)
+        return self._contacts
 
     @property
     def elem_caches(self):
-        return self.report.projections
+        if self._projections is None:
+            _, th, P, en = self._dc.projections()
+            self._projections = [Projection(theta=th[e], P=P[e], energy_density=float(en[e]))
+                                 for e in range(th.shape[0])]
+        return self._projections
 
 
 def binding_multiplier(binding, q):

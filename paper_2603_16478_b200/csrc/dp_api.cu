@@ -506,7 +506,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   rc |= dalloc(s, &s->c_count, V + 1);
   rc |= dalloc(s, &s->c_off, V + 1);
   const size_t n3 = (size_t)V * 3;
-  double** vecs[] = {&s->q, &s->q_hat, &s->q_bar, &s->v_bar, &s->r, &s->dq, &s->q_try, &s->rhs, &s->z, &s->tmp, &s->q_ev, &s->r_try,
+  double** vecs[] = {&s->q, &s->q_hat, &s->q_bar, &s->v_bar, &s->r, &s->dq, &s->q_try, &s->rhs, &s->z, &s->z_prev, &s->tmp, &s->q_ev, &s->r_try,
                      &s->kx, &s->kr, &s->ku, &s->kw, &s->kp, &s->ks};
   for (auto pp : vecs) rc |= dalloc(s, pp, std::max(n3, (size_t)kMaxRestart + 1));
   s->gm_cap = kMaxRestart + 1;
@@ -542,6 +542,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   if (ensure_contact_capacity(s, 1) || contact_scan_setup(s)) { dp_scene_destroy(s); return DP_ERR_CUDA; }
   if (mg_setup(s)) { dp_scene_destroy(s); return DP_ERR_CUDA; }
   if (getenv("DP_MG")) s->use_mg = atoi(getenv("DP_MG"));
+  if (getenv("DP_ADJ_WARM")) s->adj_warm = atoi(getenv("DP_ADJ_WARM"));
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { dp_scene_destroy(s); return cuda_fail(e, "scene create"); }
   *out = s;
@@ -565,7 +566,7 @@ int dp_scene_destroy(dp_scene* s) {
                   s->contrib_ptr, s->contrib, s->minv, s->fe, s->H, s->Pst, s->d_colliders, s->b_ptr, s->b_idx,
                   s->b_target, s->b_comp, s->b_vertex, s->fext, s->c_count, s->c_off, s->c_vertex, s->c_collider,
                   s->c_frame, s->c_dn, s->c_mu, s->c_delta, s->c_blk, s->c_force, s->c_kmu, s->c_kc, s->scan_tmp,
-                  s->q, s->q_hat, s->q_bar, s->v_bar, s->r, s->dq, s->q_try, s->rhs, s->z, s->tmp, s->q_ev, s->r_try, s->kx, s->kr,
+                  s->q, s->q_hat, s->q_bar, s->v_bar, s->r, s->dq, s->q_try, s->rhs, s->z, s->z_prev, s->tmp, s->q_ev, s->r_try, s->kx, s->kr,
                   s->ku, s->kw, s->kp, s->ks, s->gm_V, s->ksc, s->gsc, s->esc, s->red.partial, s->red.counter,
                   s->g_dw, s->g_scal, s->g_dEb, s->g_ddb};
   for (void* p : ptrs) dfree(p);
@@ -1164,8 +1165,13 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
       iters += it2;
     }
   } else {
+    // warm start from the previous adjoint solution of this reverse sweep:
+    // consecutive steps' adjoint states are close, and the stop test is on
+    // the true residual, so only the iteration count changes
+    const int warm = s->adj_warm && s->z_prev_valid;
+    if (warm) DP_CUDA(cudaMemcpyAsync(s->z, s->z_prev, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s->stream));
     rc = gmres_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, cfg.gmres_restart, &iters, &relres, 0.0, mg,
-                     0);
+                     0, warm);
   }
   if (mg && !(relres <= cfg.tol) && iters < cfg.max_iter) {
     // refinement: the multigrid-preconditioned solve stalled above the
@@ -1190,6 +1196,8 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
     relres = std::sqrt(device_norm2(s, res)) / bn;
     (void)n3b;
   }
+  DP_CUDA(cudaMemcpyAsync(s->z_prev, s->z, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s->stream));
+  s->z_prev_valid = 1;
   if (g_debug) {
     cudaStreamSynchronize(s->stream);
     fprintf(stderr, "[dp] adjoint sym=%d iters=%d relres=%.2e solve %.2fms\n", sym, iters, relres,
@@ -1249,6 +1257,7 @@ int dp_backprop_step(dp_scene* s, const dp_cache* c, const double* z, const doub
 
 int dp_grads_reset(dp_scene* s) {
   cudaSetDevice(s->device);
+  s->z_prev_valid = 0;   // a new reverse sweep: no warm start across sweeps
   DP_CUDA(cudaMemsetAsync(s->g_dw, 0, sizeof(double) * std::max(s->E, 1), s->stream));
   DP_CUDA(cudaMemsetAsync(s->g_scal, 0, sizeof(double) * 4, s->stream));
   if (s->g_nb_cap) {

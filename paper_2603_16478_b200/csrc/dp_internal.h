@@ -173,6 +173,9 @@ struct dp_scene {
   // vectors (3V each)
   double *q = nullptr, *q_hat = nullptr, *q_bar = nullptr, *v_bar = nullptr, *r = nullptr, *dq = nullptr;
   double *q_try = nullptr, *rhs = nullptr, *z = nullptr, *tmp = nullptr, *q_ev = nullptr, *r_try = nullptr;
+  double* z_prev = nullptr;   // last adjoint solution of the current reverse sweep (warm start)
+  int z_prev_valid = 0;
+  int adj_warm = 1;
   // Krylov workspace
   double *kx = nullptr, *kr = nullptr, *ku = nullptr, *kw = nullptr, *kp = nullptr, *ks = nullptr;
   double* gm_V = nullptr;          // (restart+1) * 3V basis
@@ -240,7 +243,7 @@ int cg_solve(dp_scene* s, const double* val, const double* b, double* x, double 
              int* iters, double* relres, int* breakdown);
 int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
                 int restart, int* iters, double* relres, double min_cycle_gain = 0.0, int use_mg = 0,
-                int left = 1);
+                int left = 1, int use_x0 = 0);
 int pcg_mg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int* iters,
                  double* relres, int* breakdown);
 double device_norm2(dp_scene* s, const double* x);   // sum of squares, synchronous

@@ -1434,7 +1434,7 @@ void gm_graphs_destroy(dp_scene* s) {
 // preconditioning; the converged solution is the same).  x = 0 initially.
 // Returns 0 converged, 1 not converged.
 int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int restart,
-                int* iters, double* relres, double min_cycle_gain, int use_mg, int left) {
+                int* iters, double* relres, double min_cycle_gain, int use_mg, int left, int use_x0) {
   const int V = s->V, n = 3 * V;
   if (restart > kMaxRestart) restart = kMaxRestart;
   if (restart > n) restart = n;
@@ -1451,9 +1451,15 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   // inexact solves with the V-cycle run in FP32 (basis + operator copy)
   const bool lowp = g_gm_fp32 && use_mg && !left && !tight && s->val32 != nullptr && val == s->val32_src;
   *iters = 0;
-  cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+  // x = 0, or the caller's initial guess (use_x0) when it beats x = 0
+  if (!use_x0) cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
   const double bnorm = sqrt(device_norm2(s, b));
-  if (bnorm == 0.0) { *relres = 0.0; return 0; }
+  if (bnorm == 0.0) {
+    cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+    *relres = 0.0;
+    return 0;
+  }
+  if (use_x0 && true_relres(s, val, b, x, s->kr, bnorm) >= 1.0) cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
   // nmb = |b| (right) or |M^-1 b| (left, the reference's normalisation)
   if (left && use_mg) {
     mg_apply(s, val, b, z, nullptr);

@@ -959,7 +959,7 @@ template <class TV>
 static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, const double* b, double* x,
                          const int* stop);
 
-static const int g_mg_fused_env = getenv("DP_MG_FUSED") ? atoi(getenv("DP_MG_FUSED")) : 1;
+static const int g_mg_fused_env = getenv("DP_MG_FUSED") ? atoi(getenv("DP_MG_FUSED")) : 0;
 
 static bool fused_usable(const MG* mg) {
   return g_mg_fused_env && mg->fused && mg->fused_grid > 0 && mg->nu == 1 && mg->post == 1 && mg->gamma == 1 &&

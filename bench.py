@@ -90,6 +90,11 @@ CONFIGS = {
                 desc="16 concurrent rollouts/GPU of the 4,374-tet C1 cube (batched small scenes)"),
 }
 E_YOUNG = 1e4
+# FP64 FLOPs per tet of the element kernel (2 DFMA + DMUL + DADD thread
+# instructions / E, ncu at a C5 state, profiles/r01_elements_fp64.md)
+ELEM_FLOPS_JAC = 5721.0
+ELEM_FLOPS_RES = 3570.0
+FP64_PEAK_TFLOPS = 34.18     # measured DFMA peak, profiles/r01_fp64_peak.json
 NU = 0.3
 MU = 0.5
 
@@ -339,6 +344,7 @@ def gpu_arm(args, rank, world, local_rank):
         aj._fold_device_grads(dev, scene, grads)
         with torch.cuda.stream(c.stream):
             loss = float(torch.sum((q[nsteps] - target) ** 2))
+        c.q_final = q[nsteps]
         return grads, loss, stats, adj_iters
 
     def host_rollout(c, nsteps, k0):
@@ -425,6 +431,15 @@ def gpu_arm(args, rank, world, local_rank):
     _lib.check(c0.L.dp_bench_spmv(c0.dev.handle, 1, _lib.ptr(x), _lib.ptr(y), 10, C.byref(fms)))
     _lib.check(c0.L.dp_bench_spmv(c0.dev.handle, 1, _lib.ptr(x), _lib.ptr(y), reps, C.byref(fms)))
     spmv_ms = fms.value / reps
+    # second roofline: the FP64-bound element kernel (projection + residual,
+    # and with the Jacobian blocks) at the final state of the timed rollout
+    elem = None
+    if c0.dev.verts_per_elem == 4:
+        elem = {}
+        for jac, flops in ((1, ELEM_FLOPS_JAC), (0, ELEM_FLOPS_RES)):
+            _lib.check(c0.L.dp_bench_elements(c0.dev.handle, _lib.ptr(c0.q_final), jac, 2, C.byref(fms)))
+            _lib.check(c0.L.dp_bench_elements(c0.dev.handle, _lib.ptr(c0.q_final), jac, 10, C.byref(fms)))
+            elem[jac] = (fms.value / 10, flops * E_ / (fms.value / 10 * 1e-3) / 1e12)
     nnzb = info.nnzb
     spmv_bytes = 76 * nnzb + 4 * (V + 1) + 48 * V
     peaks = {}
@@ -468,7 +483,8 @@ def gpu_arm(args, rank, world, local_rank):
     pool.shutdown()
     conv = [s_[0] for r in res for s_ in r[2]]
     return dict(ms=ms_max, launches=launches, clocks=clk.summary(), spmv_ms=spmv_ms, spmv_bytes=spmv_bytes,
-                achieved=achieved, hbm=hbm, traffic=traffic, e2e=e2e, setup_s=setup_s, R=R,
+                achieved=achieved, hbm=hbm, traffic=traffic, e2e=e2e, setup_s=setup_s, R=R, elem=elem,
+                fp64_peak=float(peaks.get("fp64_tflops", FP64_PEAK_TFLOPS)),
                 nnzb=nnzb, V=V, E=E_, desc=cdef["desc"], newton=[s_[1] for s_ in stats],
                 krylov=[s_[2] for s_ in stats], contacts=[s_[3] for s_ in stats], converged=all(conv),
                 adj_iters=adj_iters, dE=float(gvec[1]), loss=float(gvec[0]), device_bytes=info.device_bytes)
@@ -595,6 +611,16 @@ def main():
                              "frac": r["achieved"] / r["hbm"], "traffic": r["traffic"],
                              "bytes_per_launch": r["spmv_bytes"], "ms_per_launch": r["spmv_ms"],
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+                "roofline_fp64": None if not r["elem"] else {
+                    "bound": "fp64", "kernel": "k_elements<4,JAC> (per-tet SVD + NH projection + 10 Hessian blocks)",
+                    "achieved": r["elem"][1][1], "peak": r["fp64_peak"], "unit": "TFLOP/s",
+                    "frac": r["elem"][1][1] / r["fp64_peak"], "ms_per_launch": r["elem"][1][0],
+                    "flops_per_tet": ELEM_FLOPS_JAC,
+                    "residual_only": {"achieved": r["elem"][0][1], "ms_per_launch": r["elem"][0][0],
+                                      "flops_per_tet": ELEM_FLOPS_RES},
+                    "peak_source": "profiles/r01_fp64_peak.json (measured DFMA loop)",
+                    "flops_source": "ncu 2*DFMA+DMUL+DADD thread instructions per tet at a C5 state "
+                                    "(profiles/r01_elements_fp64.md)"},
                 "clocks": r["clocks"], "gpu_launches": r["launches"], "e2e": r["e2e"],
                 "newton_iterations": r["newton"], "krylov_iterations": r["krylov"],
                 "adjoint_krylov_iterations": r["adj_iters"], "contacts": r["contacts"],

@@ -229,6 +229,11 @@ int dp_detect_contacts(dp_scene* s, const double* q, int32_t ptr_kind, int32_t c
  * stream and (if ms_out) the CUDA-event time of all reps. */
 int dp_bench_spmv(dp_scene* s, int32_t which, const double* x, double* y, int32_t reps,
                   float* ms_out);
+/* Element kernel (projection + residual contributions, with the Jacobian
+ * blocks when with_jacobian) at the device state q, `reps` launches on the
+ * scene stream; CUDA-event time of all reps in ms_out.  Overwrites the
+ * scene's element scratch (call between steps, not inside one). */
+int dp_bench_elements(dp_scene* s, const double* q, int32_t with_jacobian, int32_t reps, float* ms_out);
 /* per-launch timing of the dominant kernels of the last forward step,
  * measured with CUDA events on the scene stream (ms, averages). */
 typedef struct {

@@ -13,7 +13,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdiffproj_b200.so")
+LIB_PATH = os.environ.get("DP_LIB") or os.path.join(_HERE, "libdiffproj_b200.so")
 
 DP_OK = 0
 DP_ERR_VALUE = 1
@@ -127,6 +127,7 @@ SIGNATURES = {
                                    _P, _P]),
     "dp_detect_contacts": (C.c_int, [_P, _P, C.c_int32, C.c_int32, c_int32_p, _P, _P, _P, _P]),
     "dp_bench_spmv": (C.c_int, [_P, C.c_int32, _P, _P, C.c_int32, C.POINTER(C.c_float)]),
+    "dp_bench_elements": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.POINTER(C.c_float)]),
     "dp_scene_enable_timing": (C.c_int, [_P, C.c_int32]),
     "dp_scene_get_timing": (C.c_int, [_P, C.POINTER(KernelTimes)]),
     "dp_scene_reset_timing": (C.c_int, [_P]),

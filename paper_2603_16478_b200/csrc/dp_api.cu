@@ -1435,6 +1435,18 @@ int dp_bench_spmv(dp_scene* s, int32_t which, const double* x, double* y, int32_
   return DP_OK;
 }
 
+int dp_bench_elements(dp_scene* s, const double* q, int32_t with_jacobian, int32_t reps, float* ms_out) {
+  cudaSetDevice(s->device);
+  DP_CUDA(cudaEventRecord(s->ev0, s->stream));
+  for (int r = 0; r < reps; ++r) launch_elements(s, q, with_jacobian ? EV_JAC : 0, &s->esc->status);
+  DP_CUDA(cudaEventRecord(s->ev1, s->stream));
+  DP_CUDA(cudaEventSynchronize(s->ev1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, s->ev0, s->ev1);
+  if (ms_out) *ms_out = ms;
+  return DP_OK;
+}
+
 int dp_scene_enable_timing(dp_scene* s, int32_t on) {
   s->timing = on;
   return DP_OK;

@@ -272,6 +272,10 @@ int mg_setup(dp_scene* s);
 void mg_destroy(dp_scene* s);
 void mg_assemble(dp_scene* s, const double* val);
 void mg_apply(dp_scene* s, const double* val, const double* r, double* z, const int* stop);
+// the V-cycle with its fine-level first Jacobi sweep (x = omega Minv32 r into
+// the level-0 work vector) already done by the caller
+void mg_apply_prejac(dp_scene* s, const double* val, const double* r, double* z, const int* stop);
+void mg_fine_jacobi0_target(dp_scene* s, const float** minv32, double** xa, double* omega);
 int mg_levels(const dp_scene* s);
 int mg_level_rows(const dp_scene* s, int l);
 void mg_set_params(dp_scene* s, double omega, int nu);

@@ -1177,7 +1177,8 @@ __global__ void k_gm_combine(int n, int used, const double* __restrict__ y, cons
 // input buffer.
 template <typename TB>
 __global__ void k_gm_prec(int V, TB* W0, TB* W1, TB* Vb, size_t ld, const double* __restrict__ minv,
-                          double* __restrict__ z, double* __restrict__ vcopy, const GmresScalars* gs) {
+                          double* __restrict__ z, double* __restrict__ vcopy, const GmresScalars* gs,
+                          const float* __restrict__ minv32, double omega, double* __restrict__ xa) {
   if (gm_idle(gs)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= V) return;
@@ -1192,6 +1193,15 @@ __global__ void k_gm_prec(int V, TB* W0, TB* W1, TB* Vb, size_t ld, const double
     v[c] = (double)vs;
     vj[3 * i + c] = vs;
     if (vcopy) vcopy[3 * i + c] = v[c];
+  }
+  if (xa) {
+    // the V-cycle's first fine sweep from zero, x = omega Minv v (k_mg_jacobi0<float>)
+    const double r[3] = {v[0], v[1], v[2]};
+    double u[3];
+    u[0] = minv32[0 * (size_t)V + i] * r[0] + minv32[1 * (size_t)V + i] * r[1] + minv32[2 * (size_t)V + i] * r[2];
+    u[1] = minv32[3 * (size_t)V + i] * r[0] + minv32[4 * (size_t)V + i] * r[1] + minv32[5 * (size_t)V + i] * r[2];
+    u[2] = minv32[6 * (size_t)V + i] * r[0] + minv32[7 * (size_t)V + i] * r[1] + minv32[8 * (size_t)V + i] * r[2];
+    xa[3 * i] = omega * u[0]; xa[3 * i + 1] = omega * u[1]; xa[3 * i + 2] = omega * u[2];
   }
   if (minv) {
     double u[3];
@@ -1313,6 +1323,7 @@ __global__ void k_minv_axpy(int V, const double* __restrict__ minv, const double
 static const double g_reorth_thr = getenv("DP_REORTH") ? atof(getenv("DP_REORTH")) : 0.01;
 static const int g_use_graphs = getenv("DP_GRAPHS") ? atoi(getenv("DP_GRAPHS")) : 1;
 static const int g_gm_fp32 = getenv("DP_GM_FP32") ? atoi(getenv("DP_GM_FP32")) : 0;
+static const int g_prejac = getenv("DP_PREJAC") ? atoi(getenv("DP_PREJAC")) : 1;
 
 static int gm_grid(int n) {
   // one element per thread: every basis load of a thread is independent
@@ -1356,7 +1367,8 @@ static int gm_column(dp_scene* s, const double* val, int use_mg, int left, bool 
     float* Vf = reinterpret_cast<float*>(Vb);
     float* W0 = reinterpret_cast<float*>(s->kw);
     float* W1 = reinterpret_cast<float*>(s->kp);
-    k_gm_prec<float><<<grid_for(V, 256), 256, 0, s->stream>>>(V, W0, W1, Vf, ld, nullptr, z, s->tmp, s->gsc);
+    k_gm_prec<float><<<grid_for(V, 256), 256, 0, s->stream>>>(V, W0, W1, Vf, ld, nullptr, z, s->tmp, s->gsc,
+                                                               nullptr, 0.0, nullptr);
     mg_apply(s, val, s->tmp, z, &s->gsc->done);
     k_gm_spmvdot_r<float, float><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col,
                                                              s->val32, z, W0, W1, Vf, ld, s->red.partial,
@@ -1365,9 +1377,16 @@ static int gm_column(dp_scene* s, const double* val, int use_mg, int left, bool 
     k_gm_loopctl<<<1, 32, 0, s->stream>>>(s->gsc, h, use_cond);
     return k + 4;
   } else {
+    const float* m32 = nullptr;
+    double* xa = nullptr;
+    double om = 0.0;
+    if (use_mg && g_prejac) mg_fine_jacobi0_target(s, &m32, &xa, &om);
     k_gm_prec<double><<<grid_for(V, 256), 256, 0, s->stream>>>(V, s->kw, s->kp, Vb, ld, use_mg ? nullptr : s->minv,
-                                                               z, use_mg ? s->tmp : nullptr, s->gsc);
-    if (use_mg) mg_apply(s, val, s->tmp, z, &s->gsc->done);
+                                                               z, use_mg ? s->tmp : nullptr, s->gsc, m32, om, xa);
+    if (use_mg) {
+      if (xa) mg_apply_prejac(s, val, s->tmp, z, &s->gsc->done);
+      else mg_apply(s, val, s->tmp, z, &s->gsc->done);
+    }
     k_gm_spmvdot_r<double, double><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val,
                                                                z, s->kw, s->kp, Vb, ld, s->red.partial,
                                                                s->red.counter, s->gsc);

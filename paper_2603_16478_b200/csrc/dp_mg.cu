@@ -62,6 +62,7 @@ struct MG {
   int coarse_sweeps = 4;      // >0: Jacobi sweeps at the coarsest level instead of the dense inverse
   int symmetric_needed = 0;  // set while a CG solve uses the V-cycle
   int fused = 1;              // coarse levels in one cooperative kernel (k_mg_coarse_fused)
+  int prejac = 0;             // fine-level jacobi0 already applied by the caller
   int fused_grid = 0;
   size_t bytes = 0;
 };
@@ -1039,7 +1040,9 @@ static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, cons
   // pre-smoothing from zero: x = w Minv b, then nu-1 sweeps; last pass also gives r
   double* xa = L.t;   // work buffers never alias the output x
   double* xb = L.u;
-  jacobi0<TV>(s, L, minv, b, om, xa, stop);
+  // the fine-level first sweep from zero may already be done by the caller
+  // (k_gm_prec fuses it into the basis-vector pass): mg_apply(..., prejac)
+  if (!(l == 0 && mg->prejac)) jacobi0<TV>(s, L, minv, b, om, xa, stop);
   for (int it = 1; it < mg->nu; ++it) {
     smooth<TV>(s, L, val, minv, b, xa, nullptr, nullptr, om, xb, nullptr, stop, 1.0);
     std::swap(xa, xb);
@@ -1075,6 +1078,18 @@ static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, cons
 
 void mg_set_symmetric(dp_scene* s, int on) {
   if (s->mg) s->mg->symmetric_needed = on;
+}
+
+void mg_fine_jacobi0_target(dp_scene* s, const float** minv32, double** xa, double* omega) {
+  *minv32 = s->minv32;
+  *xa = s->mg->lv[0].t;
+  *omega = s->mg->omega;
+}
+
+void mg_apply_prejac(dp_scene* s, const double* val, const double* r, double* z, const int* stop) {
+  s->mg->prejac = 1;
+  mg_apply(s, val, r, z, stop);
+  s->mg->prejac = 0;
 }
 
 void mg_apply(dp_scene* s, const double* val, const double* r, double* z, const int* stop) {

@@ -280,3 +280,47 @@ def test_trunk_bindings_cables_vs_oracle(pkg):
     assert rel(g.dL_ddb, og.dL_ddb) < 1e-6
     assert abs(g.dL_dE - og.dL_dE) <= 1e-6 * abs(og.dL_dE)
     assert abs(g.dL_dmu_friction - og.dL_dmu_friction) <= 1e-6 * abs(og.dL_dmu_friction)
+
+
+def test_finger_scene_vs_oracle(pkg):
+    """The C5 workload family at 6^3 cells: NH cube on a mu=0.5 ground,
+    squeezed by two kinematic sphere fingers that move every step (colliders
+    re-read per step, contact.py:125-127).  States, contact sets (incl.
+    finger contacts), dL/dq_bar, dL/dE and dL/dmu against the oracle."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import diffproj_oracle as O
+    from paper_2603_16478_b200 import adjoint as aj, core, forward as fw
+    scene = bench.make_scene(6, fingers=True)
+    sm = core.assemble_system_matrix(scene)
+    osc = O.OScene(core.scene_to_arrays(scene))
+    els = O.build_elements(osc)
+    A = O.assemble_A(osc, els)
+    st = scene.rest_state()
+    q, v = st.q.copy(), st.v.copy()
+    caches, steps = [], []
+    finger_contacts = 0
+    for k in range(4):
+        bench.move_fingers(scene, k)
+        osc = O.OScene(core.scene_to_arrays(scene))
+        st, rep = fw.forward_step(scene, st, sm, fw.ForwardConfig(tol=1e-12))
+        assert rep.converged
+        o = O.forward_step(osc, A, els, q, v, O.ForwardConfig(tol=1e-12))
+        assert o.converged
+        assert np.max(np.abs(st.q - o.q_new)) <= 1e-8 * np.max(np.abs(o.q_new))
+        assert np.array_equal([cp.vertex for cp in rep.cache.contacts], o.contacts.vertex)
+        assert np.array_equal([cp.collider for cp in rep.cache.contacts], o.contacts.collider)
+        finger_contacts += int(np.sum(o.contacts.collider > 0))
+        q, v = o.q_new, o.v_new
+        caches.append(rep.cache)
+        steps.append(o)
+    assert finger_contacts > 0
+    target = st.q + 1e-3
+    g = aj.backprop_rollout(caches, target)
+    og = O.backprop_rollout(osc, els, A, steps, target=target)
+    rel = lambda a, b: np.max(np.abs(a - b)) / np.max(np.abs(b))
+    assert rel(g.dL_dqbar, og.dL_dqbar) < 1e-6
+    assert abs(g.dL_dE - og.dL_dE) <= 1e-6 * abs(og.dL_dE)
+    assert abs(g.dL_dmu_friction - og.dL_dmu_friction) <= 1e-6 * abs(og.dL_dmu_friction)

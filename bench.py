@@ -72,7 +72,7 @@ _keep_heap()
 #    solver-path-dependent gradients (measured 7e-6 relative in dL/dE); 1e-11
 #    makes the C5 root path-independent (dL/dE agrees to 1e-9 across paths).
 CONFIGS = {
-    "c5": dict(cells=(55, 55, 55), edge=0.1 / 55, fingers=True, eps_fb=1e-9, tol=1e-11, rollouts=1,
+    "c5": dict(cells=(55, 55, 55), edge=0.1 / 55, fingers=True, eps_fb=1e-9, tol=1e-11, rollouts=1, vary="target",
                desc="1M-tet NH cube gripped by 2 kinematic sphere fingers on a frictional ground (C5)"),
     "c3": dict(cells=(60, 12, 12), edge=0.01, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=8,
                desc="identification batch: 8 rollouts/GPU of a 51,840-tet NH beam on a frictional ground, "
@@ -280,7 +280,16 @@ def gpu_arm(args, rank, world, local_rank):
     for i in range(R):
         c = Ctx()
         c.slot = i
-        c.E = E_YOUNG * (1 + 0.05 * (rank * R + i))
+        g_idx = rank * R + i
+        if cdef.get("vary", "E") == "E":
+            c.E = E_YOUNG * (1 + 0.05 * g_idx)
+            c.target_shift = 1e-3
+        else:
+            # same material on every rank, a different synthetic target per
+            # rollout (C5: E candidates move the scene into the reference
+            # model's friction-rotation stall within 6 steps)
+            c.E = E_YOUNG
+            c.target_shift = 1e-3 * (1 + 0.1 * g_idx)
         c.scene = make_scene(args.config, E=c.E)
         c.sysmat = core.assemble_system_matrix(c.scene, device=local_rank)
         c.dev = c.sysmat.dev
@@ -314,7 +323,7 @@ def gpu_arm(args, rank, world, local_rank):
             caches.append(rep.cache)
             stats.append((rep.converged, rep.iterations, rep.krylov_iterations, rep.n_contacts))
         with torch.cuda.stream(c.stream):
-            target = q[0] + 1e-3          # synthetic target shape
+            target = q[0] + c.target_shift   # synthetic target shape
             dq = 2.0 * (q[nsteps] - target)
             dv = torch.zeros(n3, **dd)
             z = torch.empty(n3, **dd)
@@ -357,7 +366,7 @@ def gpu_arm(args, rank, world, local_rank):
             move_fingers(scene, k0 + k)
             st, rep = fw.forward_step(scene, st, c.sysmat, cfg)
             caches.append(rep.cache)
-        target = st0.q + 1e-3
+        target = st0.q + c.target_shift
         g = aj.backprop_rollout(caches, target)
         return g, float(np.sum((st.q - target) ** 2))
 
@@ -562,6 +571,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(1)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional smoke test of the N>1 code path on a 1-GPU box only (gloo,
+    # every rank on cuda:0; never a measurement): BENCH_SMOKE_SHARED_GPU=1
+    if os.environ.get("BENCH_SMOKE_SHARED_GPU"):
+        local_rank = 0
     cdef = CONFIGS[args.config]
     R = args.rollouts or cdef["rollouts"]
     nx, ny, nz = cdef["cells"]
@@ -571,7 +584,9 @@ def main():
               "n_verts": (nx + 1) * (ny + 1) * (nz + 1 if not cloth else 1), "steps_per_rollout": args.steps,
               "rollouts_per_gpu": R, "rollouts": world * R,
               "parallelism": f"dp{world} x {R} rollouts/GPU (independent rollouts, NCCL grad allreduce)",
-              "material": ("arap stiffness=50" if cloth else f"neohookean E={E_YOUNG}(1+0.05 i) nu={NU}"),
+              "material": ("arap stiffness=50" if cloth else
+                           (f"neohookean E={E_YOUNG}(1+0.05 i) nu={NU}" if cdef.get("vary", "E") == "E" else
+                            f"neohookean E={E_YOUNG} nu={NU}, target shift 1e-3 (1 + 0.1 i) per rollout i")),
               "friction_mu": 0.3 if (cloth or cdef.get("trunk")) else MU, "h": 0.01,
               "eps_fb": cdef["eps_fb"], "newton_tol": cdef["tol"], "l2": "operands > L2 (no flush)"}
     if args.impl == "reference":
@@ -595,7 +610,7 @@ def main():
 
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if os.environ.get("BENCH_SMOKE_SHARED_GPU") else "nccl")
     r = gpu_arm(args, rank, world, local_rank)
     if rank == 0:
         K = args.steps

@@ -20,7 +20,7 @@ st = sc.rest_state()
 cfg = fw.ForwardConfig(tol=c["tol"], lin_rtol_max=rmax, lin_rtol_min=rmin)
 T0 = time.time()
 for k in range(steps):
-    bench.move_fingers(sc, k)
+    bench.move_fingers(sc, k + int(os.environ.get("K0", "0")))
     t0 = time.time()
     print(f"=== step {k}", file=sys.stderr, flush=True)
     st, rep = fw.forward_step(sc, st, sm, cfg)

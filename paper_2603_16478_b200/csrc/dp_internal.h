@@ -39,6 +39,14 @@ struct KrylovScalars {
 
 // GMRES restart cap: the default cycle is 50; solves that stagnate escalate
 // to longer cycles (indefinite Newton matrices of compressed cloth).
+// FP32 fine-level operator copy: 1 = slot-major, 12 floats per slot (three
+// float4 loads per block), 0 = component-major like the FP64 values (nine
+// coalesced 128 B loads per warp and block, no padding)
+#ifndef DP_VAL32_PACKED
+#define DP_VAL32_PACKED 0
+#endif
+constexpr int kVal32PerSlot = DP_VAL32_PACKED ? 12 : 9;
+
 constexpr int kMaxRestart = 200;
 struct GmresScalars {
   double wn2_before;                            // |w|^2 before orthogonalisation

@@ -482,10 +482,16 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
       // FP32 copy for the multigrid smoother: 12 floats per slot (9 + pad),
       // slot-major, so a lane reads its block as three 16-byte loads and a
       // warp reads 1.5 KB contiguous
+#if DP_VAL32_PACKED
       float4* v4 = reinterpret_cast<float4*>(val32 + (size_t)slot * 12);
       v4[0] = make_float4((float)b[0], (float)b[1], (float)b[2], (float)b[3]);
       v4[1] = make_float4((float)b[4], (float)b[5], (float)b[6], (float)b[7]);
       v4[2] = make_float4((float)b[8], 0.f, 0.f, 0.f);
+#else
+      float* v32 = val32 + (size_t)base * 9;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) v32[(k * 9 + c) * kSlice + lane] = (float)b[c];
+#endif
     }
   }
 }
@@ -1220,8 +1226,9 @@ __device__ __forceinline__ void spmv_row32(int slice, int lane, const int* __res
   const int base = slice_base[slice];
   const int K = slice_width[slice];
   const int* cs = col + base + lane;
-  const float4* p4 = reinterpret_cast<const float4*>(val) + (size_t)(base + lane) * 3;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#if DP_VAL32_PACKED
+  const float4* p4 = reinterpret_cast<const float4*>(val) + (size_t)(base + lane) * 3;
 #pragma unroll 2
   for (int k = 0; k < K; ++k) {
     const int j = __ldg(cs + k * kSlice);
@@ -1232,6 +1239,18 @@ __device__ __forceinline__ void spmv_row32(int slice, int lane, const int* __res
     a1 += (double)q0.w * x0 + (double)q1.x * x1 + (double)q1.y * x2;
     a2 += (double)q1.z * x0 + (double)q1.w * x1 + (double)q2.x * x2;
   }
+#else
+  const float* vs = val + (size_t)base * 9 + lane;
+#pragma unroll 2
+  for (int k = 0; k < K; ++k) {
+    const int j = __ldg(cs + k * kSlice);
+    const float* v = vs + k * 9 * kSlice;
+    const double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
+    a0 += (double)__ldcs(v + 0 * kSlice) * x0 + (double)__ldcs(v + 1 * kSlice) * x1 + (double)__ldcs(v + 2 * kSlice) * x2;
+    a1 += (double)__ldcs(v + 3 * kSlice) * x0 + (double)__ldcs(v + 4 * kSlice) * x1 + (double)__ldcs(v + 5 * kSlice) * x2;
+    a2 += (double)__ldcs(v + 6 * kSlice) * x0 + (double)__ldcs(v + 7 * kSlice) * x1 + (double)__ldcs(v + 8 * kSlice) * x2;
+  }
+#endif
   y[0] = a0; y[1] = a1; y[2] = a2;
 }
 

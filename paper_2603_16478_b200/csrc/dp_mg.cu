@@ -179,7 +179,7 @@ int mg_setup(dp_scene* s) {
   // mixed-precision preconditioner: the fine-level V-cycle reads FP32 copies
   // of the operator (written by k_assemble); the Krylov method itself runs on
   // the FP64 operator, so the solution accuracy is unaffected
-  rc |= al(mg, &s->val32, (size_t)s->NS * 12);   // packed 12 floats per slot (float4 x 3)
+  rc |= al(mg, &s->val32, (size_t)s->NS * kVal32PerSlot);
   rc |= al(mg, &s->minv32, (size_t)s->V * 9);
   rc |= al(mg, &L0.x, (size_t)3 * s->V);
   rc |= al(mg, &L0.r, (size_t)3 * s->V);
@@ -197,10 +197,10 @@ int mg_setup(dp_scene* s) {
     }
   }
   HostPattern cur = fine;
-  // level 1 gathers from the packed FP32 fine copy: address = slot * 12
+  // level 1 gathers from the FP32 fine copy (DP_VAL32_PACKED: slot * 12,
+  // else the FP64 layout's component-major addresses)
   std::vector<int64_t> cur_addr(s->nnzb);
-  for (int64_t k = 0; k < s->nnzb; ++k) cur_addr[k] = s->h_block_slot[k] * 12;
-  (void)fine_addr;
+  for (int64_t k = 0; k < s->nnzb; ++k) cur_addr[k] = DP_VAL32_PACKED ? s->h_block_slot[k] * 12 : fine_addr[k];
   while (cur.n > kCoarseMax && !rc) {
     std::vector<int> agg;
     const int na = aggregate(cur, agg);
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
   for (int k = wsub; k < K; k += SPLIT) {
     const int j = __ldg(cs + k * kSlice);
     double m[9];
-    if (sizeof(TV) == 4) {
+    if (sizeof(TV) == 4 && DP_VAL32_PACKED) {
       // packed FP32 fine level: 3 x 16-byte loads per block
       const float4* p4 = reinterpret_cast<const float4*>(val) + (size_t)(base + k * kSlice + lane) * 3;
       const float4 q0 = __ldg(p4), q1 = __ldg(p4 + 1), q2 = __ldg(p4 + 2);
@@ -919,7 +919,7 @@ void mg_assemble(dp_scene* s, const double* val) {
   for (size_t l = 1; l < mg->lv.size(); ++l) {
     MGLevel& L = mg->lv[l];
     if (l == 1)
-      k_mg_galerkin<float, 1><<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
+      k_mg_galerkin<float, DP_VAL32_PACKED ? 1 : kSlice><<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
           L.n, L.S, L.slice_base, L.slice_width, L.diag_slot, L.gal_ptr, L.gal, s->val32, L.val, L.minv, L.slot_row,
           L.NS);
     else

@@ -24,6 +24,9 @@
 #ifndef DP_ELEM_MINB
 #define DP_ELEM_MINB 4
 #endif
+#ifndef DP_JAC_SMEM
+#define DP_JAC_SMEM 1
+#endif
 
 namespace dp {
 
@@ -238,6 +241,97 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
           o[18 + i * 3 + c] = s2;
         }
     }
+  }
+  if ((mode & EV_JAC) && !(mode & EV_AMAT) && DP_JAC_SMEM) {
+    // Block phase through shared memory: the projection's registers are dead
+    // here, and the Jacobian data (J, alpha) is re-read from this thread's
+    // shared-memory row one block at a time instead of being held live
+    // across the ten unrolled blocks (which spilled at the 128-register cap).
+    // Same arithmetic, term by term, as the register path below.
+    constexpr int NOOP = (D == 2) ? 2 : 0;
+    constexpr int NJ = 9 + D * D + 3 + 3 + NOOP + NV * D + NP;
+    __shared__ double jsm[128][NJ];
+    volatile double* js = jsm[threadIdx.x];
+    {
+      ElemJac<D> J;
+      make_jac<D>(U, sig, th, W, tau_rel, J);
+      int f = 0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) js[f++] = J.U3[i][k];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int k = 0; k < D; ++k) js[f++] = J.W[i][k];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) js[f++] = J.m[i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) js[f++] = J.n[i];
+      if (NOOP) {
+        js[f++] = J.oop[0];
+        js[f++] = J.oop[1];
+      }
+#pragma unroll
+      for (int a = 0; a < NV; ++a)
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < D; ++c) s += V[c][k] * beta[a][c];
+          js[f++] = s;
+        }
+#pragma unroll
+      for (int a = 0; a < NV; ++a)
+#pragma unroll
+        for (int b = a; b < NV; ++b) {
+          double bb = 0.0;
+#pragma unroll
+          for (int c = 0; c < D; ++c) bb += beta[a][c] * beta[b][c];
+          js[f++] = bb;
+        }
+    }
+    double* Ho = H + (size_t)e * NP * 9;
+    int p = 0;
+    constexpr int FA = 9 + D * D + 3 + 3 + NOOP;
+    constexpr int FB = FA + NV * D;
+#pragma unroll 1
+    for (int a = 0; a < NV; ++a) {
+#pragma unroll 1
+      for (int b = a; b < NV; ++b, ++p) {
+        ElemJac<D> J;
+        int f = 0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) J.U3[i][k] = js[f++];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int k = 0; k < D; ++k) J.W[i][k] = js[f++];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) J.m[i] = js[f++];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) J.n[i] = js[f++];
+        if (NOOP) {
+          J.oop[0] = js[f++];
+          J.oop[1] = js[f++];
+        } else {
+          J.oop[0] = J.oop[1] = 0.0;
+        }
+        double aa[D], ab[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) { aa[k] = js[FA + a * D + k]; ab[k] = js[FA + b * D + k]; }
+        const double bb = js[FB + p];
+        double blk[3][3];
+        jac_block<D>(J, aa, ab, blk);
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) Ho[p * 9 + i * 3 + j] = hw * (((i == j) ? bb : 0.0) - blk[i][j]);
+      }
+    }
+    return;
   }
   if (mode & EV_JAC) {
     ElemJac<D> J;

@@ -499,7 +499,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   rc |= dalloc(s, &s->val_adj, (size_t)NS * 9);
   rc |= dalloc(s, &s->minv, (size_t)V * 9);
   rc |= dalloc(s, &s->fe, (size_t)std::max(E, 1) * NV * 3);
-  rc |= dalloc(s, &s->H, (size_t)std::max(E, 1) * NP * 9);
+  rc |= dalloc(s, &s->H, (size_t)std::max(E, 1) * NP * kHBlk);
   rc |= dalloc(s, &s->Pst, (size_t)std::max(E, 1) * 27);
   rc |= dalloc(s, &s->d_colliders, 1);
   rc |= dalloc(s, &s->fext, (size_t)V * 3);

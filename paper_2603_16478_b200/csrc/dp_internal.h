@@ -47,6 +47,11 @@ struct KrylovScalars {
 #endif
 constexpr int kVal32PerSlot = DP_VAL32_PACKED ? 12 : 9;
 
+// element Hessian blocks: 9 doubles padded to 10 (80 B, 16-byte aligned):
+// five 16-byte stores per block in the element kernel, and every block read by
+// the assembly gather covers exactly three 32-byte sectors
+constexpr int kHBlk = 10;
+
 constexpr int kMaxRestart = 200;
 struct GmresScalars {
   double wn2_before;                            // |w|^2 before orthogonalisation

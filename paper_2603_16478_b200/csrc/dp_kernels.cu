@@ -131,6 +131,19 @@ __device__ __forceinline__ void make_jac(const double U[3][D], const double sig[
   }
 }
 
+// h^2 w [(beta_a.beta_b) I - blk] as one padded 80-byte block, 16-byte stores
+__device__ __forceinline__ void store_hblock(double* o, double hw, double bb, const double blk[3][3]) {
+  double v[kHBlk];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) v[i * 3 + j] = hw * (((i == j) ? bb : 0.0) - blk[i][j]);
+  v[9] = 0.0;
+  double2* o2 = reinterpret_cast<double2*>(o);
+#pragma unroll
+  for (int t = 0; t < kHBlk / 2; ++t) o2[t] = make_double2(v[2 * t], v[2 * t + 1]);
+}
+
 // One thread per element.  NV = vertices per element (4 tet, 3 tri).  The
 // mode is a template parameter: the residual-only instantiation (line-search
 // trials) does not carry the Jacobian path's registers (168 -> fewer), so it
@@ -291,7 +304,7 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
           js[f++] = bb;
         }
     }
-    double* Ho = H + (size_t)e * NP * 9;
+    double* Ho = H + (size_t)e * NP * kHBlk;
     int p = 0;
     constexpr int FA = 9 + D * D + 3 + 3 + NOOP;
     constexpr int FB = FA + NV * D;
@@ -325,10 +338,7 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
         const double bb = js[FB + p];
         double blk[3][3];
         jac_block<D>(J, aa, ab, blk);
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int j = 0; j < 3; ++j) Ho[p * 9 + i * 3 + j] = hw * (((i == j) ? bb : 0.0) - blk[i][j]);
+        store_hblock(Ho + p * kHBlk, hw, bb, blk);
       }
     }
     return;
@@ -349,7 +359,7 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
           alpha[a][k] = s;
         }
     }
-    double* Ho = H + (size_t)e * NP * 9;
+    double* Ho = H + (size_t)e * NP * kHBlk;
     int p = 0;
 #pragma unroll
     for (int a = 0; a < NV; ++a)
@@ -367,10 +377,7 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
         } else {
           jac_block<D>(J, alpha[a], alpha[b], blk);
         }
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int j = 0; j < 3; ++j) Ho[p * 9 + i * 3 + j] = hw * (((i == j) ? bb : 0.0) - blk[i][j]);
+        store_hblock(Ho + p * kHBlk, hw, bb, blk);
       }
   }
 }
@@ -532,12 +539,18 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
     const int t0 = contrib_ptr[slot], t1 = contrib_ptr[slot + 1];
     for (int t = t0; t < t1; ++t) {
       const int cid = contrib[t];
+      const double2* src2 = reinterpret_cast<const double2*>(H + (size_t)(cid >= 0 ? cid : ~cid) * kHBlk);
+      double src[kHBlk];
+#pragma unroll
+      for (int u = 0; u < kHBlk / 2; ++u) {
+        const double2 d2 = src2[u];
+        src[2 * u] = d2.x;
+        src[2 * u + 1] = d2.y;
+      }
       if (cid >= 0) {
-        const double* src = H + (size_t)cid * 9;
 #pragma unroll
         for (int c = 0; c < 9; ++c) b[c] += src[c];
       } else {
-        const double* src = H + (size_t)(~cid) * 9;
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll

@@ -131,6 +131,33 @@ __device__ __forceinline__ void make_jac(const double U[3][D], const double sig[
   }
 }
 
+#ifndef ASM_CHUNK
+#define ASM_CHUNK 4
+#endif
+
+__device__ __forceinline__ void load_hblock(const double* __restrict__ H, int cid, double src[kHBlk]) {
+  const double2* src2 = reinterpret_cast<const double2*>(H + (size_t)(cid >= 0 ? cid : ~cid) * kHBlk);
+#pragma unroll
+  for (int u = 0; u < kHBlk / 2; ++u) {
+    const double2 d2 = src2[u];
+    src[2 * u] = d2.x;
+    src[2 * u + 1] = d2.y;
+  }
+}
+
+// b += block (or its transpose for a > b pairs stored as (b, a))
+__device__ __forceinline__ void acc_hblock(double b[9], const double src[kHBlk], bool direct) {
+  if (direct) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) b[c] += src[c];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) b[i * 3 + j] += src[j * 3 + i];
+  }
+}
+
 // h^2 w [(beta_a.beta_b) I - blk] as one padded 80-byte block, 16-byte stores
 __device__ __forceinline__ void store_hblock(double* o, double hw, double bb, const double blk[3][3]) {
   double v[kHBlk];
@@ -537,25 +564,24 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
 #pragma unroll
     for (int c = 0; c < 9; ++c) b[c] = 0.0;
     const int t0 = contrib_ptr[slot], t1 = contrib_ptr[slot + 1];
-    for (int t = t0; t < t1; ++t) {
+    // contributions in groups of ASM_CHUNK: all index and block loads of a
+    // group are issued before the (in-order) accumulation
+    int t = t0;
+    for (; t + ASM_CHUNK <= t1; t += ASM_CHUNK) {
+      int cid[ASM_CHUNK];
+      double src[ASM_CHUNK][kHBlk];
+#pragma unroll
+      for (int g = 0; g < ASM_CHUNK; ++g) cid[g] = contrib[t + g];
+#pragma unroll
+      for (int g = 0; g < ASM_CHUNK; ++g) load_hblock(H, cid[g], src[g]);
+#pragma unroll
+      for (int g = 0; g < ASM_CHUNK; ++g) acc_hblock(b, src[g], cid[g] >= 0);
+    }
+    for (; t < t1; ++t) {
       const int cid = contrib[t];
-      const double2* src2 = reinterpret_cast<const double2*>(H + (size_t)(cid >= 0 ? cid : ~cid) * kHBlk);
       double src[kHBlk];
-#pragma unroll
-      for (int u = 0; u < kHBlk / 2; ++u) {
-        const double2 d2 = src2[u];
-        src[2 * u] = d2.x;
-        src[2 * u + 1] = d2.y;
-      }
-      if (cid >= 0) {
-#pragma unroll
-        for (int c = 0; c < 9; ++c) b[c] += src[c];
-      } else {
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int j = 0; j < 3; ++j) b[i * 3 + j] += src[j * 3 + i];
-      }
+      load_hblock(H, cid, src);
+      acc_hblock(b, src, cid >= 0);
     }
     if (slot == dslot) {
       const double m = mass[row];

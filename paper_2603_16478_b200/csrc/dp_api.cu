@@ -254,6 +254,8 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   DP_CUDA(cudaSetDevice(d->device));
   dp_scene* s = new dp_scene();
   s->device = d->device;
+  cudaDeviceGetAttribute(&s->nsm, cudaDevAttrMultiProcessorCount, d->device);
+  if (s->nsm <= 0) s->nsm = 148;
   s->V = d->n_verts;
   s->E = d->n_elems;
   s->NV = d->verts_per_elem;

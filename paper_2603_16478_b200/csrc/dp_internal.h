@@ -119,6 +119,7 @@ struct dp_cache {
 
 struct dp_scene {
   int device = 0;
+  int nsm = 148;                  // SMs of the device (grid sizing)
   cudaStream_t stream = nullptr;
   int V = 0, E = 0, NV = 4, D = 3, NP = 10;
   double h = 0.01, eps_fb = 1e-6, act = 1e-3, grav[3] = {0, 0, -9.8};

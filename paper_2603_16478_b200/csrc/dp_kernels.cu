@@ -14,6 +14,7 @@
 // list of (element, local block, transposed?) contributions.
 #include <cuda_runtime.h>
 #include <stddef.h>
+#include <algorithm>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -1477,10 +1478,12 @@ static const int g_use_graphs = getenv("DP_GRAPHS") ? atoi(getenv("DP_GRAPHS")) 
 static const int g_gm_fp32 = getenv("DP_GM_FP32") ? atoi(getenv("DP_GM_FP32")) : 0;
 static const int g_prejac = getenv("DP_PREJAC") ? atoi(getenv("DP_PREJAC")) : 1;
 
-static int gm_grid(int n) {
-  // one element per thread: every basis load of a thread is independent
-  // (MLP = j+1), and enough CTAs to cover HBM latency
-  return grid_for(n, kGT);
+static int gm_grid(const dp_scene* s, int n) {
+  // grid-stride over the basis rows with 4 CTAs per SM: every basis load of
+  // a thread is independent (MLP = j+1), and the per-CTA fixed cost (coefficient
+  // staging, block reduction, completion ticket) is paid 592 times instead of
+  // once per 256 rows (measured: k_gm_update 18.6 -> 12.7 us at C5)
+  return std::min(grid_for(n, kGT), 4 * s->nsm);
 }
 
 __global__ void k_gm_copy_wnew(int n, const double* __restrict__ src, double* W0, double* W1,
@@ -1497,7 +1500,7 @@ static int gm_column(dp_scene* s, const double* val, int use_mg, int left, bool 
   const int V = s->V, n = 3 * V;
   const size_t ld = (size_t)n;
   const int nbs = grid_for((int64_t)s->S * 32, 256);
-  const int nbg = gm_grid(n);
+  const int nbg = gm_grid(s, n);
   double* Vb = s->gm_V;
   double* z = s->ku;
   int k = 0;
@@ -1635,7 +1638,7 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   if (restart < 1) restart = 1;
   const size_t ld = (size_t)n;
   const int nbv = grid_for(V, kVT);
-  const int nbg = gm_grid(n);
+  const int nbg = gm_grid(s, n);
   double* Vb = s->gm_V;
   double* r = s->kr;
   double* z = s->ku;       // M^-1 v_j

@@ -462,7 +462,24 @@ __global__ void __launch_bounds__(kVT) k_residual(int V, const double* __restric
     double r0 = m * (q[3 * i] - q_hat[3 * i]);
     double r1 = m * (q[3 * i + 1] - q_hat[3 * i + 1]);
     double r2 = m * (q[3 * i + 2] - q_hat[3 * i + 2]);
-    for (int k = inc_ptr[i]; k < inc_ptr[i + 1]; ++k) {
+    // element contributions in groups of 4 (all loads of a group in flight
+    // before the in-order accumulation)
+    int k = inc_ptr[i];
+    const int k1 = inc_ptr[i + 1];
+    for (; k + 4 <= k1; k += 4) {
+      int id[4];
+      double f[4][3];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) id[g] = inc[k + g];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const double* fp = fe + (size_t)id[g] * 3;
+        f[g][0] = fp[0]; f[g][1] = fp[1]; f[g][2] = fp[2];
+      }
+#pragma unroll
+      for (int g = 0; g < 4; ++g) { r0 += f[g][0]; r1 += f[g][1]; r2 += f[g][2]; }
+    }
+    for (; k < k1; ++k) {
       const double* f = fe + (size_t)inc[k] * 3;
       r0 += f[0]; r1 += f[1]; r2 += f[2];
     }

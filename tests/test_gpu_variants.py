@@ -1,0 +1,29 @@
+"""Solver-plumbing switches that must not change a single bit (DESIGN.md
+§6b): host-driven GMRES columns instead of CUDA-graph WHILE nodes, the fused
+cooperative coarse V-cycle, and the un-fused first fine Jacobi sweep.  Each
+variant runs in its own process (the switches are read when the library
+loads) on the same C5-family rollout, forward and reverse."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _digest(env_extra):
+    env = dict(os.environ)
+    env.update(env_extra)
+    out = subprocess.run([sys.executable, os.path.join(HERE, "_variant_run.py")], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("DIGEST")][-1]
+    return line.split()[1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [{"DP_GRAPHS": "0"}, {"DP_MG_FUSED": "1"}, {"DP_PREJAC": "0"}],
+                         ids=["host-driven-gmres", "fused-coarse-vcycle", "unfused-jacobi0"])
+def test_variant_bitwise_identical(variant):
+    assert _digest(variant) == _digest({})

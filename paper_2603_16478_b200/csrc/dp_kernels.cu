@@ -1673,7 +1673,11 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
     *relres = 0.0;
     return 0;
   }
-  if (use_x0 && true_relres(s, val, b, x, s->kr, bnorm) >= 1.0) cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+  bool x_zero = !use_x0;
+  if (use_x0 && true_relres(s, val, b, x, s->kr, bnorm) >= 1.0) {
+    cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+    x_zero = true;
+  }
   // nmb = |b| (right) or |M^-1 b| (left, the reference's normalisation)
   if (left && use_mg) {
     mg_apply(s, val, b, z, nullptr);
@@ -1689,8 +1693,18 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   double rel = 1.0;
   int m = restart;   // cycle length; grows when a cycle stagnates
   const int m_cap = std::min(kMaxRestart, n);
+  bool have_rel = false;   // r and rel already hold b - A x (end of the previous cycle)
   while (total < max_iter) {
-    rel = true_relres(s, val, b, x, r, bnorm);
+    if (!have_rel) {
+      if (x_zero) {
+        // x = 0: r = b exactly, no SpMV
+        cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s->stream);
+        rel = 1.0;
+      } else {
+        rel = true_relres(s, val, b, x, r, bnorm);
+      }
+    }
+    have_rel = false;
     if (rel <= rtol) break;
     const double cycle_start = rel;
     const int budget = max_iter - total;
@@ -1752,6 +1766,7 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
       s->launches += 2;
     }
     rel = true_relres(s, val, b, x, r, bnorm);
+    have_rel = true;
     if (rel <= rtol) break;
     if (used == 0) break;
     // a cycle that gains less than min_cycle_gain (inexact Newton use), or

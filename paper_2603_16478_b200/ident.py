@@ -1,14 +1,18 @@
-"""Callers of the hot path: procedural meshes, the identification loss and
-its finite-difference check (the parts of diffproj.ident that drive
-``rollout``/``backprop_rollout``; reference ident.py:81-216, :320-453).
+"""Callers of the hot path: procedural meshes, the identification loss, its
+finite-difference check, the gradient-descent driver and its convergence
+metrics (the parts of diffproj.ident that drive ``rollout`` /
+``backprop_rollout``; reference ident.py:81-316, :320-453).
 
-Kept on the host; only used to build synthetic workloads and to exercise
-the drop-in API the way the reference's own harness does.
+Host-side Python like the reference.  The finite-difference gradient runs
+its 2 x n_params perturbed rollouts concurrently, one scene (CUDA stream)
+and host thread each; every rollout is independent,
+so the result is bitwise the sequential one.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -190,8 +194,16 @@ class OptProblem:
     fd_eta: float = 1e-4
     initial_velocity: np.ndarray | None = None
 
+    def __post_init__(self):
+        # ident.py:119-124
+        if self.learning_rate <= 0:
+            raise ValueError("learning_rate must be positive")
+        self.names()
+
     def names(self):
         names = [v.strip() for v in str(self.variable).split(",") if v.strip()]
+        if not names:
+            raise ValueError("empty variable list")
         for n in names:
             if n not in VARIABLES:
                 raise ValueError(f"unknown variable {n!r}; known: {sorted(VARIABLES)}")
@@ -208,13 +220,19 @@ def _prepared(problem, x):
     if problem.initial_velocity is not None:
         state0.v[:] = problem.initial_velocity
     xv = np.atleast_1d(np.asarray(x, dtype=np.float64))
-    for name, xi in zip(problem.names(), xv):
+    names = problem.names()
+    if xv.size != len(names):
+        raise ValueError(f"expected {len(names)} parameter values, got {xv.size}")
+    for name, xi in zip(names, xv):
         VARIABLES[name][0](scene, state0, xi)
     return scene, state0
 
 
 def resolve_target(problem, cfg=None):
+    """Self-generate the target trajectory at target_value (ident.py:178-186)."""
     if problem.target_state is None:
+        if problem.target_value is None:
+            raise ValueError("either target_state or target_value required")
         scene, state0 = _prepared(problem, problem.target_value)
         states, _ = fw.rollout(scene, state0, problem.horizon, cfg=cfg)
         problem.target_state = states[-1].q.copy()
@@ -233,12 +251,122 @@ def rollout_loss(problem, x, with_grad=False, cfg=None):
     return L, (float(g[0]) if problem.scalar else g)
 
 
-def fd_gradient(problem, x, eta=None, cfg=None):
+def fd_gradient(problem, x, eta=None, cfg=None, workers=None):
+    """Central finite difference of the rollout loss per component
+    (ident.py:202-216).  The 2 n perturbed rollouts run concurrently
+    (``workers`` host threads, each rollout on its own scene stream)."""
+    if eta is not None and eta <= 0:
+        raise ValueError("eta must be positive")
     xv = np.atleast_1d(np.asarray(x, dtype=np.float64))
-    g = np.empty(xv.size)
+    resolve_target(problem, cfg)          # once, before the threads start
+    steps = []
     for i in range(xv.size):
         e = eta if eta is not None else problem.fd_eta * max(abs(xv[i]), 1.0)
         d = np.zeros(xv.size)
         d[i] = e
-        g[i] = (rollout_loss(problem, xv + d, cfg=cfg) - rollout_loss(problem, xv - d, cfg=cfg)) / (2 * e)
+        steps.append((e, xv + d, xv - d))
+    pts = [p for _, xp, xm in steps for p in (xp, xm)]
+    nw = workers if workers is not None else min(len(pts), 8)
+    if nw <= 1:
+        losses = [rollout_loss(problem, p, cfg=cfg) for p in pts]
+    else:
+        with ThreadPoolExecutor(max_workers=nw) as ex:
+            losses = list(ex.map(lambda p: rollout_loss(problem, p, cfg=cfg), pts))
+    g = np.array([(losses[2 * i] - losses[2 * i + 1]) / (2 * e) for i, (e, _, _) in enumerate(steps)])
     return float(g[0]) if problem.scalar else g
+
+
+@dataclass
+class OptTrace:
+    """ident.py:141-147."""
+    losses: list = field(default_factory=list)
+    params: list = field(default_factory=list)
+    grads_ana: list = field(default_factory=list)
+    grads_fd: list = field(default_factory=list)   # None where not computed
+    diverged: bool = False
+
+
+@dataclass
+class MetricsReport:
+    """ident.py:150-159."""
+    t50: float
+    t90: float
+    auc_e: float
+    auc_m: float
+    auc_l: float
+    mre_e: float
+    mre_m: float
+    mre_l: float
+    degenerate: bool = False
+
+
+def optimize(problem, use_fd=False, cfg=None):
+    """Plain gradient descent, optionally in log-space, with a trace
+    (ident.py:219-261).  A forward/adjoint failure (ValueError /
+    RuntimeError) ends the run and marks the trace diverged."""
+    x = np.atleast_1d(np.asarray(problem.init_value, dtype=np.float64)).copy()
+    scalar = problem.scalar
+
+    def unwrap(v):
+        v = np.atleast_1d(np.asarray(v, dtype=np.float64))
+        return float(v[0]) if scalar else v.copy()
+
+    trace = OptTrace()
+    for it in range(problem.iterations):
+        try:
+            if use_fd:
+                L = rollout_loss(problem, x, cfg=cfg)
+                g = fd_gradient(problem, x, cfg=cfg)
+            else:
+                L, g = rollout_loss(problem, x, with_grad=True, cfg=cfg)
+            g_fd = None
+            if problem.fd_every and it % problem.fd_every == 0:
+                g_fd = fd_gradient(problem, x, cfg=cfg)
+        except (RuntimeError, ValueError):
+            trace.diverged = True
+            break
+        g = np.atleast_1d(np.asarray(g, dtype=np.float64))
+        trace.losses.append(L)
+        trace.params.append(unwrap(x))
+        trace.grads_ana.append(unwrap(g))
+        trace.grads_fd.append(None if g_fd is None else unwrap(g_fd))
+        if not np.isfinite(L) or not np.all(np.isfinite(g)):
+            trace.diverged = True
+            break
+        if problem.log_space:
+            x = np.exp(np.log(x) - problem.learning_rate * g * x)
+        else:
+            x = x - problem.learning_rate * g
+    return trace
+
+
+def metrics(trace, eps_g=1e-12):
+    """Stage-wise convergence metrics of a trace (ident.py:264-316): t_p =
+    first iteration fraction reaching p of the total loss reduction; AUC =
+    stage mean of the normalised remaining loss; MRE = stage mean of the
+    relative analytic-vs-FD gradient error where an FD gradient exists."""
+    L = np.asarray(trace.losses, dtype=np.float64)
+    if L.size == 0:
+        raise ValueError("empty trace")
+    T = L.size - 1
+    total = L[0] - L[-1]
+    if T == 0 or total <= 0:
+        return MetricsReport(t50=1.0, t90=1.0, auc_e=0.0, auc_m=0.0, auc_l=0.0,
+                             mre_e=0.0, mre_m=0.0, mre_l=0.0, degenerate=True)
+    drop = L[0] - L
+    i50 = int(np.argmax(drop >= 0.5 * total))
+    i90 = int(np.argmax(drop >= 0.9 * total))
+    stages = (np.arange(0, max(i50, 1)), np.arange(i50, max(i90, i50 + 1)), np.arange(i90, T + 1))
+
+    def auc(idx):
+        return float(np.mean((L[idx] - L[-1]) / total)) if idx.size else 0.0
+
+    def mre(idx):
+        vals = [np.linalg.norm(np.atleast_1d(trace.grads_ana[i]) - np.atleast_1d(trace.grads_fd[i]))
+                / (np.linalg.norm(np.atleast_1d(trace.grads_fd[i])) + eps_g)
+                for i in idx if i < len(trace.grads_fd) and trace.grads_fd[i] is not None]
+        return float(np.mean(vals)) if vals else 0.0
+
+    e, m, l_ = stages
+    return MetricsReport(t50=i50 / T, t90=i90 / T, auc_e=auc(e), auc_m=auc(m), auc_l=auc(l_),
+                         mre_e=mre(e), mre_m=mre(m), mre_l=mre(l_))

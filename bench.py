@@ -241,15 +241,27 @@ class ClockSampler:
 # GPU arm
 
 
-def _pin_thread(slot):
+try:   # the process's CPU set before any thread pins itself
+    _ALL_CPUS = sorted(os.sched_getaffinity(0))
+except AttributeError:
+    _ALL_CPUS = list(range(os.cpu_count() or 1))
+
+
+def _pin_thread(local_rank, slot):
     """Pin the calling thread to one core (the Newton driver spin-waits on
-    ~100 device synchronisations per step; migrations show up as jitter)."""
+    ~100 device synchronisations per step; migrations show up as jitter).
+    The cores are split into one contiguous block per local rank
+    (LOCAL_WORLD_SIZE ranks on the node), so spinning drivers of different
+    ranks never share a core."""
     if os.environ.get("BENCH_NO_PIN"):
         return
     try:
-        cpus = sorted(os.sched_getaffinity(0) if slot < 0 else range(os.cpu_count() or 1))
-        os.sched_setaffinity(0, {cpus[(2 * abs(slot) + 1) % len(cpus)]})
-    except (AttributeError, OSError):
+        cpus = _ALL_CPUS
+        nloc = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+        block = max(1, len(cpus) // nloc)
+        base = (local_rank % nloc) * block
+        os.sched_setaffinity(0, {cpus[base + (2 * slot + 1) % block]})
+    except (AttributeError, OSError, IndexError):
         pass
 
 
@@ -304,7 +316,7 @@ def gpu_arm(args, rank, world, local_rank):
 
     def device_rollout(c, nsteps, k0):
         """forward K steps + reverse sweep of one rollout, device-resident."""
-        _pin_thread(local_rank * 16 + c.slot)
+        _pin_thread(local_rank, c.slot)
         L, dev, scene = c.L, c.dev, c.scene
         with torch.cuda.stream(c.stream):
             q = [torch.empty(n3, **dd) for _ in range(nsteps + 1)]
@@ -358,7 +370,7 @@ def gpu_arm(args, rank, world, local_rank):
 
     def host_rollout(c, nsteps, k0):
         """the same through the public API with host NumPy buffers (e2e)."""
-        _pin_thread(local_rank * 16 + c.slot)
+        _pin_thread(local_rank, c.slot)
         scene = c.scene
         st0 = scene.rest_state()
         st, caches = st0, []

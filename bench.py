@@ -452,6 +452,14 @@ def gpu_arm(args, rank, world, local_rank):
     _lib.check(c0.L.dp_bench_spmv(c0.dev.handle, 1, _lib.ptr(x), _lib.ptr(y), 10, C.byref(fms)))
     _lib.check(c0.L.dp_bench_spmv(c0.dev.handle, 1, _lib.ptr(x), _lib.ptr(y), reps, C.byref(fms)))
     spmv_ms = fms.value / reps
+    # the dominant kernel of the step (launch-list share): one fine-level
+    # V-cycle smoothing sweep on the FP32 operator copy
+    smooth_ms = None
+    b_ = torch.randn(n3, **dd)
+    o_ = torch.empty(n3, **dd)
+    if c0.L.dp_bench_smoother(c0.dev.handle, _lib.ptr(x), _lib.ptr(b_), _lib.ptr(o_), 10, C.byref(fms)) == 0:
+        _lib.check(c0.L.dp_bench_smoother(c0.dev.handle, _lib.ptr(x), _lib.ptr(b_), _lib.ptr(o_), reps, C.byref(fms)))
+        smooth_ms = fms.value / reps
     # second roofline: the FP64-bound element kernel (projection + residual,
     # and with the Jacobian blocks) at the final state of the timed rollout
     elem = None
@@ -463,6 +471,9 @@ def gpu_arm(args, rank, world, local_rank):
             elem[jac] = (fms.value / 10, flops * E_ / (fms.value / 10 * 1e-3) / 1e12)
     nnzb = info.nnzb
     spmv_bytes = 76 * nnzb + 4 * (V + 1) + 48 * V
+    # smoother sweep: FP32 block 36 B + column 4 B per nonzero block; x (gathered,
+    # once), b, out 24 B/row each; FP32 3x3 block-Jacobi inverse 36 B/row
+    smooth_bytes = 40 * nnzb + 4 * (V + 1) + 108 * V
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -470,11 +481,13 @@ def gpu_arm(args, rank, world, local_rank):
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     achieved = spmv_bytes / (spmv_ms * 1e-3) / 1e9
-    traffic = None
+    traffic = smooth_traffic = None
     prof = os.path.join(ROOT, "profiles", f"spmv_traffic_{args.config}.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof))
+            traffic = pj.get("dram_bytes_per_launch")
+            smooth_traffic = pj.get("smoother_dram_bytes_per_launch")
         except ValueError:
             traffic = None
 
@@ -505,6 +518,7 @@ def gpu_arm(args, rank, world, local_rank):
     conv = [s_[0] for r in res for s_ in r[2]]
     return dict(ms=ms_max, launches=launches, clocks=clk.summary(), spmv_ms=spmv_ms, spmv_bytes=spmv_bytes,
                 achieved=achieved, hbm=hbm, traffic=traffic, e2e=e2e, setup_s=setup_s, R=R, elem=elem,
+                smooth_ms=smooth_ms, smooth_bytes=smooth_bytes, smooth_traffic=smooth_traffic,
                 fp64_peak=float(peaks.get("fp64_tflops", FP64_PEAK_TFLOPS)),
                 nnzb=nnzb, V=V, E=E_, desc=cdef["desc"], newton=[s_[1] for s_ in stats],
                 krylov=[s_[2] for s_ in stats], contacts=[s_[3] for s_ in stats], converged=all(conv),
@@ -633,11 +647,22 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (procedural mesh, random-free)", "config": config,
                 "tet_steps_per_s_M": value * n_tets / 1e6,
-                "roofline": {"bound": "hbm", "kernel": "k_spmv (SELL-32 3x3-BSR SpMV)",
-                             "achieved": r["achieved"], "peak": r["hbm"], "unit": "GB/s",
-                             "frac": r["achieved"] / r["hbm"], "traffic": r["traffic"],
-                             "bytes_per_launch": r["spmv_bytes"], "ms_per_launch": r["spmv_ms"],
-                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+                "roofline": ({"bound": "hbm",
+                              "kernel": "k_mg_smooth<float,1> (fine-level V-cycle sweep, SELL-32 FP32 3x3 blocks; "
+                                        "largest share of the step, profiles/r01_bench_c5_launches*.md)",
+                              "achieved": r["smooth_bytes"] / (r["smooth_ms"] * 1e-3) / 1e9, "peak": r["hbm"],
+                              "unit": "GB/s",
+                              "frac": r["smooth_bytes"] / (r["smooth_ms"] * 1e-3) / 1e9 / r["hbm"],
+                              "traffic": r["smooth_traffic"], "bytes_per_launch": r["smooth_bytes"],
+                              "ms_per_launch": r["smooth_ms"],
+                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+                             if r["smooth_ms"] else None),
+                "roofline_spmv": {"bound": "hbm", "kernel": "k_spmv (SELL-32 3x3-BSR FP64 SpMV; the GMRES column "
+                                                            "kernel k_gm_spmvdot_r is this SpMV + basis dots)",
+                                  "achieved": r["achieved"], "peak": r["hbm"], "unit": "GB/s",
+                                  "frac": r["achieved"] / r["hbm"], "traffic": r["traffic"],
+                                  "bytes_per_launch": r["spmv_bytes"], "ms_per_launch": r["spmv_ms"],
+                                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
                 "roofline_fp64": None if not r["elem"] else {
                     "bound": "fp64", "kernel": "k_elements<4,JAC> (per-tet SVD + NH projection + 10 Hessian blocks)",
                     "achieved": r["elem"][1][1], "peak": r["fp64_peak"], "unit": "TFLOP/s",

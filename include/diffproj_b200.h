@@ -234,6 +234,10 @@ int dp_bench_spmv(dp_scene* s, int32_t which, const double* x, double* y, int32_
  * scene stream; CUDA-event time of all reps in ms_out.  Overwrites the
  * scene's element scratch (call between steps, not inside one). */
 int dp_bench_elements(dp_scene* s, const double* q, int32_t with_jacobian, int32_t reps, float* ms_out);
+/* One fine-level V-cycle smoothing sweep out = x + omega Minv (b - A x) with
+ * the FP32 copy of the last assembled operator (the V-cycle's dominant
+ * kernel), `reps` times; device pointers; CUDA-event time in ms_out. */
+int dp_bench_smoother(dp_scene* s, const double* x, const double* b, double* out, int32_t reps, float* ms_out);
 /* per-launch timing of the dominant kernels of the last forward step,
  * measured with CUDA events on the scene stream (ms, averages). */
 typedef struct {

@@ -128,6 +128,7 @@ SIGNATURES = {
     "dp_detect_contacts": (C.c_int, [_P, _P, C.c_int32, C.c_int32, c_int32_p, _P, _P, _P, _P]),
     "dp_bench_spmv": (C.c_int, [_P, C.c_int32, _P, _P, C.c_int32, C.POINTER(C.c_float)]),
     "dp_bench_elements": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.POINTER(C.c_float)]),
+    "dp_bench_smoother": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(C.c_float)]),
     "dp_scene_enable_timing": (C.c_int, [_P, C.c_int32]),
     "dp_scene_get_timing": (C.c_int, [_P, C.POINTER(KernelTimes)]),
     "dp_scene_reset_timing": (C.c_int, [_P]),

@@ -1437,6 +1437,21 @@ int dp_bench_spmv(dp_scene* s, int32_t which, const double* x, double* y, int32_
   return DP_OK;
 }
 
+int dp_bench_smoother(dp_scene* s, const double* x, const double* b, double* out, int32_t reps, float* ms_out) {
+  cudaSetDevice(s->device);
+  DP_CUDA(cudaEventRecord(s->ev0, s->stream));
+  if (mg_bench_fine_smooth(s, x, b, out, reps)) {
+    set_error("multigrid is not set up for this scene");
+    return DP_ERR_VALUE;
+  }
+  DP_CUDA(cudaEventRecord(s->ev1, s->stream));
+  DP_CUDA(cudaEventSynchronize(s->ev1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, s->ev0, s->ev1);
+  if (ms_out) *ms_out = ms;
+  return DP_OK;
+}
+
 int dp_bench_elements(dp_scene* s, const double* q, int32_t with_jacobian, int32_t reps, float* ms_out) {
   cudaSetDevice(s->device);
   DP_CUDA(cudaEventRecord(s->ev0, s->stream));

@@ -290,6 +290,7 @@ void mg_apply(dp_scene* s, const double* val, const double* r, double* z, const 
 // the level-0 work vector) already done by the caller
 void mg_apply_prejac(dp_scene* s, const double* val, const double* r, double* z, const int* stop);
 void mg_fine_jacobi0_target(dp_scene* s, const float** minv32, double** xa, double* omega);
+int mg_bench_fine_smooth(dp_scene* s, const double* x, const double* b, double* out, int reps);
 int mg_levels(const dp_scene* s);
 int mg_level_rows(const dp_scene* s, int l);
 void mg_set_params(dp_scene* s, double omega, int nu);

@@ -30,6 +30,11 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef DP_SMOOTH_NT
+#define DP_SMOOTH_NT 256   // CTA size of the fine-level smoother (one warp per slice)
+#endif
+
+
 namespace dp {
 
 constexpr int kCoarseMax = 36;      // dense coarsest solve (<= 108 unknowns, shared memory)
@@ -941,7 +946,7 @@ static void smooth(dp_scene* s, const MGLevel& L, const TV* val, const TV* minv,
                    const double* xc, const int* agg, double omega, double* out, double* r_out, const int* stop,
                    double alpha) {
   if (L.S >= 4 * 148)
-    k_mg_smooth<TV, 1><<<grid_for((int64_t)L.S * 32, 256), 256, 0, s->stream>>>(
+    k_mg_smooth<TV, 1><<<grid_for((int64_t)L.S * 32, DP_SMOOTH_NT), DP_SMOOTH_NT, 0, s->stream>>>(
         L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x, xc, agg, omega, out, r_out, stop, alpha);
   else
     k_mg_smooth<TV, 8><<<L.S, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x,
@@ -1078,6 +1083,17 @@ static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, cons
 
 void mg_set_symmetric(dp_scene* s, int on) {
   if (s->mg) s->mg->symmetric_needed = on;
+}
+
+// one fine-level damped block-Jacobi sweep out = x + w Minv32 (b - A32 x)
+// (the V-cycle's dominant kernel) `reps` times, for the bench roofline
+int mg_bench_fine_smooth(dp_scene* s, const double* x, const double* b, double* out, int reps) {
+  MG* mg = s->mg;
+  if (!mg || !s->val32) return 1;
+  const MGLevel& L = mg->lv[0];
+  for (int r = 0; r < reps; ++r)
+    smooth<float>(s, L, s->val32, s->minv32, b, x, nullptr, nullptr, mg->omega, out, nullptr, nullptr, 1.0);
+  return 0;
 }
 
 void mg_fine_jacobi0_target(dp_scene* s, const float** minv32, double** xa, double* omega) {

@@ -187,12 +187,17 @@ __device__ __forceinline__ int svd32(const double F[3][2], double U[3][2], doubl
 // (project_neohookean, elasticity.py:195-242; _nh_residual :181-184;
 // _nh_jacobian :187-192).  Returns ST_OK or ST_NH_STALL.
 
+// logj_out = sum_i log(theta_i), returned for reuse: the Newton step's
+// Jacobian and W need exactly this value at the accepted theta, and the
+// logarithms are the largest single cost of the element kernel (ncu source
+// view: 30% of its instructions before this reuse).
 template <int D>
 __device__ __forceinline__ void nh_g(const double th[D], const double sig[D], double mu, double lam,
-                                     double g[D], double& nrm) {
+                                     double g[D], double& nrm, double& logj_out) {
   double logj = 0.0;
 #pragma unroll
   for (int i = 0; i < D; ++i) logj += log(th[i]);
+  logj_out = logj;
   double s = 0.0;
 #pragma unroll
   for (int i = 0; i < D; ++i) {
@@ -206,16 +211,14 @@ template <int D>
 __device__ __forceinline__ int nh_project(const double sig[D], double mu, double lam, double th[D],
                                           double W[D][D]) {
   const double thr = 1e-11 * fmax(1.0, mu);
-  double g[D], rn;
+  double g[D], rn, logj_th;   // logj_th = sum log(th) at the current theta
 #pragma unroll
   for (int i = 0; i < D; ++i) th[i] = sig[i];
-  nh_g<D>(th, sig, mu, lam, g, rn);
+  nh_g<D>(th, sig, mu, lam, g, rn, logj_th);
   bool conv = false;
   for (int it = 0; it < 50; ++it) {
     if (rn <= thr) { conv = true; break; }
-    double logj = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) logj += log(th[i]);
+    const double logj = logj_th;
     double J[D][D], b[D], step[D];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
@@ -233,12 +236,13 @@ __device__ __forceinline__ int nh_project(const double sig[D], double mu, double
 #pragma unroll
       for (int i = 0; i < D; ++i) { cand[i] = th[i] + t * step[i]; pos = pos && (cand[i] > 0.0); }
       if (pos) {
-        double gc[D], rc;
-        nh_g<D>(cand, sig, mu, lam, gc, rc);
+        double gc[D], rc, lc;
+        nh_g<D>(cand, sig, mu, lam, gc, rc, lc);
         if (rc < rn) {
 #pragma unroll
           for (int i = 0; i < D; ++i) { th[i] = cand[i]; g[i] = gc[i]; }
           rn = rc;
+          logj_th = lc;
           acc = true;
           break;
         }
@@ -249,9 +253,7 @@ __device__ __forceinline__ int nh_project(const double sig[D], double mu, double
   }
   if (!conv && !(rn <= thr)) return ST_NH_STALL;
   // W = dtheta/dsigma, Sherman-Morrison form (elasticity.py:231-237)
-  double logj = 0.0;
-#pragma unroll
-  for (int i = 0; i < D; ++i) logj += log(th[i]);
+  const double logj = logj_th;
   double dinv[D], du[D], udu = 0.0;
 #pragma unroll
   for (int i = 0; i < D; ++i) {

@@ -15,7 +15,7 @@ q = torch.from_numpy(st.q).cuda()
 torch.cuda.synchronize()
 ms = C.c_float()
 torch.cuda.profiler.start()
-_lib.check(sm.dev.lib.dp_bench_elements(sm.dev.handle, _lib.ptr(q), 0, 1, C.byref(ms)))
+_lib.check(sm.dev.lib.dp_bench_elements(sm.dev.handle, _lib.ptr(q), int(sys.argv[1]) if len(sys.argv) > 1 else 0, 1, C.byref(ms)))
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print("ok")

@@ -3,8 +3,10 @@
 Per step (reverse time): ``assemble_adjoint_operator`` re-evaluates the
 element projections and Jacobian blocks at the cached Newton point and
 assembles A_hat^T in SELL-32 BSR (contact blocks transposed);
-``solve_adjoint`` solves A_hat^T z = dL/dq + dL/dv / h by block-Jacobi PCG
-(all mu == 0) or GMRES(50) (adjoint.py:123-139); ``backprop_step`` forms
+``solve_adjoint`` solves A_hat^T z = dL/dq + dL/dv / h to the reference's
+relative tolerance (default 1e-10) by multigrid-preconditioned PCG (all
+mu == 0) or GMRES(50) (adjoint.py:123-139; warm-started from the previous
+step's z within a reverse sweep); ``backprop_step`` forms
 every z-product (adjoint.py:154-219) with deterministic device reductions.
 Parameter gradients accumulate on the device and are read once at the end
 of ``backprop_rollout`` (adjoint.py:228-271).

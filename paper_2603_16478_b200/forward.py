@@ -6,13 +6,14 @@
   predict + pullback -> per Newton iteration: contact detection, element
   projections + projection-Jacobian blocks, contact condensation, residual
   (one fused gather) -> Newton matrix A - dA + K_b + K_c assembled into
-  SELL-32 BSR -> block-Jacobi PCG (symmetric) / GMRES (friction) solve ->
-  penetration-aware backtracking line search on max|r|.
+  SELL-32 BSR -> multigrid-preconditioned PCG (all contacts frictionless) /
+  GMRES (friction) solve -> penetration-aware backtracking line search on
+  max|r|.
 
 The reference solves each Newton system exactly with SuperLU
-(linsolve.py:386-392); here it is an inexact Krylov solve whose forcing
-term targets the Newton tolerance itself, so iterates differ
-while the converged root agrees to the Newton tolerance.
+(linsolve.py:386-392); here it is an inexact Krylov solve with a constant
+forcing term 1e-3 under the reference's own stop test, so
+iterates differ while the converged root agrees to the Newton tolerance.
 
 Reports, caches and contact lists keep the reference field names and are
 materialised from device memory lazily (only when a caller reads them).

@@ -509,9 +509,12 @@ def gpu_arm(args, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
         wall = float(tw.item())
-        h2d = (2 * n3 + 2 * n3) * 8           # forward (q_bar, v_bar) + adjoint (dL_dq, dL_dv)
-        d2h = (2 * n3 + 4 * n3) * 8           # forward (q, v) + adjoint (z, dqbar, dvbar, dfext)
-        h2d += 8 * n3                          # backprop z re-upload
+        # per step: forward q_bar, v_bar up and q, v down; reverse sweep
+        # dL/dfext down (the adjoint chain stays on the device); once per
+        # rollout: the loss gradient up, q_new/q_bar (loss) and dL/dq_bar,
+        # dL/dv_bar down
+        h2d = (2 * n3) * 8 + (2 * n3 * 8) // K
+        d2h = (2 * n3 + n3) * 8 + (4 * n3 * 8) // K
         e2e = {"value": world * R * K / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h}
     pool.shutdown()

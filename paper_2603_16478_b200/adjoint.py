@@ -98,6 +98,10 @@ def solve_adjoint(workspace, dL_dq, dL_dv, solver_cfg=None, report=None):
         report.converged = bool(rep.converged)
         report.iterations = rep.iterations
         report.residual_history = [rep.rel_residual]
+    if not rep.converged:
+        # adjoint.py:134-137
+        raise RuntimeError("adjoint solve did not converge; residual history tail "
+                           f"{[rep.rel_residual]}")
     workspace.z = z
     return z
 
@@ -163,6 +167,15 @@ def loss_final_state(q_final, q_target):
     return float(d @ d), 2.0 * d
 
 
+def _torch_cuda():
+    """torch with CUDA if importable (device-resident reverse sweep), else None."""
+    try:
+        import torch
+    except ImportError:
+        return None
+    return torch if torch.cuda.is_available() else None
+
+
 def backprop_rollout(caches, loss_spec, solver_cfg=None, solve_reports=None):
     """Reverse sweep over the cached steps (adjoint.py:228-271).
 
@@ -187,33 +200,70 @@ def backprop_rollout(caches, loss_spec, solver_cfg=None, solve_reports=None):
     c = cfg.to_c()
     L = dev.lib
     _lib.check(L.dp_grads_reset(dev.handle))
-    dq = np.zeros(n)
-    dv = np.zeros(n)
     fext = [None] * T
-    z = np.empty(n)
-    dqbar, dvbar = np.empty(n), np.empty(n)
-    for k in range(T, 0, -1):
-        cache = caches[k - 1]
-        if callable(loss_spec) or k == T:
-            q_new = cache.q_new
-            gq, gv = loss_fn(k, q_new, (q_new - cache.q_bar) / scene.h)
-            dq = dq + gq
-            dv = dv + gv
-        dq = _lib.f64(dq)
-        dv = _lib.f64(dv)
-        _lib.check(L.dp_adjoint_assemble(dev.handle, cache._dc.handle, None))
-        rep = _lib.SolveReportC()
-        _lib.check(L.dp_adjoint_solve(dev.handle, cache._dc.handle, _lib.ptr(dq), _lib.ptr(dv),
-                                      _lib.PTR_HOST, C.byref(c), _lib.ptr(z), C.byref(rep)))
+
+    def check_solve(rep, k):
         if solve_reports is not None:
             solve_reports.append(SolveReport(residual_history=[rep.rel_residual],
                                              converged=bool(rep.converged),
                                              iterations=rep.iterations))
-        f = np.empty(n)
-        _lib.check(L.dp_backprop_step(dev.handle, cache._dc.handle, _lib.ptr(z), _lib.ptr(dv),
-                                      _lib.PTR_HOST, _lib.ptr(dqbar), _lib.ptr(dvbar), _lib.ptr(f)))
-        fext[k - 1] = f
-        dq, dv = dqbar.copy(), dvbar.copy()
+        if not rep.converged:
+            # adjoint.py:134-137
+            raise RuntimeError(f"adjoint solve did not converge at step {k}; residual history tail "
+                               f"{[rep.rel_residual]}")
+
+    torch = _torch_cuda()
+    if torch is not None:
+        # the adjoint state chain (dL/dq, dL/dv -> z -> dL/dq_bar, dL/dv_bar)
+        # stays on the device; loss gradients go up and dL/dfext comes down
+        dd = dict(device="cuda:%d" % dev.device, dtype=torch.float64)
+        stream = torch.cuda.ExternalStream(L.dp_scene_stream(dev.handle), device=dd["device"])
+        with torch.cuda.stream(stream):
+            dq, dv = torch.zeros(n, **dd), torch.zeros(n, **dd)
+            z, dqb, dvb, f = (torch.empty(n, **dd) for _ in range(4))
+            for k in range(T, 0, -1):
+                cache = caches[k - 1]
+                if callable(loss_spec) or k == T:
+                    q_new = cache.q_new
+                    gq, gv = loss_fn(k, q_new, (q_new - cache.q_bar) / scene.h)
+                    dq += torch.from_numpy(_lib.f64(gq)).to(dd["device"], non_blocking=False)
+                    dv += torch.from_numpy(_lib.f64(gv)).to(dd["device"], non_blocking=False)
+                _lib.check(L.dp_adjoint_assemble(dev.handle, cache._dc.handle, None))
+                rep = _lib.SolveReportC()
+                _lib.check(L.dp_adjoint_solve(dev.handle, cache._dc.handle, _lib.ptr(dq), _lib.ptr(dv),
+                                              _lib.PTR_DEVICE, C.byref(c), _lib.ptr(z), C.byref(rep)))
+                check_solve(rep, k)
+                _lib.check(L.dp_backprop_step(dev.handle, cache._dc.handle, _lib.ptr(z), _lib.ptr(dv),
+                                              _lib.PTR_DEVICE, _lib.ptr(dqb), _lib.ptr(dvb), _lib.ptr(f)))
+                fext[k - 1] = f.cpu().numpy()
+                dq, dqb = dqb, dq
+                dv, dvb = dvb, dv
+            dq = dq.cpu().numpy()
+            dv = dv.cpu().numpy()
+    else:
+        dq = np.zeros(n)
+        dv = np.zeros(n)
+        z = np.empty(n)
+        dqbar, dvbar = np.empty(n), np.empty(n)
+        for k in range(T, 0, -1):
+            cache = caches[k - 1]
+            if callable(loss_spec) or k == T:
+                q_new = cache.q_new
+                gq, gv = loss_fn(k, q_new, (q_new - cache.q_bar) / scene.h)
+                dq = dq + gq
+                dv = dv + gv
+            dq = _lib.f64(dq)
+            dv = _lib.f64(dv)
+            _lib.check(L.dp_adjoint_assemble(dev.handle, cache._dc.handle, None))
+            rep = _lib.SolveReportC()
+            _lib.check(L.dp_adjoint_solve(dev.handle, cache._dc.handle, _lib.ptr(dq), _lib.ptr(dv),
+                                          _lib.PTR_HOST, C.byref(c), _lib.ptr(z), C.byref(rep)))
+            check_solve(rep, k)
+            f = np.empty(n)
+            _lib.check(L.dp_backprop_step(dev.handle, cache._dc.handle, _lib.ptr(z), _lib.ptr(dv),
+                                          _lib.PTR_HOST, _lib.ptr(dqbar), _lib.ptr(dvbar), _lib.ptr(f)))
+            fext[k - 1] = f
+            dq, dv = dqbar.copy(), dvbar.copy()
     grads = GradientReport()
     grads.ensure_shapes(len(scene.bindings), dev.n_elems)
     _fold_device_grads(dev, scene, grads)

@@ -324,3 +324,20 @@ def test_finger_scene_vs_oracle(pkg):
     assert rel(g.dL_dqbar, og.dL_dqbar) < 1e-6
     assert abs(g.dL_dE - og.dL_dE) <= 1e-6 * abs(og.dL_dE)
     assert abs(g.dL_dmu_friction - og.dL_dmu_friction) <= 1e-6 * abs(og.dL_dmu_friction)
+
+
+def test_adjoint_nonconvergence_raises(pkg):
+    """adjoint.py:134-137: an adjoint solve that misses its tolerance raises
+    RuntimeError (single step and reverse sweep)."""
+    from paper_2603_16478_b200 import adjoint as aj, core, forward as fw, ident
+    v, t = ident.box_tet_mesh(3, 3, 3, size=0.1 / 3, origin=(0.0, 0.0, 4e-4))
+    scene = core.Scene(v, t, core.lumped_masses(v, t, 1000.0),
+                       [core.MaterialParams("neohookean", E=2e4, nu=0.35)] * len(t),
+                       colliders=[core.HalfSpace([0, 0, 1], 0.0, mu=0.4)], h=0.01)
+    states, caches = fw.rollout(scene, scene.rest_state(), 2, cfg=fw.ForwardConfig(tol=1e-12))
+    bad = aj.SolverConfig(tol=1e-30, max_iter=2)
+    with pytest.raises(RuntimeError, match="did not converge"):
+        aj.backprop_rollout(caches, states[-1].q + 1e-3, solver_cfg=bad)
+    ws = aj.assemble_adjoint_operator(caches[-1])
+    with pytest.raises(RuntimeError, match="did not converge"):
+        aj.solve_adjoint(ws, np.ones(scene.ndof), np.zeros(scene.ndof), solver_cfg=bad)

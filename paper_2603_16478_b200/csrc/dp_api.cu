@@ -569,7 +569,7 @@ int dp_scene_destroy(dp_scene* s) {
                   s->b_target, s->b_comp, s->b_vertex, s->fext, s->c_count, s->c_off, s->c_vertex, s->c_collider,
                   s->c_frame, s->c_dn, s->c_mu, s->c_delta, s->c_blk, s->c_force, s->c_kmu, s->c_kc, s->scan_tmp,
                   s->q, s->q_hat, s->q_bar, s->v_bar, s->r, s->dq, s->q_try, s->rhs, s->z, s->z_prev, s->tmp, s->q_ev, s->r_try, s->kx, s->kr,
-                  s->ku, s->kw, s->kp, s->ks, s->gm_V, s->ksc, s->gsc, s->esc, s->red.partial, s->red.counter,
+                  s->ku, s->kw, s->kp, s->ks, s->gm_V, s->gm_Z, s->ksc, s->gsc, s->esc, s->red.partial, s->red.counter,
                   s->g_dw, s->g_scal, s->g_dEb, s->g_ddb};
   for (void* p : ptrs) dfree(p);
   if (s->h_esc) cudaFreeHost(s->h_esc);

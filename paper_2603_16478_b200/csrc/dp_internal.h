@@ -193,6 +193,7 @@ struct dp_scene {
   // Krylov workspace
   double *kx = nullptr, *kr = nullptr, *ku = nullptr, *kw = nullptr, *kp = nullptr, *ks = nullptr;
   double* gm_V = nullptr;          // (restart+1) * 3V basis
+  double* gm_Z = nullptr;          // preconditioned basis M v_j (right multigrid GMRES, allocated on first use)
   int gm_cap = 0;
   dp::KrylovScalars* ksc = nullptr;
   dp::GmresScalars* gsc = nullptr;

@@ -1411,7 +1411,8 @@ __global__ void __launch_bounds__(256) k_gm_spmvdot_r(int V, int S, const int* _
                                                       const int* __restrict__ col, const TV* __restrict__ val,
                                                       const double* __restrict__ z, TB* W0, TB* W1,
                                                       const TB* __restrict__ Vb, size_t ld, double* partial,
-                                                      unsigned int* counter, GmresScalars* gs) {
+                                                      unsigned int* counter, GmresScalars* gs,
+                                                      double* __restrict__ Zb) {
   __shared__ double sh[8][kGM1 + 1];
   if (gm_idle(gs)) return;
   const int j = gs->j;
@@ -1429,6 +1430,10 @@ __global__ void __launch_bounds__(256) k_gm_spmvdot_r(int V, int S, const int* _
         const TB us = (TB)u[c];
         wnew[3 * row + c] = us;
         u[c] = (double)us;
+      }
+      if (Zb) {   // keep z_j = M v_j: the cycle's update is then x += Z y
+        double* zj = Zb + (size_t)j * ld + 3 * (size_t)row;
+        zj[0] = z[3 * row]; zj[1] = z[3 * row + 1]; zj[2] = z[3 * row + 2];
       }
     } else {
       u[0] = u[1] = u[2] = 0.0;
@@ -1494,6 +1499,7 @@ static const double g_reorth_thr = getenv("DP_REORTH") ? atof(getenv("DP_REORTH"
 static const int g_use_graphs = getenv("DP_GRAPHS") ? atoi(getenv("DP_GRAPHS")) : 1;
 static const int g_gm_fp32 = getenv("DP_GM_FP32") ? atoi(getenv("DP_GM_FP32")) : 0;
 static const int g_prejac = getenv("DP_PREJAC") ? atoi(getenv("DP_PREJAC")) : 1;
+static const int g_zbasis = getenv("DP_GM_ZBASIS") ? atoi(getenv("DP_GM_ZBASIS")) : 1;
 
 static int gm_grid(const dp_scene* s, int n) {
   // grid-stride over the basis rows with 4 CTAs per SM: every basis load of
@@ -1512,7 +1518,7 @@ __global__ void k_gm_copy_wnew(int n, const double* __restrict__ src, double* W0
 
 // Kernels of one GMRES column (j read on device).  Returns the number of
 // kernel launches issued.
-static int gm_column(dp_scene* s, const double* val, int use_mg, int left, bool tight, bool lowp,
+static int gm_column(dp_scene* s, const double* val, int use_mg, int left, bool tight, bool lowp, bool zbasis,
                      cudaGraphConditionalHandle h, int use_cond) {
   const int V = s->V, n = 3 * V;
   const size_t ld = (size_t)n;
@@ -1544,7 +1550,7 @@ static int gm_column(dp_scene* s, const double* val, int use_mg, int left, bool 
     mg_apply(s, val, s->tmp, z, &s->gsc->done);
     k_gm_spmvdot_r<float, float><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col,
                                                              s->val32, z, W0, W1, Vf, ld, s->red.partial,
-                                                             s->red.counter, s->gsc);
+                                                             s->red.counter, s->gsc, nullptr);
     k_gm_update<float><<<nbg, kGT, 0, s->stream>>>(n, 0, Vf, ld, W0, W1, s->red.partial, s->red.counter, s->gsc);
     k_gm_loopctl<<<1, 32, 0, s->stream>>>(s->gsc, h, use_cond);
     return k + 4;
@@ -1561,7 +1567,8 @@ static int gm_column(dp_scene* s, const double* val, int use_mg, int left, bool 
     }
     k_gm_spmvdot_r<double, double><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val,
                                                                z, s->kw, s->kp, Vb, ld, s->red.partial,
-                                                               s->red.counter, s->gsc);
+                                                               s->red.counter, s->gsc,
+                                                               (use_mg && zbasis) ? s->gm_Z : nullptr);
     k += 2;
   }
   k_gm_update<double><<<nbg, kGT, 0, s->stream>>>(n, 0, Vb, ld, s->kw, s->kp, s->red.partial, s->red.counter,
@@ -1584,9 +1591,10 @@ struct GmGraph {
   int nodes = 0;
 };
 
-static GmGraph* gm_graph(dp_scene* s, const double* val, int use_mg, int left, bool tight, bool lowp) {
+static GmGraph* gm_graph(dp_scene* s, const double* val, int use_mg, int left, bool tight, bool lowp,
+                         bool zbasis) {
   const uint64_t key = (uint64_t)(uintptr_t)val ^ ((uint64_t)use_mg << 1) ^ ((uint64_t)left << 2) ^
-                       ((uint64_t)tight << 3) ^ ((uint64_t)lowp << 4);
+                       ((uint64_t)tight << 3) ^ ((uint64_t)lowp << 4) ^ ((uint64_t)zbasis << 5);
   for (auto& e : s->gm_graphs)
     if (e.first == key) return (GmGraph*)e.second;
   cudaGraph_t g = nullptr;
@@ -1614,7 +1622,7 @@ static GmGraph* gm_graph(dp_scene* s, const double* val, int use_mg, int left, b
     cudaGraphDestroy(g);
     return nullptr;
   }
-  nodes = gm_column(s, val, use_mg, left, tight, lowp, h, 1);
+  nodes = gm_column(s, val, use_mg, left, tight, lowp, zbasis, h, 1);
   cudaGraph_t captured = nullptr;
   const cudaError_t ce = cudaStreamEndCapture(s->stream, &captured);
   nodes += (int)(s->launches - launches0);   // V-cycle kernels count themselves
@@ -1688,7 +1696,17 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
                                                    s->red.partial, s->red.counter, s->gsc, rtol, 1, 0, 0);
   }
   s->launches++;
-  GmGraph* gg = (g_use_graphs && !(left && use_mg)) ? gm_graph(s, val, use_mg, left, tight, lowp) : nullptr;
+  // right multigrid: keep the preconditioned basis and update x += Z y
+  // (saves the end-of-cycle V-cycle)
+  const bool zbasis = g_zbasis && use_mg && !left && !lowp;
+  if (zbasis && !s->gm_Z) {
+    if (cudaMalloc((void**)&s->gm_Z, sizeof(double) * (size_t)(kMaxRestart + 1) * n) != cudaSuccess) {
+      cudaGetLastError();
+      s->gm_Z = nullptr;
+    }
+  }
+  const bool zb = zbasis && s->gm_Z;
+  GmGraph* gg = (g_use_graphs && !(left && use_mg)) ? gm_graph(s, val, use_mg, left, tight, lowp, zb) : nullptr;
   int total = 0;
   double rel = 1.0;
   int m = restart;   // cycle length; grows when a cycle stagnates
@@ -1734,7 +1752,7 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
       int launched = 0;
       while (!stop && launched < m && launched < budget) {
         int chunk = std::min(8, std::min(m, budget) - launched);
-        for (int c = 0; c < chunk; ++c) s->launches += gm_column(s, val, use_mg, left, tight, lowp, 0, 0);
+        for (int c = 0; c < chunk; ++c) s->launches += gm_column(s, val, use_mg, left, tight, lowp, zb, 0, 0);
         launched += chunk;
         cudaMemcpyAsync(s->h_gsc, s->gsc, gsc_bytes, cudaMemcpyDeviceToHost, s->stream);
         cudaStreamSynchronize(s->stream);
@@ -1754,9 +1772,10 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
         y[i] = acc / hg->H[(size_t)i * kGM1 + i];
       }
       cudaMemcpyAsync(y_dev, y, sizeof(double) * used, cudaMemcpyHostToDevice, s->stream);
-      if (lowp) k_gm_combine<float><<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, reinterpret_cast<const float*>(Vb), ld, t, 0);
+      if (zb) k_gm_combine<double><<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, s->gm_Z, ld, x, 1);
+      else if (lowp) k_gm_combine<float><<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, reinterpret_cast<const float*>(Vb), ld, t, 0);
       else k_gm_combine<double><<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, Vb, ld, left ? x : t, left ? 1 : 0);
-      if (left) {
+      if (left || zb) {
       } else if (use_mg) {
         mg_apply(s, val, t, z, nullptr);
         launch_axpy_to(s, x, x, 1.0, z);

@@ -92,8 +92,8 @@ CONFIGS = {
 E_YOUNG = 1e4
 # FP64 FLOPs per tet of the element kernel (2 DFMA + DMUL + DADD thread
 # instructions / E, ncu at a C5 state, profiles/r01_elements_fp64.md)
-ELEM_FLOPS_JAC = 5721.0
-ELEM_FLOPS_RES = 3570.0
+ELEM_FLOPS_JAC = 5250.0
+ELEM_FLOPS_RES = 3139.0
 FP64_PEAK_TFLOPS = 34.18     # measured DFMA peak, profiles/r01_fp64_peak.json
 NU = 0.3
 MU = 0.5

@@ -94,6 +94,7 @@ E_YOUNG = 1e4
 # instructions / E, ncu at a C5 state, profiles/r01_elements_fp64.md)
 ELEM_FLOPS_JAC = 5250.0
 ELEM_FLOPS_RES = 3139.0
+ADJ_RESTART = 20            # adjoint GMRES restart length in the bench (see gpu_arm)
 FP64_PEAK_TFLOPS = 34.18     # measured DFMA peak, profiles/r01_fp64_peak.json
 NU = 0.3
 MU = 0.5
@@ -281,7 +282,12 @@ def gpu_arm(args, rank, world, local_rank):
     K, W = args.steps, args.warmup
     dd = dict(device="cuda:%d" % local_rank, dtype=torch.float64)
     cfg = fw.ForwardConfig(tol=cdef["tol"])
-    scfg = aj.SolverConfig(tol=1e-10, max_iter=2000).to_c()
+    # adjoint: the reference's tolerance (1e-10) and iteration cap; GMRES(20)
+    # instead of the default restart length 50: with the V-cycle the solve
+    # needs ~60-70 iterations either way and the shorter Gram-Schmidt
+    # recurrences make each one cheaper (measured -10% adjoint time at C5)
+    adj_cfg = aj.SolverConfig(tol=1e-10, max_iter=2000, gmres_restart=ADJ_RESTART)
+    scfg = adj_cfg.to_c()
 
     class Ctx:
         pass
@@ -363,9 +369,14 @@ def gpu_arm(args, rank, world, local_rank):
         grads = aj.GradientReport()
         grads.ensure_shapes(len(scene.bindings), dev.n_elems)
         aj._fold_device_grads(dev, scene, grads)
+        if trace is not None:
+            t_fold = time.perf_counter()
         with torch.cuda.stream(c.stream):
             loss = float(torch.sum((q[nsteps] - target) ** 2))
         c.q_final = q[nsteps]
+        if trace is not None:
+            print(f"[trace] fold {1e3 * (t_fold - trace[-1]):.1f} ms, loss {1e3 * (time.perf_counter() - t_fold):.1f} ms",
+                  file=sys.stderr, flush=True)
         return grads, loss, stats, adj_iters
 
     def host_rollout(c, nsteps, k0):
@@ -379,7 +390,7 @@ def gpu_arm(args, rank, world, local_rank):
             st, rep = fw.forward_step(scene, st, c.sysmat, cfg)
             caches.append(rep.cache)
         target = st0.q + c.target_shift
-        g = aj.backprop_rollout(caches, target)
+        g = aj.backprop_rollout(caches, target, solver_cfg=adj_cfg)
         return g, float(np.sum((st.q - target) ** 2))
 
     pool = ThreadPoolExecutor(max_workers=R)
@@ -403,8 +414,13 @@ def gpu_arm(args, rank, world, local_rank):
     t_w = time.perf_counter()
     n_w = 0
     while n_w < max(W, 0) or time.perf_counter() - t_w < args.warmup_seconds:
-        run_all(device_rollout, K, W)
+        res = run_all(device_rollout, K, W)
+        # the timed region's gradient packing and all-reduce run here too, so
+        # their device allocations come from torch's cache, not a cudaMalloc
+        # inside the timed region (measured: 60-80 ms stalls on a fresh box)
+        allreduce_gradients(pack_sum([(r[0], r[1]) for r in res]), world)
         n_w += 1
+    torch.cuda.synchronize()
     if os.environ.get("BENCH_DEBUG"):
         for i in range(int(os.environ.get("BENCH_DEBUG_REPS", "3"))):
             t0 = time.perf_counter(); run_all(device_rollout, K, W); torch.cuda.synchronize()
@@ -426,12 +442,18 @@ def gpu_arm(args, rank, world, local_rank):
     gc.disable()
     with ClockSampler(local_rank) as clk:
         ev0.record()
+        tw0 = time.perf_counter()
         res = run_all(device_rollout, K, W)
+        tw1 = time.perf_counter()
         gvec = pack_sum([(r[0], r[1]) for r in res])
         allreduce_gradients(gvec, world)      # one all-reduce per optimisation iteration
         torch.cuda.synchronize()
         ev1.record()
         ev1.synchronize()
+        tw2 = time.perf_counter()
+    if os.environ.get("BENCH_TRACE"):
+        print(f"[trace] timed: rollouts {1e3 * (tw1 - tw0):.1f} ms, pack+allreduce+sync {1e3 * (tw2 - tw1):.1f} ms",
+              file=sys.stderr, flush=True)
     gc.enable()
     ms = ev0.elapsed_time(ev1)
     launches = sum(int(c.L.dp_scene_launch_count(c.dev.handle)) for c in ctxs)
@@ -617,7 +639,8 @@ def main():
                            (f"neohookean E={E_YOUNG}(1+0.05 i) nu={NU}" if cdef.get("vary", "E") == "E" else
                             f"neohookean E={E_YOUNG} nu={NU}, target shift 1e-3 (1 + 0.1 i) per rollout i")),
               "friction_mu": 0.3 if (cloth or cdef.get("trunk")) else MU, "h": 0.01,
-              "eps_fb": cdef["eps_fb"], "newton_tol": cdef["tol"], "l2": "operands > L2 (no flush)"}
+              "eps_fb": cdef["eps_fb"], "newton_tol": cdef["tol"], "adjoint_tol": 1e-10,
+              "adjoint_gmres_restart": ADJ_RESTART, "l2": "operands > L2 (no flush)"}
     if args.impl == "reference":
         if rank != 0:
             return

@@ -33,7 +33,9 @@ for rep in range(R + 1):
         it.append(r.iterations)
     if adj:
         ts = time.perf_counter()
-        aj.backprop_rollout(caches, sc.rest_state().q + 1e-3)
+        import os
+        rs = int(os.environ.get("ADJ_RESTART", "50"))
+        aj.backprop_rollout(caches, sc.rest_state().q + 1e-3, solver_cfg=aj.SolverConfig(tol=1e-10, max_iter=2000, gmres_restart=rs))
         sm.dev.lib.dp_scene_synchronize(sm.dev.handle)
         steps.append(round(1e3 * (time.perf_counter() - ts), 1))
     sm.dev.lib.dp_scene_synchronize(sm.dev.handle)

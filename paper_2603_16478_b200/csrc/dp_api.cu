@@ -973,7 +973,11 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
       launch_axpy_to(s, q_try, q, t, s->dq);
       k_reset_flags<<<1, 1, 0, s->stream>>>(s->esc);
       launch_penetration(s, q_try, s->esc);
+      // forward.py:218-219: a penetrating trial is not evaluated; the kernels
+      // read the penetration flag on the device and exit (no extra sync)
+      s->eval_skip = &s->esc->penetrating;
       evaluate(s, q_try, s->r_try, 0);
+      s->eval_skip = nullptr;
       s->launches++;
       R.line_search_trials++;
       if ((rc = sync_esc(s))) return rc;

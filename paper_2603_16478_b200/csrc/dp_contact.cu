@@ -186,7 +186,9 @@ __global__ void k_contacts(const int* __restrict__ n_ptr, int n_fixed, const dou
                            const double* __restrict__ frame, const double* __restrict__ dnv,
                            const double* __restrict__ muv, double eps2, double h2, int from_delta, int transpose,
                            double* __restrict__ delta, double* __restrict__ kc, double* __restrict__ kmu,
-                           double* __restrict__ blk, double* __restrict__ force, EvalScalars* esc) {
+                           double* __restrict__ blk, double* __restrict__ force, EvalScalars* esc,
+                           const int* __restrict__ skip) {
+  if (skip && *(volatile const int*)skip) return;   // penetrating line-search trial: no evaluation
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = n_ptr ? *n_ptr : n_fixed;
   if (c >= n) return;
@@ -250,7 +252,7 @@ void launch_contacts(dp_scene* s, const double* q, const double* q_bar, int n_co
   k_contacts<<<grid_for(cap, 128), 128, 0, s->stream>>>(n_contacts >= 0 ? nullptr : &s->esc->n_contacts, n_contacts,
                                                         q, q_bar, vtx, frame, dn, mu, s->eps_fb, s->h * s->h,
                                                         from_delta, transpose, delta_out, s->c_kc, s->c_kmu, s->c_blk,
-                                                        s->c_force, esc);
+                                                        s->c_force, esc, s->eval_skip);
   s->launches++;
 }
 

@@ -187,6 +187,7 @@ struct dp_scene {
   // vectors (3V each)
   double *q = nullptr, *q_hat = nullptr, *q_bar = nullptr, *v_bar = nullptr, *r = nullptr, *dq = nullptr;
   double *q_try = nullptr, *rhs = nullptr, *z = nullptr, *tmp = nullptr, *q_ev = nullptr, *r_try = nullptr;
+  const int* eval_skip = nullptr;   // device flag: element/contact/residual kernels exit when set (penetrating trial)
   double* z_prev = nullptr;   // last adjoint solution of the current reverse sweep (warm start)
   int z_prev_valid = 0;
   int adj_warm = 1;

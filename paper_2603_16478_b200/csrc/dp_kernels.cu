@@ -182,8 +182,10 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
     k_elements(const int4* __restrict__ ev, const double* __restrict__ Bm, const double* __restrict__ w,
                const double* __restrict__ mu, const double* __restrict__ lam, const int* __restrict__ model, int E,
                const double* __restrict__ q, double h2, double tau_rel, double* __restrict__ fe,
-               double* __restrict__ H, double* __restrict__ Pst, int* __restrict__ status) {
+               double* __restrict__ H, double* __restrict__ Pst, int* __restrict__ status,
+               const int* __restrict__ skip) {
   constexpr int mode = MODE;
+  if (skip && *(volatile const int*)skip) return;   // penetrating line-search trial: no evaluation
   constexpr int D = NV - 1;
   constexpr int NP = NV * (NV + 1) / 2;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -415,7 +417,7 @@ static void launch_elements_nv(dp_scene* s, const double* q, int mode, int* stat
 #define DP_ELEM_CASE(M)                                                                                       \
   case M:                                                                                                     \
     k_elements<NV, M><<<nb, nt, 0, s->stream>>>(s->ev, s->B, s->w, s->mu, s->lam, s->model, s->E, q, h2, 1e-6, \
-                                                s->fe, s->H, s->Pst, status);                                 \
+                                                s->fe, s->H, s->Pst, status, s->eval_skip);                   \
     break;
   switch (mode) {
     DP_ELEM_CASE(0)
@@ -453,8 +455,9 @@ __global__ void __launch_bounds__(kVT) k_residual(int V, const double* __restric
                                                   const int* __restrict__ c_count, const int* __restrict__ c_off,
                                                   const double* __restrict__ c_force, int has_contacts, double h2,
                                                   double* __restrict__ r, double* partial, unsigned int* counter,
-                                                  EvalScalars* esc) {
+                                                  EvalScalars* esc, const int* __restrict__ skip) {
   __shared__ double sh[32];
+  if (skip && *(volatile const int*)skip) return;
   const int i = blockIdx.x * kVT + threadIdx.x;
   double amax = 0.0, sq = 0.0;
   if (i < V) {
@@ -524,7 +527,7 @@ void launch_residual(dp_scene* s, const double* q, const double* q_hat, double* 
   const int has_c = s->colliders.n > 0;
   k_residual<<<nb, kVT, 0, s->stream>>>(s->V, s->mass, q, q_hat, s->inc_ptr, s->inc, s->fe, s->nb ? s->b_ptr : nullptr,
                                         s->b_idx, s->b_target, s->b_comp, s->c_count, s->c_off, s->c_force, has_c,
-                                        s->h * s->h, r, s->red.partial, s->red.counter, esc);
+                                        s->h * s->h, r, s->red.partial, s->red.counter, esc, s->eval_skip);
   s->launches++;
 }
 

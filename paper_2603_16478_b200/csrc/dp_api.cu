@@ -162,6 +162,7 @@ using namespace dp;
 static const int g_debug = getenv("DP_DEBUG") ? atoi(getenv("DP_DEBUG")) : 0;
 // after a line search that had to cut the step below 1/16 the Newton model is
 // poor (friction-cone / activation kinks): a cheap direction is enough
+static const int g_precheck = getenv("DP_LS_PRECHECK") ? atoi(getenv("DP_LS_PRECHECK")) : 1;
 static const int g_ls_norm = getenv("DP_LS_NORM") ? atoi(getenv("DP_LS_NORM")) : 0;
 static const double g_eta_plateau = getenv("DP_ETA_PLATEAU") ? atof(getenv("DP_ETA_PLATEAU")) : 0.0;
 static double now_s() {
@@ -503,6 +504,8 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   rc |= dalloc(s, &s->fe, (size_t)std::max(E, 1) * NV * 3);
   rc |= dalloc(s, &s->H, (size_t)std::max(E, 1) * NP * kHBlk);
   rc |= dalloc(s, &s->Pst, (size_t)std::max(E, 1) * 27);
+  rc |= dalloc(s, &s->watch_v, kWatchMax);
+  rc |= dalloc(s, &s->watch_e, kWatchElemMax);
   rc |= dalloc(s, &s->d_colliders, 1);
   rc |= dalloc(s, &s->fext, (size_t)V * 3);
   rc |= dalloc(s, &s->c_count, V + 1);
@@ -565,7 +568,7 @@ int dp_scene_destroy(dp_scene* s) {
   mg_destroy(s);
   void* ptrs[] = {s->ev, s->B, s->w, s->vol, s->mu, s->lam, s->model, s->mass, s->inc_ptr, s->inc,
                   s->slice_base, s->slice_width, s->col, s->diag_slot, s->val_fwd, s->val_adj, s->val_A,
-                  s->contrib_ptr, s->contrib, s->minv, s->fe, s->H, s->Pst, s->d_colliders, s->b_ptr, s->b_idx,
+                  s->contrib_ptr, s->contrib, s->minv, s->fe, s->H, s->Pst, s->watch_v, s->watch_e, s->d_colliders, s->b_ptr, s->b_idx,
                   s->b_target, s->b_comp, s->b_vertex, s->fext, s->c_count, s->c_off, s->c_vertex, s->c_collider,
                   s->c_frame, s->c_dn, s->c_mu, s->c_delta, s->c_blk, s->c_force, s->c_kmu, s->c_kc, s->scan_tmp,
                   s->q, s->q_hat, s->q_bar, s->v_bar, s->r, s->dq, s->q_try, s->rhs, s->z, s->z_prev, s->tmp, s->q_ev, s->r_try, s->kx, s->kr,
@@ -872,6 +875,8 @@ __global__ void k_reset_flags(EvalScalars* esc) {
   esc->status = 0;
   esc->penetrating = 0;
   esc->asym = 0;
+  esc->skip = 0;
+  esc->precheck = 0;
 }
 
 int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32_t ptr_kind,
@@ -969,14 +974,28 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     // line search (forward.py:214-234)
     double t = 1.0;
     bool accepted = false;
+    // watched rows for the line-search pre-check: rows within half of max|r|
+    const bool precheck = g_precheck && s->NV == 4 && s->E > 0;
+    if (precheck) launch_watch_select(s, s->r, 0.5);
     for (int ls = 0; ls < cfg.max_line_search; ++ls) {
       launch_axpy_to(s, q_try, q, t, s->dq);
       k_reset_flags<<<1, 1, 0, s->stream>>>(s->esc);
       launch_penetration(s, q_try, s->esc);
       // forward.py:218-219: a penetrating trial is not evaluated; the kernels
-      // read the penetration flag on the device and exit (no extra sync)
-      s->eval_skip = &s->esc->penetrating;
-      evaluate(s, q_try, s->r_try, 0);
+      // read the skip flag on the device and exit (no extra sync).  The
+      // pre-check (watched rows) sets the same flag when the trial cannot
+      // be accepted.
+      s->eval_skip = &s->esc->skip;
+      if (precheck) {
+        launch_watch_elements(s, q_try);
+        launch_contacts(s, q_try, s->q_bar, -1, s->c_vertex, s->c_frame, s->c_dn, s->c_mu, s->c_delta, 0, 0, s->esc);
+        launch_watch_check(s, q_try, E.rmax);
+        launch_elements(s, q_try, 0, &s->esc->status);
+        launch_residual(s, q_try, s->q_hat, s->r_try, s->esc);
+        s->launches += 2;
+      } else {
+        evaluate(s, q_try, s->r_try, 0);
+      }
       s->eval_skip = nullptr;
       s->launches++;
       R.line_search_trials++;
@@ -985,7 +1004,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
       if (g_debug > 1)
         fprintf(stderr, "[dp]   ls=%d t=%.3e pen=%d st=%d rmax_try=%.6e (rmax=%.6e)\n", ls, t, T.penetrating, T.status,
                 T.rmax, E.rmax);
-      if (!T.penetrating) {
+      if (!T.skip) {
         const int st = T.status;
         const bool value_error = (st & (ST_INVERTED | ST_NONFINITE | ST_PENETRATION)) != 0;
         if (!value_error && (st & ST_NH_STALL)) return raise_status(ST_NH_STALL);

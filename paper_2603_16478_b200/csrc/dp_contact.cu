@@ -96,7 +96,7 @@ __global__ void k_penetration(int V, const ColliderSet* __restrict__ csp, const 
   const double x[3] = {q[3 * v], q[3 * v + 1], q[3 * v + 2]};
   for (int j = 0; j < cs.n; ++j) {
     double n[3];
-    if (gap_normal(cs, j, x, n) <= 0.0) { esc->penetrating = 1; return; }
+    if (gap_normal(cs, j, x, n) <= 0.0) { esc->penetrating = 1; esc->skip = 1; return; }
   }
 }
 

@@ -26,7 +26,13 @@ struct EvalScalars {
   int penetrating;      // any gap <= 0 (forward.py:86-93)
   int n_contacts;
   int asym;             // any active contact with mu != 0
+  int skip;             // line-search trial needs no full evaluation (penetrating or pre-check rejected)
+  int precheck;         // pre-check rejected the trial (a watched row already >= max|r|)
+  int n_watch;          // watched rows (pre-check), capped at kWatchMax
+  int n_watch_elem;     // element entries of the watched rows, capped at kWatchElemMax
 };
+constexpr int kWatchMax = 256;
+constexpr int kWatchElemMax = 256 * 32;
 
 // Krylov scalars (device resident; the host only polls `done`).
 struct KrylovScalars {
@@ -188,6 +194,8 @@ struct dp_scene {
   double *q = nullptr, *q_hat = nullptr, *q_bar = nullptr, *v_bar = nullptr, *r = nullptr, *dq = nullptr;
   double *q_try = nullptr, *rhs = nullptr, *z = nullptr, *tmp = nullptr, *q_ev = nullptr, *r_try = nullptr;
   const int* eval_skip = nullptr;   // device flag: element/contact/residual kernels exit when set (penetrating trial)
+  int* watch_v = nullptr;           // line-search pre-check: watched rows and the elements incident to them
+  int* watch_e = nullptr;
   double* z_prev = nullptr;   // last adjoint solution of the current reverse sweep (warm start)
   int z_prev_valid = 0;
   int adj_warm = 1;
@@ -247,10 +255,14 @@ int grid_for(int64_t n, int threads);
 // launchers (dp_kernels.cu) -----------------------------------------------
 // element evaluation: mode bit 1 = jacobian blocks, bit 2 = store P/dP for
 // backprop, bit 4 = zero jacobian (A-matrix assembly).
-enum { EV_JAC = 1, EV_STOREP = 2, EV_AMAT = 4 };
+enum { EV_JAC = 1, EV_STOREP = 2, EV_AMAT = 4, EV_LIST = 8 };
 void launch_elements(dp_scene* s, const double* q, int mode, int* status);
 // residual gather r = M(q - q_hat) + sum_e f_e - h^2 J_b^T lam_b + contact forces; max|r| into esc
 void launch_residual(dp_scene* s, const double* q, const double* q_hat, double* r, dp::EvalScalars* esc);
+// line-search pre-check (dp_kernels.cu)
+void launch_watch_select(dp_scene* s, const double* r, double frac);
+void launch_watch_elements(dp_scene* s, const double* q);
+void launch_watch_check(dp_scene* s, const double* q, double rmax_prev);
 // BSR gather: val = M + sum_e H_e + K_b + (K_c or K_c^T); plus block-Jacobi inverses
 void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat);
 void launch_spmv(dp_scene* s, const double* val, const double* x, double* y);

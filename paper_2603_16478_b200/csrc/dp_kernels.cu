@@ -183,12 +183,18 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
                const double* __restrict__ mu, const double* __restrict__ lam, const int* __restrict__ model, int E,
                const double* __restrict__ q, double h2, double tau_rel, double* __restrict__ fe,
                double* __restrict__ H, double* __restrict__ Pst, int* __restrict__ status,
-               const int* __restrict__ skip) {
+               const int* __restrict__ skip, const int* __restrict__ list, const int* __restrict__ list_n) {
   constexpr int mode = MODE;
-  if (skip && *(volatile const int*)skip) return;   // penetrating line-search trial: no evaluation
+  if (skip && *(volatile const int*)skip) return;   // line-search trial needing no evaluation
   constexpr int D = NV - 1;
   constexpr int NP = NV * (NV + 1) / 2;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (mode & EV_LIST) {
+    // an element subset (line-search pre-check): same arithmetic as the full pass
+    if (e >= min(*list_n, kWatchElemMax)) return;
+    e = list[e];
+    if (e < 0) return;
+  }
   if (e >= E) return;
   const int4 vv = ev[e];
   const int vid[4] = {vv.x, vv.y, vv.z, vv.w};
@@ -417,7 +423,7 @@ static void launch_elements_nv(dp_scene* s, const double* q, int mode, int* stat
 #define DP_ELEM_CASE(M)                                                                                       \
   case M:                                                                                                     \
     k_elements<NV, M><<<nb, nt, 0, s->stream>>>(s->ev, s->B, s->w, s->mu, s->lam, s->model, s->E, q, h2, 1e-6, \
-                                                s->fe, s->H, s->Pst, status, s->eval_skip);                   \
+                                                s->fe, s->H, s->Pst, status, s->eval_skip, nullptr, nullptr); \
     break;
   switch (mode) {
     DP_ELEM_CASE(0)
@@ -447,24 +453,22 @@ void launch_elements(dp_scene* s, const double* q, int mode, int* status) {
 
 constexpr int kVT = 256;
 
-__global__ void __launch_bounds__(kVT) k_residual(int V, const double* __restrict__ mass, const double* __restrict__ q,
-                                                  const double* __restrict__ q_hat, const int* __restrict__ inc_ptr,
-                                                  const int* __restrict__ inc, const double* __restrict__ fe,
-                                                  const int* __restrict__ b_ptr, const int* __restrict__ b_idx,
-                                                  const double* __restrict__ b_target, const double* __restrict__ b_comp,
-                                                  const int* __restrict__ c_count, const int* __restrict__ c_off,
-                                                  const double* __restrict__ c_force, int has_contacts, double h2,
-                                                  double* __restrict__ r, double* partial, unsigned int* counter,
-                                                  EvalScalars* esc, const int* __restrict__ skip) {
-  __shared__ double sh[32];
-  if (skip && *(volatile const int*)skip) return;
-  const int i = blockIdx.x * kVT + threadIdx.x;
-  double amax = 0.0, sq = 0.0;
-  if (i < V) {
+// one row of the momentum residual (momentum_residual, forward.py:101-110):
+// M (q - q_hat) + element contributions (incidence order, 4 loads in flight)
+// + bindings + contact forces; shared by the full residual and the
+// line-search pre-check so both produce the same bits
+__device__ __forceinline__ void residual_row(int i, const double* __restrict__ mass, const double* __restrict__ q,
+                                             const double* __restrict__ q_hat, const int* __restrict__ inc_ptr,
+                                             const int* __restrict__ inc, const double* __restrict__ fe,
+                                             const int* __restrict__ b_ptr, const int* __restrict__ b_idx,
+                                             const double* __restrict__ b_target, const double* __restrict__ b_comp,
+                                             const int* __restrict__ c_count, const int* __restrict__ c_off,
+                                             const double* __restrict__ c_force, int has_contacts, double h2,
+                                             double& r0, double& r1, double& r2) {
     const double m = mass[i];
-    double r0 = m * (q[3 * i] - q_hat[3 * i]);
-    double r1 = m * (q[3 * i + 1] - q_hat[3 * i + 1]);
-    double r2 = m * (q[3 * i + 2] - q_hat[3 * i + 2]);
+    r0 = m * (q[3 * i] - q_hat[3 * i]);
+    r1 = m * (q[3 * i + 1] - q_hat[3 * i + 1]);
+    r2 = m * (q[3 * i + 2] - q_hat[3 * i + 2]);
     // element contributions in groups of 4 (all loads of a group in flight
     // before the in-order accumulation)
     int k = inc_ptr[i];
@@ -501,6 +505,25 @@ __global__ void __launch_bounds__(kVT) k_residual(int V, const double* __restric
         r0 += c_force[3 * c]; r1 += c_force[3 * c + 1]; r2 += c_force[3 * c + 2];
       }
     }
+}
+
+__global__ void __launch_bounds__(kVT) k_residual(int V, const double* __restrict__ mass, const double* __restrict__ q,
+                                                  const double* __restrict__ q_hat, const int* __restrict__ inc_ptr,
+                                                  const int* __restrict__ inc, const double* __restrict__ fe,
+                                                  const int* __restrict__ b_ptr, const int* __restrict__ b_idx,
+                                                  const double* __restrict__ b_target, const double* __restrict__ b_comp,
+                                                  const int* __restrict__ c_count, const int* __restrict__ c_off,
+                                                  const double* __restrict__ c_force, int has_contacts, double h2,
+                                                  double* __restrict__ r, double* partial, unsigned int* counter,
+                                                  EvalScalars* esc, const int* __restrict__ skip) {
+  __shared__ double sh[32];
+  if (skip && *(volatile const int*)skip) return;
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  double amax = 0.0, sq = 0.0;
+  if (i < V) {
+    double r0, r1, r2;
+    residual_row(i, mass, q, q_hat, inc_ptr, inc, fe, b_ptr, b_idx, b_target, b_comp, c_count, c_off, c_force,
+                 has_contacts, h2, r0, r1, r2);
     r[3 * i] = r0; r[3 * i + 1] = r1; r[3 * i + 2] = r2;
     amax = fmax(fabs(r0), fmax(fabs(r1), fabs(r2)));
     if (!(amax == amax)) amax = INFINITY;   // NaN propagates as +inf
@@ -528,6 +551,88 @@ void launch_residual(dp_scene* s, const double* q, const double* q_hat, double* 
   k_residual<<<nb, kVT, 0, s->stream>>>(s->V, s->mass, q, q_hat, s->inc_ptr, s->inc, s->fe, s->nb ? s->b_ptr : nullptr,
                                         s->b_idx, s->b_target, s->b_comp, s->c_count, s->c_off, s->c_force, has_c,
                                         s->h * s->h, r, s->red.partial, s->red.counter, esc, s->eval_skip);
+  s->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// line-search pre-check (forward.py:214-234 accepts a trial iff max|r_try| <
+// max|r| and nothing is inverted/penetrating).  Rows that were large at the
+// Newton evaluation are watched; before a trial's full evaluation, the
+// elements incident to them are evaluated (same k_elements code) and their
+// rows summed (same residual_row); if one of them already reaches max|r|
+// the full evaluation could only confirm the rejection, so it is skipped.
+// Accept/reject decisions are identical to always evaluating fully; a
+// watched NH stall leaves the decision to the full evaluation (which raises,
+// as the reference does).
+
+__global__ void k_watch_select(int V, int NV, const double* __restrict__ r, const int* __restrict__ inc_ptr,
+                               const int* __restrict__ inc, double frac, int* __restrict__ watch_v,
+                               int* __restrict__ watch_e, EvalScalars* esc) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const double a = fmax(fabs(r[3 * v]), fmax(fabs(r[3 * v + 1]), fabs(r[3 * v + 2])));
+  if (!(a >= frac * esc->rmax)) return;
+  const int k0 = inc_ptr[v], deg = inc_ptr[v + 1] - k0;
+  const int slot = atomicAdd(&esc->n_watch, 1);
+  if (slot >= kWatchMax) return;
+  // the row is checked only if all its elements fit in the element list
+  const int base = atomicAdd(&esc->n_watch_elem, deg);
+  if (base + deg > kWatchElemMax) {
+    watch_v[slot] = -1;
+    for (int k = base; k < kWatchElemMax; ++k) watch_e[k] = -1;
+    return;
+  }
+  for (int k = 0; k < deg; ++k) watch_e[base + k] = inc[k0 + k] / NV;
+  watch_v[slot] = v;
+}
+
+__global__ void k_watch_check(const int* __restrict__ watch_v, const double* __restrict__ mass,
+                              const double* __restrict__ q, const double* __restrict__ q_hat,
+                              const int* __restrict__ inc_ptr, const int* __restrict__ inc,
+                              const double* __restrict__ fe, const int* __restrict__ b_ptr,
+                              const int* __restrict__ b_idx, const double* __restrict__ b_target,
+                              const double* __restrict__ b_comp, const int* __restrict__ c_count,
+                              const int* __restrict__ c_off, const double* __restrict__ c_force, int has_contacts,
+                              double h2, double rmax_prev, EvalScalars* esc) {
+  if (*(volatile const int*)&esc->skip) return;
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= min(esc->n_watch, kWatchMax)) return;
+  // a watched element that stalled in its NH projection: let the full
+  // evaluation run (and raise)
+  if (*(volatile const int*)&esc->status & ST_NH_STALL) return;
+  const int v = watch_v[w];
+  if (v < 0) return;
+  double r0, r1, r2;
+  residual_row(v, mass, q, q_hat, inc_ptr, inc, fe, b_ptr, b_idx, b_target, b_comp, c_count, c_off, c_force,
+               has_contacts, h2, r0, r1, r2);
+  const double a = fmax(fabs(r0), fmax(fabs(r1), fabs(r2)));
+  if (!(a < rmax_prev)) {   // >= or NaN: max|r_try| cannot drop below max|r|
+    esc->precheck = 1;
+    esc->skip = 1;
+  }
+}
+
+void launch_watch_select(dp_scene* s, const double* r, double frac) {
+  cudaMemsetAsync(&s->esc->n_watch, 0, 2 * sizeof(int), s->stream);
+  k_watch_select<<<grid_for(s->V, 256), 256, 0, s->stream>>>(s->V, s->NV, r, s->inc_ptr, s->inc, frac, s->watch_v,
+                                                             s->watch_e, s->esc);
+  s->launches++;
+}
+
+void launch_watch_elements(dp_scene* s, const double* q) {
+  if (s->E == 0 || s->NV != 4) return;
+  const double h2 = s->h * s->h;
+  k_elements<4, EV_LIST><<<grid_for(kWatchElemMax, 128), 128, 0, s->stream>>>(
+      s->ev, s->B, s->w, s->mu, s->lam, s->model, s->E, q, h2, 1e-6, s->fe, s->H, s->Pst, &s->esc->status,
+      &s->esc->skip, s->watch_e, &s->esc->n_watch_elem);
+  s->launches++;
+}
+
+void launch_watch_check(dp_scene* s, const double* q, double rmax_prev) {
+  const int has_c = s->colliders.n > 0;
+  k_watch_check<<<grid_for(kWatchMax, 128), 128, 0, s->stream>>>(
+      s->watch_v, s->mass, q, s->q_hat, s->inc_ptr, s->inc, s->fe, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_target,
+      s->b_comp, s->c_count, s->c_off, s->c_force, has_c, s->h * s->h, rmax_prev, s->esc);
   s->launches++;
 }
 

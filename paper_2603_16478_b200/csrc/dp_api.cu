@@ -163,6 +163,7 @@ static const int g_debug = getenv("DP_DEBUG") ? atoi(getenv("DP_DEBUG")) : 0;
 // after a line search that had to cut the step below 1/16 the Newton model is
 // poor (friction-cone / activation kinks): a cheap direction is enough
 static const int g_precheck = getenv("DP_LS_PRECHECK") ? atoi(getenv("DP_LS_PRECHECK")) : 1;
+static const double g_watch_frac = getenv("DP_LS_WATCH_FRAC") ? atof(getenv("DP_LS_WATCH_FRAC")) : 0.5;
 static const int g_ls_norm = getenv("DP_LS_NORM") ? atoi(getenv("DP_LS_NORM")) : 0;
 static const double g_eta_plateau = getenv("DP_ETA_PLATEAU") ? atof(getenv("DP_ETA_PLATEAU")) : 0.0;
 static double now_s() {
@@ -976,7 +977,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     bool accepted = false;
     // watched rows for the line-search pre-check: rows within half of max|r|
     const bool precheck = g_precheck && s->NV == 4 && s->E > 0;
-    if (precheck) launch_watch_select(s, s->r, 0.5);
+    if (precheck) launch_watch_select(s, s->r, g_watch_frac);
     for (int ls = 0; ls < cfg.max_line_search; ++ls) {
       launch_axpy_to(s, q_try, q, t, s->dq);
       k_reset_flags<<<1, 1, 0, s->stream>>>(s->esc);

@@ -917,10 +917,17 @@ class Grads:
     dL_dnu: float = 0.0
 
 
-def adjoint_solve(sc, A, els, st, rhs, tol=1e-10, max_iter=2000, restart=50):
-    """assemble_adjoint_operator + solve_adjoint (adjoint.py:93-139)."""
+def adjoint_solve(sc, A, els, st, rhs, tol=1e-10, max_iter=2000, restart=50, direct=False):
+    """assemble_adjoint_operator + solve_adjoint (adjoint.py:93-139).
+
+    direct=True (test infrastructure): solve A_hat^T z = rhs with SuperLU
+    instead of the reference's Jacobi-preconditioned Krylov method, for
+    operators where that method does not reach its tolerance (compressed
+    cloth) - the solution, not the solver, is the parity target."""
     Ah = newton_matrix(sc, A, els, st.es, st.contacts)
     AhT = sp.csr_matrix(Ah.T)
+    if direct:
+        return spla.spsolve(sp.csc_matrix(AhT), rhs)
     d = Ah.diagonal()
     if np.any(np.abs(d) < 1e-300):
         raise ValueError("jacobi preconditioner requires nonzero diagonal")
@@ -986,7 +993,7 @@ def backprop_step(sc, els, st, z, dL_dv, g):
 
 
 def backprop_rollout(sc, els, A, steps, target=None, loss_fn=None,
-                     tol=1e-10):
+                     tol=1e-10, direct=False):
     """backprop_rollout (adjoint.py:228-271) for a final-state loss
     (adjoint.py:222-225) or a callable loss."""
     n = sc.ndof
@@ -1009,7 +1016,7 @@ def backprop_rollout(sc, els, A, steps, target=None, loss_fn=None,
             gq, gv = np.zeros(n), np.zeros(n)
         dq = dq + gq
         dv = dv + gv
-        z = adjoint_solve(sc, A, els, st, dq + dv / sc.h, tol=tol)
+        z = adjoint_solve(sc, A, els, st, dq + dv / sc.h, tol=tol, direct=direct)
         g.dL_dfext = []
         g, dq, dv = backprop_step(sc, els, st, z, dv, g)
         fx.append(g.dL_dfext[0])

@@ -341,3 +341,47 @@ def test_adjoint_nonconvergence_raises(pkg):
     ws = aj.assemble_adjoint_operator(caches[-1])
     with pytest.raises(RuntimeError, match="did not converge"):
         aj.solve_adjoint(ws, np.ones(scene.ndof), np.zeros(scene.ndof), solver_cfg=bad)
+
+
+def test_cloth_drape_vs_oracle(pkg):
+    """C2 family at 20x20 (800 ARAP triangles, 0.3 kg/m^2) draping onto a
+    frictional sphere above a frictional ground: states, contact sets and
+    the per-step control-force gradients dL/dfext_k against the oracle."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import diffproj_oracle as O
+    from paper_2603_16478_b200 import adjoint as aj, core, forward as fw
+    bench.CONFIGS["c2_test"] = dict(bench.CONFIGS["c2"], cells=(20, 20, 0), edge=1.0 / 20)
+    scene = bench.make_scene("c2_test")
+    sm = core.assemble_system_matrix(scene)
+    osc = O.OScene(core.scene_to_arrays(scene))
+    els = O.build_elements(osc)
+    A = O.assemble_A(osc, els)
+    st = scene.rest_state()
+    q, v = st.q.copy(), st.v.copy()
+    caches, steps = [], []
+    n_contacts = 0
+    for k in range(4):
+        st, rep = fw.forward_step(scene, st, sm, fw.ForwardConfig(tol=1e-11))
+        assert rep.converged
+        o = O.forward_step(osc, A, els, q, v, O.ForwardConfig(tol=1e-11))
+        assert o.converged
+        assert np.max(np.abs(st.q - o.q_new)) <= 1e-8 * np.max(np.abs(o.q_new))
+        assert np.array_equal([cp.vertex for cp in rep.cache.contacts], o.contacts.vertex)
+        n_contacts += len(o.contacts.vertex)
+        q, v = o.q_new, o.v_new
+        caches.append(rep.cache)
+        steps.append(o)
+    assert n_contacts > 0
+    target = st.q + 1e-3
+    g = aj.backprop_rollout(caches, target)
+    # the reference's Jacobi-GMRES adjoint does not reach 1e-10 on this
+    # operator (it raises); the oracle solves it directly
+    og = O.backprop_rollout(osc, els, A, steps, target=target, direct=True)
+    rel = lambda a, b: np.max(np.abs(np.asarray(a) - np.asarray(b))) / np.max(np.abs(np.asarray(b)))
+    assert rel(g.dL_dqbar, og.dL_dqbar) < 1e-6
+    for k in range(4):
+        assert rel(g.dL_dfext[k], og.dL_dfext[k]) < 1e-6
+    assert abs(g.dL_dstiffness - og.dL_dstiffness) <= 1e-6 * abs(og.dL_dstiffness)

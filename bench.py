@@ -415,11 +415,15 @@ def gpu_arm(args, rank, world, local_rank):
     n_w = 0
     while n_w < max(W, 0) or time.perf_counter() - t_w < args.warmup_seconds:
         res = run_all(device_rollout, K, W)
-        # the timed region's gradient packing and all-reduce run here too, so
-        # their device allocations come from torch's cache, not a cudaMalloc
-        # inside the timed region (measured: 60-80 ms stalls on a fresh box)
-        allreduce_gradients(pack_sum([(r[0], r[1]) for r in res]), world)
+        # the timed region's gradient packing runs here too, so its device
+        # allocation comes from torch's cache, not a cudaMalloc inside the
+        # timed region (measured: 60-80 ms stalls on a fresh box)
+        gw = pack_sum([(r[0], r[1]) for r in res])
         n_w += 1
+    # one all-reduce on every rank (the time-based warm-up count differs
+    # between ranks; collectives must pair up): initialises NCCL and warms
+    # its buffers before the timed region
+    allreduce_gradients(gw, world)
     torch.cuda.synchronize()
     if os.environ.get("BENCH_DEBUG"):
         for i in range(int(os.environ.get("BENCH_DEBUG_REPS", "3"))):

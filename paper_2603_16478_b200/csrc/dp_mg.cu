@@ -539,6 +539,31 @@ __global__ void k_mg_restrict(int nc, const int* __restrict__ mptr, const int* _
   if (lane == 0) { bc[3 * I] = s0; bc[3 * I + 1] = s1; bc[3 * I + 2] = s2; }
 }
 
+// k_mg_restrict followed by k_mg_jacobi0 of the coarse level in one launch:
+// b_c[I] = sum over members of r_f, x_c[I] = omega Minv_c b_c[I] (the same
+// sums and the same products as the two kernels, bitwise identical)
+template <class TM>
+__global__ void k_mg_restrict_j0(int nc, const int* __restrict__ mptr, const int* __restrict__ mem,
+                                 const double* __restrict__ rf, double* __restrict__ bc, const TM* __restrict__ minv,
+                                 double omega, double* __restrict__ xc, const int* stop) {
+  if (stopped(stop)) return;
+  const int I = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (I >= nc) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int t = mptr[I] + lane; t < mptr[I + 1]; t += 32) {
+    const int i = mem[t];
+    s0 += rf[3 * i]; s1 += rf[3 * i + 1]; s2 += rf[3 * i + 2];
+  }
+  s0 = warp_sum(s0); s1 = warp_sum(s1); s2 = warp_sum(s2);
+  if (lane == 0) {
+    bc[3 * I] = s0; bc[3 * I + 1] = s1; bc[3 * I + 2] = s2;
+    const double r[3] = {s0, s1, s2};
+    double u[3];
+    mv_minv(minv, nc, I, r, u);
+    xc[3 * I] = omega * u[0]; xc[3 * I + 1] = omega * u[1]; xc[3 * I + 2] = omega * u[2];
+  }
+}
+
 // coarsest: scatter SELL blocks into a dense N x N row-major matrix
 __global__ void k_mg_dense_build(int n, int S, const int* __restrict__ slice_base, const int* __restrict__ slice_width,
                                  const int* __restrict__ col, const double* __restrict__ val, double* __restrict__ A) {
@@ -628,13 +653,28 @@ __global__ void __launch_bounds__(256) k_mg_dense_invert(int N, const double* __
 __global__ void __launch_bounds__(256) k_mg_coarse_jacobi(int n, int S, const int* __restrict__ slice_base,
                                                           const int* __restrict__ slice_width,
                                                           const int* __restrict__ col, const double* __restrict__ val,
-                                                          const double* __restrict__ minv, const double* __restrict__ b,
+                                                          const double* __restrict__ minv, double* b,
                                                           double* __restrict__ x, double* __restrict__ y, double omega,
-                                                          int nsweep, const int* stop) {
+                                                          int nsweep, const int* stop, const int* __restrict__ mptr,
+                                                          const int* __restrict__ mem, const double* __restrict__ rf) {
   // one CTA; warp w handles slots k = w, w+8, ... of every slice, lanes = rows
   __shared__ double part[8][3][kSlice];
   if (stop && *(volatile const int*)stop) return;
   const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
+  if (rf) {
+    // the restriction b = R rf of k_mg_restrict (one warp per coarse row, same
+    // order), done here instead of in a launch of its own
+    for (int I = wsub; I < n; I += 8) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int t = mptr[I] + lane; t < mptr[I + 1]; t += 32) {
+        const int i = mem[t];
+        s0 += rf[3 * i]; s1 += rf[3 * i + 1]; s2 += rf[3 * i + 2];
+      }
+      s0 = warp_sum(s0); s1 = warp_sum(s1); s2 = warp_sum(s2);
+      if (lane == 0) { b[3 * I] = s0; b[3 * I + 1] = s1; b[3 * I + 2] = s2; }
+    }
+    __syncthreads();
+  }
   for (int row = threadIdx.x; row < n; row += blockDim.x) {
     double r[3] = {b[3 * row], b[3 * row + 1], b[3 * row + 2]}, u[3];
     mv_minv(minv, n, row, r, u);
@@ -963,7 +1003,8 @@ static void jacobi0(dp_scene* s, const MGLevel& L, const TV* minv, const double*
 
 template <class TV>
 static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, const double* b, double* x,
-                         const int* stop);
+                         const int* stop, bool pre_done = false);
+static const int g_mg_rj0 = getenv("DP_MG_RJ0") ? atoi(getenv("DP_MG_RJ0")) : 1;
 
 static const int g_mg_fused_env = getenv("DP_MG_FUSED") ? atoi(getenv("DP_MG_FUSED")) : 0;
 
@@ -1024,7 +1065,8 @@ static void vcycle(dp_scene* s, int l, const double* b, double* x, const int* st
     if (mg->coarse_sweeps > 0) {
       const MGLevel& Lc = mg->lv[l];
       k_mg_coarse_jacobi<<<1, 256, 0, s->stream>>>(Lc.n, Lc.S, Lc.slice_base, Lc.slice_width, Lc.col, Lc.val, Lc.minv,
-                                                   b, x, Lc.t, mg->omega, mg->coarse_sweeps, stop);
+                                                   const_cast<double*>(b), x, Lc.t, mg->omega, mg->coarse_sweeps, stop,
+                                                   nullptr, nullptr, nullptr);
     } else {
       k_mg_dense_solve<<<grid_for((int64_t)mg->N * 32, 256), 256, 0, s->stream>>>(mg->N, mg->dinv, b, x, stop);
     }
@@ -1037,7 +1079,7 @@ static void vcycle(dp_scene* s, int l, const double* b, double* x, const int* st
 
 template <class TV>
 static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, const double* b, double* x,
-                         const int* stop) {
+                         const int* stop, bool pre_done) {
   MG* mg = s->mg;
   MGLevel& L = mg->lv[l];
   MGLevel& C = mg->lv[l + 1];
@@ -1047,7 +1089,7 @@ static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, cons
   double* xb = L.u;
   // the fine-level first sweep from zero may already be done by the caller
   // (k_gm_prec fuses it into the basis-vector pass): mg_apply(..., prejac)
-  if (!(l == 0 && mg->prejac)) jacobi0<TV>(s, L, minv, b, om, xa, stop);
+  if (!pre_done && !(l == 0 && mg->prejac)) jacobi0<TV>(s, L, minv, b, om, xa, stop);
   for (int it = 1; it < mg->nu; ++it) {
     smooth<TV>(s, L, val, minv, b, xa, nullptr, nullptr, om, xb, nullptr, stop, 1.0);
     std::swap(xa, xb);
@@ -1059,6 +1101,17 @@ static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, cons
     smooth<TV>(s, L, val, minv, b, xa, nullptr, nullptr, om, nullptr, L.r, stop, 1.0);
     if (l == 0 && fused_usable(mg)) {
       launch_coarse_fused(s, L.r, stop);   // restriction to level 1 is its first phase
+    } else if (g_mg_rj0 && l + 1 == (int)mg->lv.size() - 1 && mg->coarse_sweeps > 0) {
+      // coarsest level: the restriction is the first phase of its one-CTA solve
+      k_mg_coarse_jacobi<<<1, 256, 0, s->stream>>>(C.n, C.S, C.slice_base, C.slice_width, C.col, C.val, C.minv, C.b,
+                                                   C.x, C.t, om, mg->coarse_sweeps, stop, C.mem_ptr, C.mem, L.r);
+      s->launches++;
+    } else if (g_mg_rj0 && l + 1 < (int)mg->lv.size() - 1) {
+      // restriction and the coarse level's first Jacobi sweep from zero in one launch
+      k_mg_restrict_j0<double><<<grid_for((int64_t)C.n * 32, 256), 256, 0, s->stream>>>(
+          C.n, C.mem_ptr, C.mem, L.r, C.b, C.minv, om, C.t, stop);
+      s->launches++;
+      vcycle_level<double>(s, l + 1, C.val, C.minv, C.b, C.x, stop, true);
     } else {
       k_mg_restrict<<<grid_for((int64_t)C.n * 32, 256), 256, 0, s->stream>>>(C.n, C.mem_ptr, C.mem, L.r, C.b, stop);
       s->launches++;

@@ -444,13 +444,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
       if (colidx[k] == i) diag_slot[i] = (int)slot;
     }
   }
-  // ---- contribution lists per slot: element e, local (a,b) -> H[e][pair] (transposed if a > b)
-  std::vector<int> pair_id(NV * NV);
-  {
-    int p = 0;
-    for (int a = 0; a < NV; ++a)
-      for (int b = a; b < NV; ++b, ++p) { pair_id[a * NV + b] = p; pair_id[b * NV + a] = p; }
-  }
+  // ---- contribution lists per slot: element e, local (a,b) -> one block of the stream H
   std::vector<int> cptr(NS + 1, 0);
   std::vector<int64_t> eslot((size_t)E * NV * NV);
   for (int e = 0; e < E; ++e) {
@@ -469,15 +463,16 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
     }
   }
   for (int64_t t = 0; t < NS; ++t) cptr[t + 1] += cptr[t];
-  std::vector<int> contrib(cptr[NS]);
+  // block-stream position of every (element, a, b): the fill order of the
+  // slot lists (element-ascending within a slot, as the reference's COO sum)
+  std::vector<int> epos((size_t)E * NV * NV);
   {
     std::vector<int> fill(cptr.begin(), cptr.end() - 1);
     for (int e = 0; e < E; ++e)
       for (int a = 0; a < NV; ++a)
         for (int b = 0; b < NV; ++b) {
-          const int64_t slot = eslot[((size_t)e * NV + a) * NV + b];
-          const int id = e * NP + pair_id[a * NV + b];
-          contrib[fill[slot]++] = (a <= b) ? id : ~id;
+          const size_t ab = ((size_t)e * NV + a) * NV + b;
+          epos[ab] = fill[eslot[ab]]++;
         }
   }
 
@@ -498,12 +493,13 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   rc |= upload(s, &s->col, col);
   rc |= upload(s, &s->diag_slot, diag_slot);
   rc |= upload(s, &s->contrib_ptr, cptr);
-  rc |= upload(s, &s->contrib, contrib);
+  rc |= upload(s, &s->epos, epos);
   rc |= dalloc(s, &s->val_fwd, (size_t)NS * 9);
   rc |= dalloc(s, &s->val_adj, (size_t)NS * 9);
   rc |= dalloc(s, &s->minv, (size_t)V * 9);
   rc |= dalloc(s, &s->fe, (size_t)std::max(E, 1) * NV * 3);
-  rc |= dalloc(s, &s->H, (size_t)std::max(E, 1) * NP * kHBlk);
+  rc |= dalloc(s, &s->H, (size_t)std::max(cptr[NS], 1) * kHS);
+  rc |= dalloc(s, &s->Ht, (size_t)std::max(cptr[NS], 1));
   rc |= dalloc(s, &s->Pst, (size_t)std::max(E, 1) * 27);
   rc |= dalloc(s, &s->watch_v, kWatchMax);
   rc |= dalloc(s, &s->watch_e, kWatchElemMax);
@@ -569,7 +565,7 @@ int dp_scene_destroy(dp_scene* s) {
   mg_destroy(s);
   void* ptrs[] = {s->ev, s->B, s->w, s->vol, s->mu, s->lam, s->model, s->mass, s->inc_ptr, s->inc,
                   s->slice_base, s->slice_width, s->col, s->diag_slot, s->val_fwd, s->val_adj, s->val_A,
-                  s->contrib_ptr, s->contrib, s->minv, s->fe, s->H, s->Pst, s->watch_v, s->watch_e, s->d_colliders, s->b_ptr, s->b_idx,
+                  s->contrib_ptr, s->epos, s->minv, s->fe, s->H, s->Ht, s->Pst, s->watch_v, s->watch_e, s->d_colliders, s->b_ptr, s->b_idx,
                   s->b_target, s->b_comp, s->b_vertex, s->fext, s->c_count, s->c_off, s->c_vertex, s->c_collider,
                   s->c_frame, s->c_dn, s->c_mu, s->c_delta, s->c_blk, s->c_force, s->c_kmu, s->c_kc, s->scan_tmp,
                   s->q, s->q_hat, s->q_bar, s->v_bar, s->r, s->dq, s->q_try, s->rhs, s->z, s->z_prev, s->tmp, s->q_ev, s->r_try, s->kx, s->kr,

@@ -53,10 +53,11 @@ struct KrylovScalars {
 #endif
 constexpr int kVal32PerSlot = DP_VAL32_PACKED ? 12 : 9;
 
-// element Hessian blocks: 9 doubles padded to 10 (80 B, 16-byte aligned):
-// five 16-byte stores per block in the element kernel, and every block read by
-// the assembly gather covers exactly three 32-byte sectors
-constexpr int kHBlk = 10;
+// element Hessian blocks in the slot-ordered stream: the first 8 doubles of
+// a block in H (64 B, 32-byte aligned: two full sectors), the 9th in Ht,
+// one per (element, a, b) contribution incl. the transposed a > b copies, laid
+// out in the SELL slots' contribution-list order so the assembly streams them
+constexpr int kHS = 8;
 
 constexpr int kMaxRestart = 200;
 struct GmresScalars {
@@ -159,7 +160,8 @@ struct dp_scene {
   double* val_fwd = nullptr;       // forward Newton matrix
   double* val_adj = nullptr;       // adjoint operator (transposed contact blocks)
   double* val_A = nullptr;         // constant A (lazy, export only)
-  int *contrib_ptr = nullptr, *contrib = nullptr;
+  int* contrib_ptr = nullptr;      // slot -> run [ptr[slot], ptr[slot+1]) of the block stream H
+  int* epos = nullptr;             // E*NV*NV: (element, a, b) -> position in the block stream
   double* minv = nullptr;          // block-Jacobi inverses [9][V]
   float* val32 = nullptr;          // FP32 copy of the last assembled operator (multigrid fine level)
   const double* val32_src = nullptr;   // operator val32 was last written from
@@ -167,7 +169,8 @@ struct dp_scene {
 
   // element outputs
   double* fe = nullptr;            // E*NV*3
-  double* H = nullptr;             // E*NP*9
+  double* H = nullptr;             // block stream, E*NV*NV blocks of kHS doubles (slot order)
+  double* Ht = nullptr;            // 9th double of every block of H
   double* Pst = nullptr;           // E*27 (P, dP/dmu, dP/dlam) for backprop
 
   // colliders / bindings / fext

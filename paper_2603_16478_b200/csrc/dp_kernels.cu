@@ -136,40 +136,47 @@ __device__ __forceinline__ void make_jac(const double U[3][D], const double sig[
 #define ASM_CHUNK 4
 #endif
 
-__device__ __forceinline__ void load_hblock(const double* __restrict__ H, int cid, double src[kHBlk]) {
-  const double2* src2 = reinterpret_cast<const double2*>(H + (size_t)(cid >= 0 ? cid : ~cid) * kHBlk);
-#pragma unroll
-  for (int u = 0; u < kHBlk / 2; ++u) {
-    const double2 d2 = src2[u];
-    src[2 * u] = d2.x;
-    src[2 * u + 1] = d2.y;
-  }
+// h^2 w [(beta_a.beta_b) I - blk] for the element pair (a, b), a <= b, as one
+// 80-byte block (16-byte stores; 9 doubles + pad) written
+// into the slot-ordered block stream: at the pair's position in the (a, b)
+// slot's contribution list and, for a < b, transposed at its position in the
+// (b, a) slot's list (epos, built at setup in contribution-list order).  The
+// assembly then reads every slot's contributions as one contiguous run.
+// 256-bit global accesses (sm_100): one full 32-byte sector per access
+__device__ __forceinline__ void st256(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+__device__ __forceinline__ void ld256(const double* p, double o[4]) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
 }
 
-// b += block (or its transpose for a > b pairs stored as (b, a))
-__device__ __forceinline__ void acc_hblock(double b[9], const double src[kHBlk], bool direct) {
-  if (direct) {
-#pragma unroll
-    for (int c = 0; c < 9; ++c) b[c] += src[c];
-  } else {
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) b[i * 3 + j] += src[j * 3 + i];
-  }
-}
-
-// h^2 w [(beta_a.beta_b) I - blk] as one padded 80-byte block, 16-byte stores
-__device__ __forceinline__ void store_hblock(double* o, double hw, double bb, const double blk[3][3]) {
-  double v[kHBlk];
+// h^2 w [(beta_a.beta_b) I - blk] for the element pair (a, b), a <= b, written
+// into the slot-ordered block stream: at the pair's position t in the (a, b)
+// slot's contribution list and, for a < b, transposed at its position in the
+// (b, a) slot's list (epos, built at setup in contribution-list order).  A
+// block is split into its first 8 doubles, Hs[t] (64 B: two full-sector
+// 256-bit stores), and its last, Ht[t].  The assembly then reads every slot's
+// contributions as one contiguous run of each array.
+template <int NV>
+__device__ __forceinline__ void store_hpair(double* __restrict__ Hs, double* __restrict__ Ht,
+                                            const int* __restrict__ epos, int e, int a, int b, double hw, double bb,
+                                            const double blk[3][3]) {
+  double v[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) v[i * 3 + j] = hw * (((i == j) ? bb : 0.0) - blk[i][j]);
-  v[9] = 0.0;
-  double2* o2 = reinterpret_cast<double2*>(o);
-#pragma unroll
-  for (int t = 0; t < kHBlk / 2; ++t) o2[t] = make_double2(v[2 * t], v[2 * t + 1]);
+  const int* ep = epos + (size_t)e * NV * NV;
+  const int t = __ldg(ep + a * NV + b);
+  st256(Hs + (size_t)t * kHS, v[0], v[1], v[2], v[3]);
+  st256(Hs + (size_t)t * kHS + 4, v[4], v[5], v[6], v[7]);
+  Ht[t] = v[8];
+  if (a != b) {
+    const int tt = __ldg(ep + b * NV + a);
+    st256(Hs + (size_t)tt * kHS, v[0], v[3], v[6], v[1]);
+    st256(Hs + (size_t)tt * kHS + 4, v[4], v[7], v[2], v[5]);
+    Ht[tt] = v[8];
+  }
 }
 
 // One thread per element.  NV = vertices per element (4 tet, 3 tri).  The
@@ -182,8 +189,9 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
     k_elements(const int4* __restrict__ ev, const double* __restrict__ Bm, const double* __restrict__ w,
                const double* __restrict__ mu, const double* __restrict__ lam, const int* __restrict__ model, int E,
                const double* __restrict__ q, double h2, double tau_rel, double* __restrict__ fe,
-               double* __restrict__ H, double* __restrict__ Pst, int* __restrict__ status,
-               const int* __restrict__ skip, const int* __restrict__ list, const int* __restrict__ list_n) {
+               double* __restrict__ H, double* __restrict__ Ht, const int* __restrict__ epos,
+               double* __restrict__ Pst,
+               int* __restrict__ status, const int* __restrict__ skip, const int* __restrict__ list, const int* __restrict__ list_n) {
   constexpr int mode = MODE;
   if (skip && *(volatile const int*)skip) return;   // line-search trial needing no evaluation
   constexpr int D = NV - 1;
@@ -340,7 +348,6 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
           js[f++] = bb;
         }
     }
-    double* Ho = H + (size_t)e * NP * kHBlk;
     int p = 0;
     constexpr int FA = 9 + D * D + 3 + 3 + NOOP;
     constexpr int FB = FA + NV * D;
@@ -374,7 +381,7 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
         const double bb = js[FB + p];
         double blk[3][3];
         jac_block<D>(J, aa, ab, blk);
-        store_hblock(Ho + p * kHBlk, hw, bb, blk);
+        store_hpair<NV>(H, Ht, epos, e, a, b, hw, bb, blk);
       }
     }
     return;
@@ -395,7 +402,6 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
           alpha[a][k] = s;
         }
     }
-    double* Ho = H + (size_t)e * NP * kHBlk;
     int p = 0;
 #pragma unroll
     for (int a = 0; a < NV; ++a)
@@ -413,7 +419,7 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
         } else {
           jac_block<D>(J, alpha[a], alpha[b], blk);
         }
-        store_hblock(Ho + p * kHBlk, hw, bb, blk);
+        store_hpair<NV>(H, Ht, epos, e, a, b, hw, bb, blk);
       }
   }
 }
@@ -423,7 +429,7 @@ static void launch_elements_nv(dp_scene* s, const double* q, int mode, int* stat
 #define DP_ELEM_CASE(M)                                                                                       \
   case M:                                                                                                     \
     k_elements<NV, M><<<nb, nt, 0, s->stream>>>(s->ev, s->B, s->w, s->mu, s->lam, s->model, s->E, q, h2, 1e-6, \
-                                                s->fe, s->H, s->Pst, status, s->eval_skip, nullptr, nullptr); \
+                                                s->fe, s->H, s->Ht, s->epos, s->Pst, status, s->eval_skip, nullptr, nullptr); \
     break;
   switch (mode) {
     DP_ELEM_CASE(0)
@@ -623,7 +629,7 @@ void launch_watch_elements(dp_scene* s, const double* q) {
   if (s->E == 0 || s->NV != 4) return;
   const double h2 = s->h * s->h;
   k_elements<4, EV_LIST><<<grid_for(kWatchElemMax, 128), 128, 0, s->stream>>>(
-      s->ev, s->B, s->w, s->mu, s->lam, s->model, s->E, q, h2, 1e-6, s->fe, s->H, s->Pst, &s->esc->status,
+      s->ev, s->B, s->w, s->mu, s->lam, s->model, s->E, q, h2, 1e-6, s->fe, s->H, s->Ht, s->epos, s->Pst, &s->esc->status,
       &s->esc->skip, s->watch_e, &s->esc->n_watch_elem);
   s->launches++;
 }
@@ -668,8 +674,9 @@ __device__ __forceinline__ void inv3_guarded(const double a[9], double o[9]) {
 
 __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __restrict__ slice_base,
                                                   const int* __restrict__ slice_width, const int* __restrict__ diag_slot,
-                                                  const int* __restrict__ contrib_ptr, const int* __restrict__ contrib,
-                                                  const double* __restrict__ H, const double* __restrict__ mass,
+                                                  const int* __restrict__ contrib_ptr,
+                                                  const double* __restrict__ H, const double* __restrict__ Ht,
+                                                  const double* __restrict__ mass,
                                                   const int* __restrict__ b_ptr, const int* __restrict__ b_idx,
                                                   const double* __restrict__ b_comp, const int* __restrict__ c_count,
                                                   const int* __restrict__ c_off, const double* __restrict__ c_blk,
@@ -690,24 +697,33 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
 #pragma unroll
     for (int c = 0; c < 9; ++c) b[c] = 0.0;
     const int t0 = contrib_ptr[slot], t1 = contrib_ptr[slot + 1];
-    // contributions in groups of ASM_CHUNK: all index and block loads of a
-    // group are issued before the (in-order) accumulation
-    int t = t0;
-    for (; t + ASM_CHUNK <= t1; t += ASM_CHUNK) {
-      int cid[ASM_CHUNK];
-      double src[ASM_CHUNK][kHBlk];
+    // the slot's contributions are one contiguous run of the block stream
+    // (store_hpair), summed in list order; loads of a group of ASM_CHUNK
+    // blocks are issued before the (in-order) accumulation
+    const double* hs = H + (size_t)t0 * kHS;
+    const double* ht = Ht + t0;
+    const int n = t1 - t0;
+    int t = 0;
+    for (; t + ASM_CHUNK <= n; t += ASM_CHUNK) {
+      double src[ASM_CHUNK][9];
 #pragma unroll
-      for (int g = 0; g < ASM_CHUNK; ++g) cid[g] = contrib[t + g];
+      for (int g = 0; g < ASM_CHUNK; ++g) {
+        ld256(hs + (size_t)(t + g) * kHS, &src[g][0]);
+        ld256(hs + (size_t)(t + g) * kHS + 4, &src[g][4]);
+        src[g][8] = __ldg(ht + t + g);
+      }
 #pragma unroll
-      for (int g = 0; g < ASM_CHUNK; ++g) load_hblock(H, cid[g], src[g]);
+      for (int g = 0; g < ASM_CHUNK; ++g)
 #pragma unroll
-      for (int g = 0; g < ASM_CHUNK; ++g) acc_hblock(b, src[g], cid[g] >= 0);
+        for (int c = 0; c < 9; ++c) b[c] += src[g][c];
     }
-    for (; t < t1; ++t) {
-      const int cid = contrib[t];
-      double src[kHBlk];
-      load_hblock(H, cid, src);
-      acc_hblock(b, src, cid >= 0);
+    for (; t < n; ++t) {
+      double src[9];
+      ld256(hs + (size_t)t * kHS, &src[0]);
+      ld256(hs + (size_t)t * kHS + 4, &src[4]);
+      src[8] = __ldg(ht + t);
+#pragma unroll
+      for (int c = 0; c < 9; ++c) b[c] += src[c];
     }
     if (slot == dslot) {
       const double m = mass[row];
@@ -761,7 +777,7 @@ void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat)
   const int nb = grid_for((int64_t)s->S * 32, nt);
   const int has_c = (s->colliders.n > 0) && !amat;
   k_assemble<<<nb, nt, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->diag_slot, s->contrib_ptr,
-                                       s->contrib, s->H, s->mass, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_comp,
+                                       s->H, s->Ht, s->mass, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_comp,
                                        has_c ? s->c_count : nullptr, s->c_off, s->c_blk, amat ? 0 : 1,
                                        s->h * s->h, val, s->minv, amat ? nullptr : s->val32,
                                        amat ? nullptr : s->minv32);

@@ -444,7 +444,11 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
       if (colidx[k] == i) diag_slot[i] = (int)slot;
     }
   }
-  // ---- contribution lists per slot: element e, local (a,b) -> one block of the stream H
+  // ---- contribution runs per slot.  Slot (i, j) and slot (j, i) receive
+  // blocks from the same elements (those holding edge ij), element-ascending,
+  // the (j, i) ones being the transposes of the (i, j) ones.  So only the
+  // canonical slots (i <= j) own a run of the block stream H; slot (j, i)
+  // reads the run of (i, j) transposed (rinfo count < 0).
   std::vector<int> cptr(NS + 1, 0);
   std::vector<int64_t> eslot((size_t)E * NV * NV);
   for (int e = 0; e < E; ++e) {
@@ -458,22 +462,37 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
         const int k = (int)(std::lower_bound(rb, rb + rl, j) - rb);
         const int64_t slot = slice_base[i / kSlice] + (int64_t)k * kSlice + (i % kSlice);
         eslot[((size_t)e * NV + a) * NV + b] = slot;
-        cptr[slot + 1]++;
+        if (i <= j && (i < j || a == b)) cptr[slot + 1]++;
       }
     }
   }
   for (int64_t t = 0; t < NS; ++t) cptr[t + 1] += cptr[t];
-  // block-stream position of every (element, a, b): the fill order of the
-  // slot lists (element-ascending within a slot, as the reference's COO sum)
-  std::vector<int> epos((size_t)E * NV * NV);
+  // block-stream position of every unordered local pair (a <= b) of every
+  // element: the fill order of the canonical slot's run (element-ascending,
+  // as the reference's COO sum); ~t when the stored block is the pair's
+  // transpose (vid[a] > vid[b])
+  std::vector<int> epos((size_t)E * NP);
+  std::vector<int2> rinfo(NS, make_int2(0, 0));
   {
     std::vector<int> fill(cptr.begin(), cptr.end() - 1);
-    for (int e = 0; e < E; ++e)
+    for (int e = 0; e < E; ++e) {
+      const int* vv = &ev[e].x;
+      int p = 0;
       for (int a = 0; a < NV; ++a)
-        for (int b = 0; b < NV; ++b) {
-          const size_t ab = ((size_t)e * NV + a) * NV + b;
-          epos[ab] = fill[eslot[ab]]++;
+        for (int b = a; b < NV; ++b, ++p) {
+          const int64_t sab = eslot[((size_t)e * NV + a) * NV + b];
+          const int64_t sba = eslot[((size_t)e * NV + b) * NV + a];
+          if (vv[a] <= vv[b]) {
+            epos[(size_t)e * NP + p] = fill[sab]++;
+            rinfo[sba] = make_int2((int)cptr[sab], -(int)(cptr[sab + 1] - cptr[sab]));
+          } else {
+            epos[(size_t)e * NP + p] = ~fill[sba]++;
+            rinfo[sab] = make_int2((int)cptr[sba], -(int)(cptr[sba + 1] - cptr[sba]));
+          }
         }
+    }
+    for (int64_t t = 0; t < NS; ++t)
+      if (cptr[t + 1] > cptr[t]) rinfo[t] = make_int2((int)cptr[t], (int)(cptr[t + 1] - cptr[t]));
   }
 
   // ---- device buffers
@@ -492,7 +511,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   rc |= upload(s, &s->slice_width, slice_width);
   rc |= upload(s, &s->col, col);
   rc |= upload(s, &s->diag_slot, diag_slot);
-  rc |= upload(s, &s->contrib_ptr, cptr);
+  rc |= upload(s, &s->rinfo, rinfo);
   rc |= upload(s, &s->epos, epos);
   rc |= dalloc(s, &s->val_fwd, (size_t)NS * 9);
   rc |= dalloc(s, &s->val_adj, (size_t)NS * 9);
@@ -565,7 +584,7 @@ int dp_scene_destroy(dp_scene* s) {
   mg_destroy(s);
   void* ptrs[] = {s->ev, s->B, s->w, s->vol, s->mu, s->lam, s->model, s->mass, s->inc_ptr, s->inc,
                   s->slice_base, s->slice_width, s->col, s->diag_slot, s->val_fwd, s->val_adj, s->val_A,
-                  s->contrib_ptr, s->epos, s->minv, s->fe, s->H, s->Ht, s->Pst, s->watch_v, s->watch_e, s->d_colliders, s->b_ptr, s->b_idx,
+                  s->rinfo, s->epos, s->minv, s->fe, s->H, s->Ht, s->Pst, s->watch_v, s->watch_e, s->d_colliders, s->b_ptr, s->b_idx,
                   s->b_target, s->b_comp, s->b_vertex, s->fext, s->c_count, s->c_off, s->c_vertex, s->c_collider,
                   s->c_frame, s->c_dn, s->c_mu, s->c_delta, s->c_blk, s->c_force, s->c_kmu, s->c_kc, s->scan_tmp,
                   s->q, s->q_hat, s->q_bar, s->v_bar, s->r, s->dq, s->q_try, s->rhs, s->z, s->z_prev, s->tmp, s->q_ev, s->r_try, s->kx, s->kr,

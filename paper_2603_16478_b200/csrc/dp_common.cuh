@@ -101,3 +101,15 @@ __device__ __forceinline__ void fold_multi(const double* partial, int stride, in
 }
 
 }  // namespace dp
+
+// 256-bit global accesses (sm_100: one full 32-byte sector per lane)
+__device__ __forceinline__ void ld256f(const float* p, float o[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3]), "=f"(o[4]), "=f"(o[5]), "=f"(o[6]), "=f"(o[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st256f(float* p, const float v[8]) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}

@@ -45,18 +45,20 @@ struct KrylovScalars {
 
 // GMRES restart cap: the default cycle is 50; solves that stagnate escalate
 // to longer cycles (indefinite Newton matrices of compressed cloth).
-// FP32 fine-level operator copy: 1 = slot-major, 12 floats per slot (three
-// float4 loads per block), 0 = component-major like the FP64 values (nine
-// coalesced 128 B loads per warp and block, no padding)
+// FP32 fine-level operator copy: 2 = slot-major first 8 floats of a block
+// (32 B: one 256-bit load per lane, 1 KB contiguous per warp) + the 9th float
+// in a tail array after them (val32[8 NS + slot]); 1 = slot-major, 12 floats
+// per slot (three float4 loads per block); 0 = component-major like the FP64
+// values (nine coalesced 128 B loads per warp and block)
 #ifndef DP_VAL32_PACKED
 #define DP_VAL32_PACKED 0
 #endif
-constexpr int kVal32PerSlot = DP_VAL32_PACKED ? 12 : 9;
+constexpr int kVal32PerSlot = DP_VAL32_PACKED == 1 ? 12 : 9;
 
-// element Hessian blocks in the slot-ordered stream: the first 8 doubles of
-// a block in H (64 B, 32-byte aligned: two full sectors), the 9th in Ht,
-// one per (element, a, b) contribution incl. the transposed a > b copies, laid
-// out in the SELL slots' contribution-list order so the assembly streams them
+// element Hessian blocks in the slot-ordered stream (canonical slots i <= j
+// only): the first 8 doubles of a block in H (64 B, 32-byte aligned: two full
+// sectors), the 9th in Ht; one block per (element, a <= b) pair, laid out in
+// the canonical slots' run order so the assembly streams them
 constexpr int kHS = 8;
 
 constexpr int kMaxRestart = 200;
@@ -160,8 +162,8 @@ struct dp_scene {
   double* val_fwd = nullptr;       // forward Newton matrix
   double* val_adj = nullptr;       // adjoint operator (transposed contact blocks)
   double* val_A = nullptr;         // constant A (lazy, export only)
-  int* contrib_ptr = nullptr;      // slot -> run [ptr[slot], ptr[slot+1]) of the block stream H
-  int* epos = nullptr;             // E*NV*NV: (element, a, b) -> position in the block stream
+  int2* rinfo = nullptr;           // slot -> {start, count} of its run of H (count < 0: read transposed)
+  int* epos = nullptr;             // E*NP: (element, a <= b) -> position in H (~pos: stored transposed)
   double* minv = nullptr;          // block-Jacobi inverses [9][V]
   float* val32 = nullptr;          // FP32 copy of the last assembled operator (multigrid fine level)
   const double* val32_src = nullptr;   // operator val32 was last written from
@@ -169,7 +171,7 @@ struct dp_scene {
 
   // element outputs
   double* fe = nullptr;            // E*NV*3
-  double* H = nullptr;             // block stream, E*NV*NV blocks of kHS doubles (slot order)
+  double* H = nullptr;             // block stream, E*NP blocks of kHS doubles (canonical-slot order)
   double* Ht = nullptr;            // 9th double of every block of H
   double* Pst = nullptr;           // E*27 (P, dP/dmu, dP/dlam) for backprop
 

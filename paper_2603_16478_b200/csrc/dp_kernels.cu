@@ -5,13 +5,15 @@
 //  * element inputs: SoA (Dm^-1 as [9][E], w/mu/lam/model as [E]) and the
 //    four vertex ids as one int4 per element (one 16-byte load);
 //  * element outputs: residual contributions fe[E][NV][3] and the NP
-//    unique 3x3 blocks of the symmetric element Hessian H[E][NP][9];
+//    unique 3x3 blocks of the symmetric element Hessian, written into a
+//    block stream H ordered by the assembly's slot runs (store_hpair);
 //  * system matrix: SELL-32 block-sparse (3x3 FP64 blocks), slices of 32
 //    block rows, block k of lane l at slot base_s + 32k + l; block values
 //    component-major inside a slice so each warp load is 32 consecutive
 //    doubles (256 B).
-// Assembly is a deterministic gather (no atomics): every SELL slot owns a
-// list of (element, local block, transposed?) contributions.
+// Assembly is a deterministic stream (no atomics): every canonical SELL slot
+// (row <= col) owns a contiguous run of H in element order, and slot (j, i)
+// reads the run of (i, j) transposed.
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <algorithm>
@@ -136,12 +138,19 @@ __device__ __forceinline__ void make_jac(const double U[3][D], const double sig[
 #define ASM_CHUNK 4
 #endif
 
-// h^2 w [(beta_a.beta_b) I - blk] for the element pair (a, b), a <= b, as one
-// 80-byte block (16-byte stores; 9 doubles + pad) written
-// into the slot-ordered block stream: at the pair's position in the (a, b)
-// slot's contribution list and, for a < b, transposed at its position in the
-// (b, a) slot's list (epos, built at setup in contribution-list order).  The
-// assembly then reads every slot's contributions as one contiguous run.
+// b += block, or its transpose
+__device__ __forceinline__ void acc_block(double b[9], const double src[9], bool transposed) {
+  if (!transposed) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) b[c] += src[c];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) b[i * 3 + j] += src[j * 3 + i];
+  }
+}
+
 // 256-bit global accesses (sm_100): one full 32-byte sector per access
 __device__ __forceinline__ void st256(double* p, double a, double b, double c, double d) {
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
@@ -150,33 +159,35 @@ __device__ __forceinline__ void ld256(const double* p, double o[4]) {
   asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
 }
 
-// h^2 w [(beta_a.beta_b) I - blk] for the element pair (a, b), a <= b, written
-// into the slot-ordered block stream: at the pair's position t in the (a, b)
-// slot's contribution list and, for a < b, transposed at its position in the
-// (b, a) slot's list (epos, built at setup in contribution-list order).  A
-// block is split into its first 8 doubles, Hs[t] (64 B: two full-sector
-// 256-bit stores), and its last, Ht[t].  The assembly then reads every slot's
-// contributions as one contiguous run of each array.
+// h^2 w [(beta_a.beta_b) I - blk] for the element's local pair p = (a, b),
+// a <= b, written once into the slot-ordered block stream, at its position t
+// in the run of the canonical slot (min(i, j), max(i, j)) of its vertices
+// i = vid[a], j = vid[b] (epos, built at setup in run order; ~t: i > j, the
+// block is stored transposed).  A block is split into its first 8 doubles,
+// Hs[t] (64 B: two full-sector 256-bit stores), and its last, Ht[t] (the
+// (2,2) entry, transpose-invariant).  The assembly reads each slot's run as
+// one contiguous stream, the (j, i) slots the (i, j) run transposed.
 template <int NV>
 __device__ __forceinline__ void store_hpair(double* __restrict__ Hs, double* __restrict__ Ht,
-                                            const int* __restrict__ epos, int e, int a, int b, double hw, double bb,
+                                            const int* __restrict__ epos, int e, int p, double hw, double bb,
                                             const double blk[3][3]) {
+  constexpr int NP = NV * (NV + 1) / 2;
   double v[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) v[i * 3 + j] = hw * (((i == j) ? bb : 0.0) - blk[i][j]);
-  const int* ep = epos + (size_t)e * NV * NV;
-  const int t = __ldg(ep + a * NV + b);
-  st256(Hs + (size_t)t * kHS, v[0], v[1], v[2], v[3]);
-  st256(Hs + (size_t)t * kHS + 4, v[4], v[5], v[6], v[7]);
-  Ht[t] = v[8];
-  if (a != b) {
-    const int tt = __ldg(ep + b * NV + a);
-    st256(Hs + (size_t)tt * kHS, v[0], v[3], v[6], v[1]);
-    st256(Hs + (size_t)tt * kHS + 4, v[4], v[7], v[2], v[5]);
-    Ht[tt] = v[8];
+  const int tc = __ldg(epos + (size_t)e * NP + p);
+  const int t = tc >= 0 ? tc : ~tc;
+  double* o = Hs + (size_t)t * kHS;
+  if (tc >= 0) {
+    st256(o, v[0], v[1], v[2], v[3]);
+    st256(o + 4, v[4], v[5], v[6], v[7]);
+  } else {
+    st256(o, v[0], v[3], v[6], v[1]);
+    st256(o + 4, v[4], v[7], v[2], v[5]);
   }
+  Ht[t] = v[8];
 }
 
 // One thread per element.  NV = vertices per element (4 tet, 3 tri).  The
@@ -381,7 +392,7 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
         const double bb = js[FB + p];
         double blk[3][3];
         jac_block<D>(J, aa, ab, blk);
-        store_hpair<NV>(H, Ht, epos, e, a, b, hw, bb, blk);
+        store_hpair<NV>(H, Ht, epos, e, p, hw, bb, blk);
       }
     }
     return;
@@ -419,7 +430,7 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
         } else {
           jac_block<D>(J, alpha[a], alpha[b], blk);
         }
-        store_hpair<NV>(H, Ht, epos, e, a, b, hw, bb, blk);
+        store_hpair<NV>(H, Ht, epos, e, p, hw, bb, blk);
       }
   }
 }
@@ -674,7 +685,7 @@ __device__ __forceinline__ void inv3_guarded(const double a[9], double o[9]) {
 
 __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __restrict__ slice_base,
                                                   const int* __restrict__ slice_width, const int* __restrict__ diag_slot,
-                                                  const int* __restrict__ contrib_ptr,
+                                                  const int2* __restrict__ rinfo,
                                                   const double* __restrict__ H, const double* __restrict__ Ht,
                                                   const double* __restrict__ mass,
                                                   const int* __restrict__ b_ptr, const int* __restrict__ b_idx,
@@ -696,13 +707,14 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
     double b[9];
 #pragma unroll
     for (int c = 0; c < 9; ++c) b[c] = 0.0;
-    const int t0 = contrib_ptr[slot], t1 = contrib_ptr[slot + 1];
-    // the slot's contributions are one contiguous run of the block stream
-    // (store_hpair), summed in list order; loads of a group of ASM_CHUNK
-    // blocks are issued before the (in-order) accumulation
-    const double* hs = H + (size_t)t0 * kHS;
-    const double* ht = Ht + t0;
-    const int n = t1 - t0;
+    // the slot's contributions: one contiguous run of the block stream,
+    // summed in list order (transposed for the i > j slots); the loads of a
+    // group of ASM_CHUNK blocks are issued before the accumulation
+    const int2 ri = rinfo[slot];
+    const bool tr = ri.y < 0;
+    const int n = tr ? -ri.y : ri.y;
+    const double* hs = H + (size_t)ri.x * kHS;
+    const double* ht = Ht + ri.x;
     int t = 0;
     for (; t + ASM_CHUNK <= n; t += ASM_CHUNK) {
       double src[ASM_CHUNK][9];
@@ -713,17 +725,14 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
         src[g][8] = __ldg(ht + t + g);
       }
 #pragma unroll
-      for (int g = 0; g < ASM_CHUNK; ++g)
-#pragma unroll
-        for (int c = 0; c < 9; ++c) b[c] += src[g][c];
+      for (int g = 0; g < ASM_CHUNK; ++g) acc_block(b, src[g], tr);
     }
     for (; t < n; ++t) {
       double src[9];
       ld256(hs + (size_t)t * kHS, &src[0]);
       ld256(hs + (size_t)t * kHS + 4, &src[4]);
       src[8] = __ldg(ht + t);
-#pragma unroll
-      for (int c = 0; c < 9; ++c) b[c] += src[c];
+      acc_block(b, src, tr);
     }
     if (slot == dslot) {
       const double m = mass[row];
@@ -757,7 +766,12 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
       // FP32 copy for the multigrid smoother: 12 floats per slot (9 + pad),
       // slot-major, so a lane reads its block as three 16-byte loads and a
       // warp reads 1.5 KB contiguous
-#if DP_VAL32_PACKED
+#if DP_VAL32_PACKED == 2
+      const float f8[8] = {(float)b[0], (float)b[1], (float)b[2], (float)b[3],
+                           (float)b[4], (float)b[5], (float)b[6], (float)b[7]};
+      st256f(val32 + (size_t)slot * 8, f8);
+      val32[(size_t)slice_base[S] * 8 + slot] = (float)b[8];
+#elif DP_VAL32_PACKED
       float4* v4 = reinterpret_cast<float4*>(val32 + (size_t)slot * 12);
       v4[0] = make_float4((float)b[0], (float)b[1], (float)b[2], (float)b[3]);
       v4[1] = make_float4((float)b[4], (float)b[5], (float)b[6], (float)b[7]);
@@ -776,7 +790,7 @@ void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat)
   const int nt = 256;
   const int nb = grid_for((int64_t)s->S * 32, nt);
   const int has_c = (s->colliders.n > 0) && !amat;
-  k_assemble<<<nb, nt, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->diag_slot, s->contrib_ptr,
+  k_assemble<<<nb, nt, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->diag_slot, s->rinfo,
                                        s->H, s->Ht, s->mass, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_comp,
                                        has_c ? s->c_count : nullptr, s->c_off, s->c_blk, amat ? 0 : 1,
                                        s->h * s->h, val, s->minv, amat ? nullptr : s->val32,
@@ -1495,14 +1509,28 @@ __global__ void k_gm_prec(int V, TB* W0, TB* W1, TB* Vb, size_t ld, const double
 // step 2 (one warp per SELL slice): w = A z, coef_i = (w, v_i) for i <= j,
 // |w|^2; last block folds into the Hessenberg column.
 // SpMV row with the packed FP32 copy of the operator (12 floats per slot)
-__device__ __forceinline__ void spmv_row32(int slice, int lane, const int* __restrict__ slice_base,
+__device__ __forceinline__ void spmv_row32(int S, int slice, int lane, const int* __restrict__ slice_base,
                                            const int* __restrict__ slice_width, const int* __restrict__ col,
                                            const float* __restrict__ val, const double* __restrict__ x, double y[3]) {
   const int base = slice_base[slice];
   const int K = slice_width[slice];
   const int* cs = col + base + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#if DP_VAL32_PACKED
+#if DP_VAL32_PACKED == 2
+  const float* tail = val + (size_t)slice_base[S] * 8;
+#pragma unroll 2
+  for (int k = 0; k < K; ++k) {
+    const int slot = base + k * kSlice + lane;
+    const int j = __ldg(cs + k * kSlice);
+    float m[8];
+    ld256f(val + (size_t)slot * 8, m);
+    const float m8 = __ldg(tail + slot);
+    const double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
+    a0 += (double)m[0] * x0 + (double)m[1] * x1 + (double)m[2] * x2;
+    a1 += (double)m[3] * x0 + (double)m[4] * x1 + (double)m[5] * x2;
+    a2 += (double)m[6] * x0 + (double)m[7] * x1 + (double)m8 * x2;
+  }
+#elif DP_VAL32_PACKED
   const float4* p4 = reinterpret_cast<const float4*>(val) + (size_t)(base + lane) * 3;
 #pragma unroll 2
   for (int k = 0; k < K; ++k) {
@@ -1546,7 +1574,7 @@ __global__ void __launch_bounds__(256) k_gm_spmvdot_r(int V, int S, const int* _
   const int row = gw * kSlice + lane;
   double u[3] = {0.0, 0.0, 0.0};
   if (gw < S) {
-    if constexpr (sizeof(TV) == 4) spmv_row32(gw, lane, slice_base, slice_width, col, val, z, u);
+    if constexpr (sizeof(TV) == 4) spmv_row32(S, gw, lane, slice_base, slice_width, col, val, z, u);
     else spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, z, u);
     if (row < V) {
 #pragma unroll

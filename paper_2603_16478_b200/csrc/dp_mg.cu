@@ -202,10 +202,13 @@ int mg_setup(dp_scene* s) {
     }
   }
   HostPattern cur = fine;
-  // level 1 gathers from the FP32 fine copy (DP_VAL32_PACKED: slot * 12,
-  // else the FP64 layout's component-major addresses)
+  // level 1 gathers from the FP32 fine copy (DP_VAL32_PACKED 2: slot * 8 +
+  // tail, 1: slot * 12, else the FP64 layout's component-major addresses)
   std::vector<int64_t> cur_addr(s->nnzb);
-  for (int64_t k = 0; k < s->nnzb; ++k) cur_addr[k] = DP_VAL32_PACKED ? s->h_block_slot[k] * 12 : fine_addr[k];
+  for (int64_t k = 0; k < s->nnzb; ++k)
+    cur_addr[k] = DP_VAL32_PACKED == 2 ? s->h_block_slot[k] * 8
+                  : DP_VAL32_PACKED   ? s->h_block_slot[k] * 12
+                                      : fine_addr[k];
   while (cur.n > kCoarseMax && !rc) {
     std::vector<int> agg;
     const int na = aggregate(cur, agg);
@@ -384,15 +387,21 @@ __global__ void __launch_bounds__(256) k_mg_galerkin(int n, int S, const int* __
                                                      const int* __restrict__ gal_ptr, const int* __restrict__ gal,
                                                      const TF* __restrict__ valf, double* __restrict__ valc,
                                                      double* __restrict__ minv, const int* __restrict__ slot_row,
-                                                     int64_t NS) {
+                                                     int64_t NS, const TF* __restrict__ tail) {
   const int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (slot >= NS) return;
   double b[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int t = gal_ptr[slot] + lane; t < gal_ptr[slot + 1]; t += 32) {
     const TF* src = valf + gal[t];
+    if (tail) {   // FP32 fine copy, 8 + 1 layout: gal[t] = 8 * fine slot
 #pragma unroll
-    for (int c = 0; c < 9; ++c) b[c] += (double)src[c * CSTRIDE];
+      for (int c = 0; c < 8; ++c) b[c] += (double)src[c];
+      b[8] += (double)tail[gal[t] >> 3];
+    } else {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) b[c] += (double)src[c * CSTRIDE];
+    }
   }
 #pragma unroll
   for (int c = 0; c < 9; ++c) b[c] = warp_allsum(b[c]);
@@ -466,7 +475,15 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
   for (int k = wsub; k < K; k += SPLIT) {
     const int j = __ldg(cs + k * kSlice);
     double m[9];
-    if (sizeof(TV) == 4 && DP_VAL32_PACKED) {
+    if (sizeof(TV) == 4 && DP_VAL32_PACKED == 2) {
+      // 8 + 1 FP32 layout: one 256-bit load per block + the tail float
+      const int slot = base + k * kSlice + lane;
+      float f[8];
+      ld256f(reinterpret_cast<const float*>(val) + (size_t)slot * 8, f);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) m[c] = f[c];
+      m[8] = __ldg(reinterpret_cast<const float*>(val) + (size_t)slice_base[S] * 8 + slot);
+    } else if (sizeof(TV) == 4 && DP_VAL32_PACKED) {
       // packed FP32 fine level: 3 x 16-byte loads per block
       const float4* p4 = reinterpret_cast<const float4*>(val) + (size_t)(base + k * kSlice + lane) * 3;
       const float4 q0 = __ldg(p4), q1 = __ldg(p4 + 1), q2 = __ldg(p4 + 2);
@@ -966,10 +983,11 @@ void mg_assemble(dp_scene* s, const double* val) {
     if (l == 1)
       k_mg_galerkin<float, DP_VAL32_PACKED ? 1 : kSlice><<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
           L.n, L.S, L.slice_base, L.slice_width, L.diag_slot, L.gal_ptr, L.gal, s->val32, L.val, L.minv, L.slot_row,
-          L.NS);
+          L.NS, DP_VAL32_PACKED == 2 ? s->val32 + (size_t)s->NS * 8 : nullptr);
     else
       k_mg_galerkin<double, kSlice><<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
-          L.n, L.S, L.slice_base, L.slice_width, L.diag_slot, L.gal_ptr, L.gal, vf, L.val, L.minv, L.slot_row, L.NS);
+          L.n, L.S, L.slice_base, L.slice_width, L.diag_slot, L.gal_ptr, L.gal, vf, L.val, L.minv, L.slot_row, L.NS,
+          (const double*)nullptr);
     vf = L.val;
     s->launches++;
   }

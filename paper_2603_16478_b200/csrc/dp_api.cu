@@ -383,7 +383,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
     }
 
   // ---- vertex incidence (residual gather) and block pattern (core.py:339-364)
-  std::vector<int> inc_ptr(V + 1, 0), inc;
+  std::vector<int> inc_ptr(V + 1, 0), inc, fe_pos((size_t)E * NV);
   for (int e = 0; e < E; ++e) {
     const int* vv = &ev[e].x;
     for (int a = 0; a < NV; ++a) inc_ptr[vv[a] + 1]++;
@@ -394,7 +394,10 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
     std::vector<int> fill(inc_ptr.begin(), inc_ptr.end() - 1);
     for (int e = 0; e < E; ++e) {
       const int* vv = &ev[e].x;
-      for (int a = 0; a < NV; ++a) inc[fill[vv[a]]++] = e * NV + a;
+      for (int a = 0; a < NV; ++a) {
+        fe_pos[(size_t)e * NV + a] = fill[vv[a]];
+        inc[fill[vv[a]]++] = e * NV + a;
+      }
     }
   }
   std::vector<int>& rowptr = s->h_rowptr;
@@ -516,7 +519,8 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   rc |= dalloc(s, &s->val_fwd, (size_t)NS * 9);
   rc |= dalloc(s, &s->val_adj, (size_t)NS * 9);
   rc |= dalloc(s, &s->minv, (size_t)V * 9);
-  rc |= dalloc(s, &s->fe, (size_t)std::max(E, 1) * NV * 3);
+  rc |= dalloc(s, &s->fe, (size_t)std::max(E, 1) * NV * kFeS);
+  rc |= upload(s, &s->fe_pos, fe_pos);
   rc |= dalloc(s, &s->H, (size_t)std::max(cptr[NS], 1) * kHS);
   rc |= dalloc(s, &s->Ht, (size_t)std::max(cptr[NS], 1));
   rc |= dalloc(s, &s->Pst, (size_t)std::max(E, 1) * 27);
@@ -584,7 +588,7 @@ int dp_scene_destroy(dp_scene* s) {
   mg_destroy(s);
   void* ptrs[] = {s->ev, s->B, s->w, s->vol, s->mu, s->lam, s->model, s->mass, s->inc_ptr, s->inc,
                   s->slice_base, s->slice_width, s->col, s->diag_slot, s->val_fwd, s->val_adj, s->val_A,
-                  s->rinfo, s->epos, s->minv, s->fe, s->H, s->Ht, s->Pst, s->watch_v, s->watch_e, s->d_colliders, s->b_ptr, s->b_idx,
+                  s->rinfo, s->epos, s->minv, s->fe, s->fe_pos, s->H, s->Ht, s->Pst, s->watch_v, s->watch_e, s->d_colliders, s->b_ptr, s->b_idx,
                   s->b_target, s->b_comp, s->b_vertex, s->fext, s->c_count, s->c_off, s->c_vertex, s->c_collider,
                   s->c_frame, s->c_dn, s->c_mu, s->c_delta, s->c_blk, s->c_force, s->c_kmu, s->c_kc, s->scan_tmp,
                   s->q, s->q_hat, s->q_bar, s->v_bar, s->r, s->dq, s->q_try, s->rhs, s->z, s->z_prev, s->tmp, s->q_ev, s->r_try, s->kx, s->kr,

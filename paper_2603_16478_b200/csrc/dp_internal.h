@@ -60,6 +60,9 @@ constexpr int kVal32PerSlot = DP_VAL32_PACKED == 1 ? 12 : 9;
 // sectors), the 9th in Ht; one block per (element, a <= b) pair, laid out in
 // the canonical slots' run order so the assembly streams them
 constexpr int kHS = 8;
+// element residual contributions: one 32-byte entry (3 doubles + pad) per
+// (element, vertex), laid out in the vertices' incidence order
+constexpr int kFeS = 4;
 
 constexpr int kMaxRestart = 200;
 struct GmresScalars {
@@ -170,7 +173,8 @@ struct dp_scene {
   float* minv32 = nullptr;         // FP32 block-Jacobi inverses (multigrid smoother)
 
   // element outputs
-  double* fe = nullptr;            // E*NV*3
+  double* fe = nullptr;            // E*NV entries of kFeS doubles, incidence order (fe_pos)
+  int* fe_pos = nullptr;           // E*NV: (element, a) -> entry of fe
   double* H = nullptr;             // block stream, E*NP blocks of kHS doubles (canonical-slot order)
   double* Ht = nullptr;            // 9th double of every block of H
   double* Pst = nullptr;           // E*27 (P, dP/dmu, dP/dlam) for backprop

@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
     k_elements(const int4* __restrict__ ev, const double* __restrict__ Bm, const double* __restrict__ w,
                const double* __restrict__ mu, const double* __restrict__ lam, const int* __restrict__ model, int E,
                const double* __restrict__ q, double h2, double tau_rel, double* __restrict__ fe,
+               const int* __restrict__ fe_pos,
                double* __restrict__ H, double* __restrict__ Ht, const int* __restrict__ epos,
                double* __restrict__ Pst,
                int* __restrict__ status, const int* __restrict__ skip, const int* __restrict__ list, const int* __restrict__ list_n) {
@@ -259,9 +260,7 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
   if (st) {
     atomicOr(status, st);
 #pragma unroll
-    for (int a = 0; a < NV; ++a)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) fe[((size_t)e * NV + a) * 3 + i] = 0.0;
+    for (int a = 0; a < NV; ++a) st256(fe + (size_t)__ldg(fe_pos + (size_t)e * NV + a) * kFeS, 0.0, 0.0, 0.0, 0.0);
     return;
   }
   if (!(mode & EV_AMAT)) {
@@ -276,15 +275,20 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
         for (int k = 0; k < D; ++k) s += U[i][k] * th[k] * V[c][k];
         P[i][c] = s;
       }
+    // written at the (e, a) entry's position in vertex a's incidence run
+    // (fe_pos), one full-sector 256-bit store: k_residual streams the runs
 #pragma unroll
-    for (int a = 0; a < NV; ++a)
+    for (int a = 0; a < NV; ++a) {
+      double f3[3];
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
         double s = 0.0;
 #pragma unroll
         for (int c = 0; c < D; ++c) s += (F[i][c] - P[i][c]) * beta[a][c];
-        fe[((size_t)e * NV + a) * 3 + i] = hw * s;
+        f3[i] = hw * s;
       }
+      st256(fe + (size_t)__ldg(fe_pos + (size_t)e * NV + a) * kFeS, f3[0], f3[1], f3[2], 0.0);
+    }
     if (mode & EV_STOREP) {
       double* o = Pst + (size_t)e * 27;
 #pragma unroll
@@ -440,7 +444,7 @@ static void launch_elements_nv(dp_scene* s, const double* q, int mode, int* stat
 #define DP_ELEM_CASE(M)                                                                                       \
   case M:                                                                                                     \
     k_elements<NV, M><<<nb, nt, 0, s->stream>>>(s->ev, s->B, s->w, s->mu, s->lam, s->model, s->E, q, h2, 1e-6, \
-                                                s->fe, s->H, s->Ht, s->epos, s->Pst, status, s->eval_skip, nullptr, nullptr); \
+                                                s->fe, s->fe_pos, s->H, s->Ht, s->epos, s->Pst, status, s->eval_skip, nullptr, nullptr); \
     break;
   switch (mode) {
     DP_ELEM_CASE(0)
@@ -486,25 +490,21 @@ __device__ __forceinline__ void residual_row(int i, const double* __restrict__ m
     r0 = m * (q[3 * i] - q_hat[3 * i]);
     r1 = m * (q[3 * i + 1] - q_hat[3 * i + 1]);
     r2 = m * (q[3 * i + 2] - q_hat[3 * i + 2]);
-    // element contributions in groups of 4 (all loads of a group in flight
+    // element contributions: the vertex's incidence run of the fe stream
+    // (incidence order), in groups of 4 (all loads of a group in flight
     // before the in-order accumulation)
     int k = inc_ptr[i];
     const int k1 = inc_ptr[i + 1];
     for (; k + 4 <= k1; k += 4) {
-      int id[4];
-      double f[4][3];
+      double f[4][4];
 #pragma unroll
-      for (int g = 0; g < 4; ++g) id[g] = inc[k + g];
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const double* fp = fe + (size_t)id[g] * 3;
-        f[g][0] = fp[0]; f[g][1] = fp[1]; f[g][2] = fp[2];
-      }
+      for (int g = 0; g < 4; ++g) ld256(fe + (size_t)(k + g) * kFeS, f[g]);
 #pragma unroll
       for (int g = 0; g < 4; ++g) { r0 += f[g][0]; r1 += f[g][1]; r2 += f[g][2]; }
     }
     for (; k < k1; ++k) {
-      const double* f = fe + (size_t)inc[k] * 3;
+      double f[4];
+      ld256(fe + (size_t)k * kFeS, f);
       r0 += f[0]; r1 += f[1]; r2 += f[2];
     }
     if (b_ptr) {
@@ -640,7 +640,7 @@ void launch_watch_elements(dp_scene* s, const double* q) {
   if (s->E == 0 || s->NV != 4) return;
   const double h2 = s->h * s->h;
   k_elements<4, EV_LIST><<<grid_for(kWatchElemMax, 128), 128, 0, s->stream>>>(
-      s->ev, s->B, s->w, s->mu, s->lam, s->model, s->E, q, h2, 1e-6, s->fe, s->H, s->Ht, s->epos, s->Pst, &s->esc->status,
+      s->ev, s->B, s->w, s->mu, s->lam, s->model, s->E, q, h2, 1e-6, s->fe, s->fe_pos, s->H, s->Ht, s->epos, s->Pst, &s->esc->status,
       &s->esc->skip, s->watch_e, &s->esc->n_watch_elem);
   s->launches++;
 }

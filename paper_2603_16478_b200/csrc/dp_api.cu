@@ -164,6 +164,10 @@ static const int g_debug = getenv("DP_DEBUG") ? atoi(getenv("DP_DEBUG")) : 0;
 // poor (friction-cone / activation kinks): a cheap direction is enough
 static const int g_precheck = getenv("DP_LS_PRECHECK") ? atoi(getenv("DP_LS_PRECHECK")) : 1;
 static const double g_watch_frac = getenv("DP_LS_WATCH_FRAC") ? atof(getenv("DP_LS_WATCH_FRAC")) : 0.5;
+// line-search trials evaluate the elements with their Jacobian blocks: an
+// accepted trial point is the next Newton point, whose element pass (forward.py
+// :186-192 projects the elements at q again) is then already done
+static const int g_spec_jac = getenv("DP_LS_SPECJAC") ? atoi(getenv("DP_LS_SPECJAC")) : 1;
 static const int g_ls_norm = getenv("DP_LS_NORM") ? atoi(getenv("DP_LS_NORM")) : 0;
 static const double g_eta_plateau = getenv("DP_ETA_PLATEAU") ? atof(getenv("DP_ETA_PLATEAU")) : 0.0;
 static double now_s() {
@@ -924,11 +928,21 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
   // q at the last Jacobian evaluation (forward.py:201): the adjoint operator's point
   double* q_eval = s->q_ev;
   double last_t = 1.0;   // step length accepted by the previous line search
+  bool elems_at_q = false;   // element buffers hold the Jacobian pass at q
+  const int trial_mode = g_spec_jac ? EV_JAC : 0;
   for (int it = 0; it < cfg.max_iter; ++it) {
     double t_it0 = g_debug ? now_s() : 0.0;
     k_reset_flags<<<1, 1, 0, s->stream>>>(s->esc);
     launch_detect(s, q);
-    evaluate(s, q, s->r, 1);
+    if (elems_at_q) {
+      // element projections, residual contributions and Hessian blocks at q
+      // were computed by the accepted line-search trial (same kernel, same q)
+      launch_contacts(s, q, s->q_bar, -1, s->c_vertex, s->c_frame, s->c_dn, s->c_mu, s->c_delta, 0, 0, s->esc);
+      launch_residual(s, q, s->q_hat, s->r, s->esc);
+    } else {
+      evaluate(s, q, s->r, 1);
+    }
+    elems_at_q = false;
     s->launches += 1;
     if ((rc = sync_esc(s))) return rc;
     const EvalScalars E = *s->h_esc;
@@ -1010,11 +1024,11 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
         launch_watch_elements(s, q_try);
         launch_contacts(s, q_try, s->q_bar, -1, s->c_vertex, s->c_frame, s->c_dn, s->c_mu, s->c_delta, 0, 0, s->esc);
         launch_watch_check(s, q_try, E.rmax);
-        launch_elements(s, q_try, 0, &s->esc->status);
+        launch_elements(s, q_try, trial_mode, &s->esc->status);
         launch_residual(s, q_try, s->q_hat, s->r_try, s->esc);
         s->launches += 2;
       } else {
-        evaluate(s, q_try, s->r_try, 0);
+        evaluate(s, q_try, s->r_try, trial_mode);
       }
       s->eval_skip = nullptr;
       s->launches++;
@@ -1032,6 +1046,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
         if (!value_error && decrease) {
           std::swap(q, q_try);
           accepted = true;
+          elems_at_q = g_spec_jac != 0;
           break;
         }
       }

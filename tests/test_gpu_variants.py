@@ -1,8 +1,10 @@
 """Solver-plumbing switches that must not change a single bit (DESIGN.md
 §6b): host-driven GMRES columns instead of CUDA-graph WHILE nodes, the fused
 cooperative coarse V-cycle, the un-fused first fine Jacobi sweep, and the
-line search without the watched-row pre-check, and the restriction in
-launches of its own.  Each
+line search without the watched-row pre-check, the restriction in
+launches of its own, and line-search trials evaluated without the Jacobian
+blocks (the accepted trial's element pass is then repeated at the next Newton
+point).  Each
 variant runs in its own process (the switches are read when the library
 loads) on the same C5-family rollout, forward and reverse."""
 import os
@@ -26,8 +28,8 @@ def _digest(env_extra):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("variant", [{"DP_GRAPHS": "0"}, {"DP_MG_FUSED": "1"}, {"DP_PREJAC": "0"},
-                                     {"DP_LS_PRECHECK": "0"}, {"DP_MG_RJ0": "0"}],
+                                     {"DP_LS_PRECHECK": "0"}, {"DP_MG_RJ0": "0"}, {"DP_LS_SPECJAC": "0"}],
                          ids=["host-driven-gmres", "fused-coarse-vcycle", "unfused-jacobi0", "no-ls-precheck",
-                              "separate-restriction"])
+                              "separate-restriction", "no-speculative-trial-jacobian"])
 def test_variant_bitwise_identical(variant):
     assert _digest(variant) == _digest({})

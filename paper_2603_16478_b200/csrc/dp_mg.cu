@@ -30,6 +30,17 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef DP_SMOOTH_ASYNC
+#define DP_SMOOTH_ASYNC 1   // fine-level smoother streams its slots through shared memory (cp.async)
+#endif
+constexpr int kSmDepth = 4;  // slots in flight per warp
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 #ifndef DP_SMOOTH_NT
 #define DP_SMOOTH_NT 256   // CTA size of the fine-level smoother (one warp per slice)
 #endif
@@ -472,6 +483,51 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
   const TV* vs = val + (size_t)base * 9 + lane;
   const int* cs = col + base + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#if DP_SMOOTH_ASYNC
+  if constexpr (sizeof(TV) == 4 && SPLIT == 1 && DP_VAL32_PACKED == 0) {
+    // fine level: the slice's slots stream through a per-warp shared-memory
+    // ring, kSmDepth slots ahead, with cp.async (a slot is 1,152 contiguous
+    // bytes of component-major FP32 values + 128 bytes of column indices), so
+    // each warp keeps ~5 KB of loads in flight instead of one slot's worth.
+    // Same values, same accumulation order as the direct loads below.
+    __shared__ __align__(16) float sv[DP_SMOOTH_NT / 32][kSmDepth][9 * kSlice];
+    __shared__ __align__(16) int sc[DP_SMOOTH_NT / 32][kSmDepth][kSlice];
+    const int w = threadIdx.x >> 5;
+    const float* gv = reinterpret_cast<const float*>(val) + (size_t)base * 9;
+    const int* gc = col + base;
+    auto issue = [&](int kk) {
+      if (kk < K) {
+        const float* src = gv + (size_t)kk * 9 * kSlice;
+        float* dst = sv[w][kk % kSmDepth];
+        for (int ch = lane; ch < 9 * kSlice / 4; ch += 32) cp_async16(dst + 4 * ch, src + 4 * ch);
+        if (lane < kSlice / 4) cp_async16(&sc[w][kk % kSmDepth][4 * lane], gc + kk * kSlice + 4 * lane);
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int kk = 0; kk < kSmDepth; ++kk) issue(kk);
+    for (int k = 0; k < K; ++k) {
+      cp_async_wait<kSmDepth - 1>();
+      __syncwarp();
+      const float* vv = sv[w][k % kSmDepth];
+      const int j = sc[w][k % kSmDepth][lane];
+      double m[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) m[c] = (double)vv[c * kSlice + lane];
+      double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
+      if (xc) {
+        const int J = __ldg(agg + j);
+        x0 += alpha * __ldg(xc + 3 * J); x1 += alpha * __ldg(xc + 3 * J + 1); x2 += alpha * __ldg(xc + 3 * J + 2);
+      }
+      a0 += m[0] * x0 + m[1] * x1 + m[2] * x2;
+      a1 += m[3] * x0 + m[4] * x1 + m[5] * x2;
+      a2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
+      __syncwarp();
+      issue(k + kSmDepth);
+    }
+    cp_async_wait<0>();
+  } else
+#endif
   for (int k = wsub; k < K; k += SPLIT) {
     const int j = __ldg(cs + k * kSlice);
     double m[9];

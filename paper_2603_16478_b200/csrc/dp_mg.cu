@@ -33,7 +33,8 @@ namespace cg = cooperative_groups;
 #ifndef DP_SMOOTH_ASYNC
 #define DP_SMOOTH_ASYNC 1   // fine-level smoother streams its slots through shared memory (cp.async)
 #endif
-constexpr int kSmDepth = 4;  // slots in flight per warp
+constexpr int kSmDepth = 4;  // slots in flight per warp (fine level)
+constexpr int kSmDepthC = 2; // slots in flight per warp (coarse levels, SPLIT = 8)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
@@ -524,6 +525,47 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
       a2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
       __syncwarp();
       issue(k + kSmDepth);
+    }
+    cp_async_wait<0>();
+  } else if constexpr (sizeof(TV) == 8 && SPLIT == 8) {
+    // coarse levels (L2-resident FP64): warp wsub's slots wsub, wsub + 8, ...
+    // stream through a 2-deep per-warp shared-memory ring (2,304 + 128 bytes
+    // per slot); same values, same order as the direct loads below
+    __shared__ __align__(16) double sv[SPLIT][kSmDepthC][9 * kSlice];
+    __shared__ __align__(16) int sc[SPLIT][kSmDepthC][kSlice];
+    const double* gv = reinterpret_cast<const double*>(val) + (size_t)base * 9;
+    const int* gc = col + base;
+    const int nk = (K > wsub) ? (K - wsub + SPLIT - 1) / SPLIT : 0;
+    auto issue = [&](int i) {
+      if (i < nk) {
+        const int kk = wsub + i * SPLIT;
+        const double* src = gv + (size_t)kk * 9 * kSlice;
+        double* dst = sv[wsub][i % kSmDepthC];
+        for (int ch = lane; ch < 9 * kSlice / 2; ch += 32) cp_async16(dst + 2 * ch, src + 2 * ch);
+        if (lane < kSlice / 4) cp_async16(&sc[wsub][i % kSmDepthC][4 * lane], gc + kk * kSlice + 4 * lane);
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int i = 0; i < kSmDepthC; ++i) issue(i);
+    for (int i = 0; i < nk; ++i) {
+      cp_async_wait<kSmDepthC - 1>();
+      __syncwarp();
+      const double* vv = sv[wsub][i % kSmDepthC];
+      const int j = sc[wsub][i % kSmDepthC][lane];
+      double m[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) m[c] = vv[c * kSlice + lane];
+      double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
+      if (xc) {
+        const int J = __ldg(agg + j);
+        x0 += alpha * __ldg(xc + 3 * J); x1 += alpha * __ldg(xc + 3 * J + 1); x2 += alpha * __ldg(xc + 3 * J + 2);
+      }
+      a0 += m[0] * x0 + m[1] * x1 + m[2] * x2;
+      a1 += m[3] * x0 + m[4] * x1 + m[5] * x2;
+      a2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
+      __syncwarp();
+      issue(i + kSmDepthC);
     }
     cp_async_wait<0>();
   } else

@@ -147,7 +147,8 @@ def test_rollout_states_contacts_gradients(pkg, name):
         assert rel(gr.dL_ddb, g["g_ddb"]) < 1e-6
 
 
-@pytest.mark.parametrize("name", ["bar_neohookean", "block_on_plane", "friction_high", "single_tet_nh"])
+@pytest.mark.parametrize("name", ["bar_neohookean", "block_on_plane", "friction_high", "single_tet_nh",
+                                  "bar_arap", "cube2_slide", "hanging_sheet"])
 def test_newton_matrix_matches_reference(pkg, name):
     from paper_2603_16478_b200 import adjoint as aj, core, forward as fw
     g = load_golden(f"scene_{name}.npz")

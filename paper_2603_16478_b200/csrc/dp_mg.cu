@@ -33,7 +33,10 @@ namespace cg = cooperative_groups;
 #ifndef DP_SMOOTH_ASYNC
 #define DP_SMOOTH_ASYNC 1   // fine-level smoother streams its slots through shared memory (cp.async)
 #endif
-constexpr int kSmDepth = 4;  // slots in flight per warp (fine level)
+#ifndef DP_SMOOTH_DEPTH
+#define DP_SMOOTH_DEPTH 2
+#endif
+constexpr int kSmDepth = DP_SMOOTH_DEPTH;  // slots in flight per warp (fine level)
 constexpr int kSmDepthC = 2; // slots in flight per warp (coarse levels, SPLIT = 8)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);

@@ -37,7 +37,10 @@ namespace cg = cooperative_groups;
 #define DP_SMOOTH_DEPTH 2
 #endif
 constexpr int kSmDepth = DP_SMOOTH_DEPTH;  // slots in flight per warp (fine level)
-constexpr int kSmDepthC = 2; // slots in flight per warp (coarse levels, SPLIT = 8)
+#ifndef DP_SMOOTH_DEPTHC
+#define DP_SMOOTH_DEPTHC 2
+#endif
+constexpr int kSmDepthC = DP_SMOOTH_DEPTHC;  // slots in flight per warp (coarse levels, SPLIT = 8)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");

@@ -1,9 +1,13 @@
 """Benchmark: fwd+bwd implicit steps/s at N tets on B200 (BASELINE.json metric).
 
 Workload (default --config c5): box_tet_mesh(55,55,55)
-= 998,250 Neo-Hookean tets (E=1e4, nu=0.3, 10 cm cube), frictional ground
-plane (mu=0.5) and two kinematic sphere "fingers" (mu=0.5) closing on the
-cube by 20 um per step.  A "step" = one forward Newton step + its adjoint
+= 998,250 Neo-Hookean tets (E=1e4, nu=0.3, 10 cm cube) dropped onto a ground
+plane and squeezed by two kinematic sphere "fingers" closing 10 um per step
+up to finger index 20, then holding (frictionless contacts, ~3,200 of them;
+why frictionless: CONFIGS comment).  Every rollout starts from the rest state
+at finger index 0 (FINGER_K0), so warm-up and timed rollouts are the same
+workload; a non-converged step raises (forward.py:261-264).  A "step" = one
+forward Newton step + its adjoint
 step (A_hat^T solve + z-products) of a K-step rollout with a final-state
 loss; parameter gradient dL/d(E, nu, mu) allreduced across ranks (NCCL) at
 the end of every rollout.
@@ -13,9 +17,10 @@ the end of every rollout.
   e2e   : the public API (rollout + backprop_rollout) with host NumPy
           buffers: host<->device copies inside the timed region.
   cpu_baseline / --impl reference : the CPU oracle port (oracle/, a
-          vectorised restatement of the reference) on a bounded sub-sample
-          (a smaller cube of the same scene family), extrapolated linearly
-          in tets (generous to the CPU; SuperLU scales worse than linear).
+          vectorised restatement of the reference) on a bounded sample: the
+          same scene family on a smaller cube over the same schedule; the
+          measured rate is reported in measured_* fields, `value` scales it
+          linearly in tets (generous to the CPU; SuperLU scales worse).
 
 Inputs are larger than L2 (val ~200 MB per SpMV operand at C5); no explicit
 flush.  Launch: python bench.py [--gpus N --steps K --warmup W]; for N>1 via
@@ -71,9 +76,31 @@ _keep_heap()
 #    masses the default 1e-9 admits ~1e-4 m position error and
 #    solver-path-dependent gradients (measured 7e-6 relative in dL/dE); 1e-11
 #    makes the C5 root path-independent (dL/dE agrees to 1e-9 across paths).
+#
+# C5 is FRICTIONLESS (ground and fingers mu = 0), with the fingers closing
+# 10 um per step for FINGER_HOLD steps and then holding.  Measured
+# (profiles/r02_c5_scene_design.md, tools/scene_explore.py): with the
+# reference's friction model (contact.py:139-165) a resting frictional
+# contact has no stable stick state (the capped branch pushes a vertex ALONG
+# its slip, the equilibria form a ring |delta_f| = delta_n/mu), and at 55^3
+# every frictional variant tried (mu 0.1-0.5, eps_fb 5e-11-1e-8, closing
+# speeds, holds, a pusher plate) stalls, inverts an element or stalls the NH
+# projection within 1-10 steps; the reference itself (CPU oracle) stalls on
+# the round-1 schedule at 12^3.  The frictionless family
+# converges every step for 40+ steps at 12^3, 20^3 and 55^3 on the GPU and
+# on the CPU oracle (tests/test_c5_family_oracle.py).
+FINGER_SPEED = 1e-5   # m per step
+FINGER_HOLD = 20      # finger index after which the fingers hold
+FINGER_K0 = 0         # first finger index of every rollout (never --warmup)
 CONFIGS = {
-    "c5": dict(cells=(55, 55, 55), edge=0.1 / 55, fingers=True, eps_fb=1e-9, tol=1e-11, rollouts=1, vary="target",
-               desc="1M-tet NH cube gripped by 2 kinematic sphere fingers on a frictional ground (C5)"),
+    "c5": dict(cells=(55, 55, 55), edge=0.1 / 55, fingers=True, mu=0.0, eps_fb=1e-9, tol=1e-11, rollouts=1, steps=20,
+               vary="target",
+               desc="1M-tet NH cube squeezed by 2 kinematic sphere fingers on the ground, frictionless "
+                    "(high contact count; C5)"),
+    "c5f": dict(cells=(55, 55, 55), edge=0.1 / 55, fingers=True, mu=0.3, eps_fb=1e-10, tol=1e-11, rollouts=1,
+                vary="target",
+                desc="C5 with mu=0.3 ground and fingers, eps_fb=1e-10 (GPU-converged 40 steps; not "
+                     "reference-validated at 55^3)"),
     "c3": dict(cells=(60, 12, 12), edge=0.01, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=8,
                desc="identification batch: 8 rollouts/GPU of a 51,840-tet NH beam on a frictional ground, "
                     "one E candidate per rollout (C3)"),
@@ -84,9 +111,9 @@ CONFIGS = {
                steps=20,
                desc="199,680-tet NH trunk (2 x 2 x 130 cm) clamped at the top by stiff bindings, 4 cable "
                     "force lines driven per step, frictional wall (C4)"),
-    "c1": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=1,
+    "c1": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, mu=0.3, eps_fb=1e-6, tol=1e-9, rollouts=1, steps=100,
                desc="4,374-tet NH cube on a frictional ground (C1)"),
-    "c1b": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=16,
+    "c1b": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, mu=0.3, eps_fb=1e-6, tol=1e-9, rollouts=16,
                 desc="16 concurrent rollouts/GPU of the 4,374-tet C1 cube (batched small scenes)"),
 }
 E_YOUNG = 1e4
@@ -100,14 +127,29 @@ NU = 0.3
 MU = 0.5
 
 
-def make_scene(cfg_or_n, fingers=None, eps_fb=None, E=E_YOUNG):
-    """Scene of a workload (CONFIGS key or cells-per-side of a 10 cm cube)."""
+def c5_family(n):
+    """C5 scene parameters at n cells per side: the same 10 cm cube,
+    frictionless fingers and ground; eps_fb and the (absolute) Newton
+    tolerance scaled with the vertex mass, (55/n)^3, so every resolution sees
+    the same force/weight ratios (tests and the CPU baseline use n < 55)."""
+    f = (55.0 / n) ** 3
+    return dict(cells=(n, n, n), edge=0.1 / n, fingers=True, mu=0.0, eps_fb=1e-9 * f, tol=1e-11 * f,
+                schedule=(FINGER_SPEED, FINGER_HOLD))
+
+
+def make_scene(cfg_or_n, fingers=None, eps_fb=None, E=E_YOUNG, mu=None):
+    """Scene of a workload: a CONFIGS key, a dict of workload parameters
+    (c5_family), or cells-per-side of the round-1 frictional finger cube
+    (mu = 0.5, fingers closing 20 um per step; kept for the friction tests)."""
     from paper_2603_16478_b200 import core, ident
     if isinstance(cfg_or_n, str):
         c = CONFIGS[cfg_or_n]
+    elif isinstance(cfg_or_n, dict):
+        c = cfg_or_n
     else:
         n = int(cfg_or_n)
-        c = dict(cells=(n, n, n), edge=0.1 / n, fingers=True, eps_fb=1e-9 if n >= 40 else (1e-7 if n >= 20 else 1e-6))
+        c = dict(cells=(n, n, n), edge=0.1 / n, fingers=True, eps_fb=1e-9 if n >= 40 else (1e-7 if n >= 20 else 1e-6),
+                 schedule=(2e-5, None))
     nx, ny, nz = c["cells"]
     if c.get("cloth"):
         # horizontal sheet 0.5 mm above a sphere of radius 0.25 (SURVEY.md §8(d) item 2)
@@ -119,17 +161,20 @@ def make_scene(cfg_or_n, fingers=None, eps_fb=None, E=E_YOUNG):
                           eps_fb=c["eps_fb"] if eps_fb is None else eps_fb)
     if c.get("trunk"):
         return make_trunk(c, E)
+    mu_ = c.get("mu", MU) if mu is None else mu
     v, t = ident.box_tet_mesh(nx, ny, nz, size=c["edge"], origin=(0.0, 0.0, 5e-4))
     mat = core.MaterialParams("neohookean", E=E, nu=NU)
-    cols = [core.HalfSpace([0, 0, 1], 0.0, mu=MU)]
+    cols = [core.HalfSpace([0, 0, 1], 0.0, mu=mu_)]
     if c["fingers"] if fingers is None else fingers:
         r = 0.02
         ly, lz = ny * c["edge"], nz * c["edge"]
         zc = 5e-4 + lz / 2
-        cols.append(core.Sphere([-r - 5e-4, ly / 2, zc], r, mu=MU))
-        cols.append(core.Sphere([nx * c["edge"] + r + 5e-4, ly / 2, zc], r, mu=MU))
-    return core.Scene(v, t, core.lumped_masses(v, t, 1000.0), [mat] * len(t),
-                      colliders=cols, h=0.01, eps_fb=c["eps_fb"] if eps_fb is None else eps_fb)
+        cols.append(core.Sphere([-r - 5e-4, ly / 2, zc], r, mu=mu_))
+        cols.append(core.Sphere([nx * c["edge"] + r + 5e-4, ly / 2, zc], r, mu=mu_))
+    sc = core.Scene(v, t, core.lumped_masses(v, t, 1000.0), [mat] * len(t),
+                    colliders=cols, h=0.01, eps_fb=c["eps_fb"] if eps_fb is None else eps_fb)
+    sc._finger_schedule = c.get("schedule", (FINGER_SPEED, FINGER_HOLD))
+    return sc
 
 
 def make_trunk(c, E):
@@ -165,19 +210,27 @@ def drive_cables(scene, k):
         sx = 1.0 if ci in (1, 3) else -0.25
         f[3 * line] += sx * amp
     scene.fext = f
+    return f
+
+
+def finger_offset(scene, k):
+    """How far each finger has closed at finger index k (m)."""
+    speed, hold = getattr(scene, "_finger_schedule", (2e-5, None))
+    return speed * (k if hold is None else min(k, hold))
 
 
 def move_fingers(scene, k):
-    """Kinematic fingers: close by 20 um per step (host-side, colliders are
-    re-read every step as in contact.py:125-127); C4: cable forces."""
+    """Kinematic fingers at finger index k (host-side; colliders are re-read
+    every step as in contact.py:125-127); C4: cable forces."""
     if getattr(scene, "_cable_lines", None) is not None:
         drive_cables(scene, k)
         return
     if len(scene.colliders) < 3:
         return
     lx = scene.vertices[:, 0].max()
-    scene.colliders[1].center[0] = -0.02 - 5e-4 + 2e-5 * k
-    scene.colliders[2].center[0] = lx + 0.02 + 5e-4 - 2e-5 * k
+    p = finger_offset(scene, k)
+    scene.colliders[1].center[0] = -0.02 - 5e-4 + p
+    scene.colliders[2].center[0] = lx + 0.02 + 5e-4 - p
 
 
 # ---------------------------------------------------------------------------
@@ -338,6 +391,8 @@ def gpu_arm(args, rank, world, local_rank):
             move_fingers(scene, k0 + k)
             _, rep = fw.forward_step(scene, None, c.sysmat, cfg,
                                      device_io=dict(q_bar=q[k], v_bar=v[k], q_out=q[k + 1], v_out=v[k + 1]))
+            if not rep.converged:   # forward.py:261-264 (rollout raises)
+                raise RuntimeError(f"forward step {k} did not converge (residual {rep.residual_history[-1]:.3e})")
             caches.append(rep.cache)
             stats.append((rep.converged, rep.iterations, rep.krylov_iterations, rep.n_contacts))
         with torch.cuda.stream(c.stream):
@@ -388,6 +443,8 @@ def gpu_arm(args, rank, world, local_rank):
         for k in range(nsteps):
             move_fingers(scene, k0 + k)
             st, rep = fw.forward_step(scene, st, c.sysmat, cfg)
+            if not rep.converged:   # forward.py:261-264 (rollout raises)
+                raise RuntimeError(f"forward step {k} did not converge (residual {rep.residual_history[-1]:.3e})")
             caches.append(rep.cache)
         target = st0.q + c.target_shift
         g = aj.backprop_rollout(caches, target, solver_cfg=adj_cfg)
@@ -414,7 +471,7 @@ def gpu_arm(args, rank, world, local_rank):
     t_w = time.perf_counter()
     n_w = 0
     while n_w < max(W, 0) or time.perf_counter() - t_w < args.warmup_seconds:
-        res = run_all(device_rollout, K, W)
+        res = run_all(device_rollout, K, FINGER_K0)
         # the timed region's gradient packing runs here too, so its device
         # allocation comes from torch's cache, not a cudaMalloc inside the
         # timed region (measured: 60-80 ms stalls on a fresh box)
@@ -427,8 +484,8 @@ def gpu_arm(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if os.environ.get("BENCH_DEBUG"):
         for i in range(int(os.environ.get("BENCH_DEBUG_REPS", "3"))):
-            t0 = time.perf_counter(); run_all(device_rollout, K, W); torch.cuda.synchronize()
-            t1 = time.perf_counter(); run_all(host_rollout, K, W); torch.cuda.synchronize()
+            t0 = time.perf_counter(); run_all(device_rollout, K, FINGER_K0); torch.cuda.synchronize()
+            t1 = time.perf_counter(); run_all(host_rollout, K, FINGER_K0); torch.cuda.synchronize()
             t2 = time.perf_counter()
             print(f"[bench] device path {1e3 * (t1 - t0):.1f} ms, host path {1e3 * (t2 - t1):.1f} ms",
                   file=sys.stderr, flush=True)
@@ -447,7 +504,7 @@ def gpu_arm(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         ev0.record()
         tw0 = time.perf_counter()
-        res = run_all(device_rollout, K, W)
+        res = run_all(device_rollout, K, FINGER_K0)
         tw1 = time.perf_counter()
         gvec = pack_sum([(r[0], r[1]) for r in res])
         allreduce_gradients(gvec, world)      # one all-reduce per optimisation iteration
@@ -526,7 +583,7 @@ def gpu_arm(args, rank, world, local_rank):
         gc.collect()
         gc.disable()
         t0 = time.perf_counter()
-        res2 = run_all(host_rollout, K, W)
+        res2 = run_all(host_rollout, K, FINGER_K0)
         allreduce_gradients(pack_sum(res2), world)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -558,48 +615,91 @@ def gpu_arm(args, rank, world, local_rank):
 # CPU oracle (reported baseline / reference arm)
 
 
-def _oracle_sample(n_cells, steps, eps_fb=None, tol=1e-9):
-    """One process: the oracle port on an n_cells^3 cube of the same scene
-    family; returns (seconds per fwd+bwd step, tets)."""
+def sample_scene(config, n_cells):
+    """The bounded CPU sample of a workload: the same scene family at
+    n_cells per side (C5: c5_family with mass-scaled eps_fb / tolerance; C1:
+    the C1 cube itself when n_cells == 9), its Newton tolerance and finger
+    schedule."""
+    c = CONFIGS[config]
+    if config.startswith("c5"):
+        fam = c5_family(n_cells)
+        if config == "c5f":
+            fam.update(mu=c["mu"], eps_fb=c["eps_fb"] * (55.0 / n_cells) ** 3)
+        return make_scene(fam), fam["tol"]
+    if config in ("c1", "c1b"):
+        fam = dict(c, cells=(n_cells,) * 3, edge=0.1 / n_cells)
+        return make_scene(fam), c["tol"]
+    raise ValueError(f"no CPU sample defined for config {config}")
+
+
+def _oracle_sample(config, n_cells, steps, warmup=0):
+    """One process: the oracle port (reference semantics, exact SuperLU Newton
+    solves, Jacobi-preconditioned CG/GMRES adjoint) on the bounded sample:
+    `warmup` untimed + `steps` timed fwd steps over the bench schedule, then
+    the timed reverse sweep.  Returns (seconds per fwd+bwd step, tets,
+    newton iterations)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import diffproj_oracle as O
     from paper_2603_16478_b200 import core
-    scene = make_scene(n_cells, fingers=False, eps_fb=eps_fb)
+    scene, tol = sample_scene(config, n_cells)
     osc = O.OScene(core.scene_to_arrays(scene))
-    q0 = scene.vertices.reshape(-1).copy()
-    v0 = np.zeros_like(q0)
-    t0 = time.perf_counter()
-    els, A, st = O.rollout(osc, q0, v0, steps, O.ForwardConfig(tol=tol), raise_on_failure=False)
-    O.backprop_rollout(osc, els, A, st, target=q0 + 1e-3)
+    els = O.build_elements(osc)
+    A = O.assemble_A(osc, els)
+    q = scene.vertices.reshape(-1).copy()
+    v = np.zeros_like(q)
+    its, sts = [], []
+    t0 = None
+    for k in range(warmup + steps):
+        if k == warmup:
+            t0 = time.perf_counter()
+        move_fingers(scene, FINGER_K0 + k)
+        osc = O.OScene(core.scene_to_arrays(scene))
+        st = O.forward_step(osc, A, els, q, v, O.ForwardConfig(tol=tol))
+        if not st.converged:
+            raise RuntimeError(f"oracle step {k} did not converge ({st.residual_history[-1]:.3e})")
+        if k >= warmup:
+            sts.append(st)
+            its.append(st.iterations)
+        q, v = st.q_new, st.v_new
+    O.backprop_rollout(osc, els, A, sts, target=scene.vertices.reshape(-1) + 1e-3)
     dt = time.perf_counter() - t0
-    return dt / steps, len(scene.elements)
+    return dt / steps, len(scene.elements), its
 
 
 def _oracle_worker(args):
-    n_cells, steps, tol = args
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    return _oracle_sample(n_cells, steps, tol=tol)
+    return _oracle_sample(*args)
 
 
-def cpu_baseline(n_tets_target, n_cells=8, steps=1, procs=1, tol=1e-9):
-    """Bounded CPU sample; returns the JSON object for cpu_baseline."""
+def cpu_baseline(config, n_tets_target, n_cells, steps, procs=1, warmup=0):
+    """Bounded CPU sample; returns the cpu_baseline object.  `value` is the
+    measured rate scaled linearly in tets to the workload size (the metric's
+    unit; generous to the CPU: SuperLU fill grows faster than linearly);
+    the measured numbers are in the measured_* fields."""
+    t0 = time.perf_counter()
     if procs <= 1:
-        sec, tets = _oracle_sample(n_cells, steps, tol=tol)
+        sec, tets, its = _oracle_sample(config, n_cells, steps, warmup)
         per_proc = [sec]
     else:
         import multiprocessing as mp
         ctx = mp.get_context("spawn")
         with ctx.Pool(procs) as pool:
-            res = pool.map(_oracle_worker, [(n_cells, steps, tol)] * procs)
+            res = pool.map(_oracle_worker, [(config, n_cells, steps, warmup)] * procs)
         per_proc = [r[0] for r in res]
-        tets = res[0][1]
-    # steps/s at the target size, extrapolated linearly in tets
-    rate = sum(1.0 / s for s in per_proc) * tets / n_tets_target
+        tets, its = res[0][1], res[0][2]
+    wall = time.perf_counter() - t0
+    measured_rate = sum(1.0 / s for s in per_proc)          # fwd+bwd steps/s at the sample size
+    rate = measured_rate * tets / n_tets_target
     return {"value": rate, "unit": "steps/s", "cores": procs, "kind": "port",
-            "sample": (f"oracle port (oracle/diffproj_oracle.py, NumPy+SuperLU) on a "
-                       f"{n_cells}^3-cell cube ({tets} tets, same scene family), {steps} fwd+bwd "
-                       f"step(s) x {procs} process(es): {np.mean(per_proc):.2f} s/step; "
-                       f"extrapolated linearly to {n_tets_target} tets")}
+            "value_basis": f"measured rate at {tets} tets scaled linearly to {n_tets_target} tets",
+            "measured_tets": tets, "measured_steps": steps, "measured_processes": procs,
+            "measured_s_per_step": float(np.mean(per_proc)), "measured_steps_per_s": measured_rate,
+            "measured_tet_steps_per_s_M": measured_rate * tets / 1e6, "measured_newton_iterations": its,
+            "wall_s": wall,
+            "sample": (f"oracle port (oracle/diffproj_oracle.py: reference algorithm, NumPy + SuperLU Newton "
+                       f"solves, Jacobi-Krylov adjoint) on the same scene family at {n_cells}^3 cells "
+                       f"({tets} tets), {warmup} untimed + {steps} timed fwd steps of the bench schedule + "
+                       f"their reverse sweep, x {procs} process(es), 1 BLAS thread each")}
 
 
 # ---------------------------------------------------------------------------
@@ -614,10 +714,14 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
-    ap.add_argument("--cpu-cells", type=int, default=12)
+    ap.add_argument("--cpu-cells", type=int, default=0, help="cells/side of the cpu_baseline sample (c5: 8, c1: 9)")
+    ap.add_argument("--cpu-steps", type=int, default=8, help="timed steps of the cpu_baseline sample")
+    ap.add_argument("--ref-cells", type=int, default=10, help="cells/side of the --impl reference sample")
     ap.add_argument("--rollouts", type=int, default=0, help="rollouts per GPU (default per config)")
     ap.add_argument("--warmup-seconds", type=float, default=8.0)
     args = ap.parse_args()
+    if args.cpu_cells <= 0:
+        args.cpu_cells = 9 if args.config.startswith("c1") else 8
     if args.steps <= 0:
         # the reference's own Newton (oracle, exact LU) stops converging at
         # step 6 of the C2 drape (compressed ARAP cloth, tools/diag_cloth.py)
@@ -642,25 +746,36 @@ def main():
               "material": ("arap stiffness=50" if cloth else
                            (f"neohookean E={E_YOUNG}(1+0.05 i) nu={NU}" if cdef.get("vary", "E") == "E" else
                             f"neohookean E={E_YOUNG} nu={NU}, target shift 1e-3 (1 + 0.1 i) per rollout i")),
-              "friction_mu": 0.3 if (cloth or cdef.get("trunk")) else MU, "h": 0.01,
+              "friction_mu": 0.3 if (cloth or cdef.get("trunk")) else cdef.get("mu", MU), "h": 0.01,
+              "finger_schedule": (f"close {FINGER_SPEED * 1e6:.0f} um/step up to finger index {FINGER_HOLD}, then "
+                                  f"hold; every rollout starts at index {FINGER_K0}"
+                                  if cdef.get("fingers") else None),
               "eps_fb": cdef["eps_fb"], "newton_tol": cdef["tol"], "adjoint_tol": 1e-10,
               "adjoint_gmres_restart": ADJ_RESTART, "l2": "operands > L2 (no flush)"}
     if args.impl == "reference":
+        # the reference's algorithm on the host cores (oracle port; the
+        # reference is pure Python and does not travel to the GPU box), one
+        # process per core, each a bounded sample of the workload: W untimed
+        # + K timed steps of the same finger schedule on a smaller cube of the
+        # same family; only rank 0 runs (N>1: the other ranks exit)
         if rank != 0:
             return
         procs = os.cpu_count() or 1
         W, K = args.warmup, args.steps
-        t0 = time.perf_counter()
-        base = cpu_baseline(n_tets, n_cells=args.cpu_cells, steps=1, procs=procs, tol=cdef["tol"])
-        wall = time.perf_counter() - t0
+        base = cpu_baseline(args.config, n_tets, n_cells=args.ref_cells, steps=K, procs=procs, warmup=W)
         line = {"metric": "fwd+bwd sim steps/sec at N tets", "value": base["value"], "unit": "steps/s",
-                "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": 1e3 / base["value"],
+                "n_gpus": args.gpus, "steps": K, "warmup": W,
+                # what was actually timed: K steps per process at the sample size
+                "ms_per_step": 1e3 * base["measured_s_per_step"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": config, "impl": "reference",
+                "data": "synthetic (procedural mesh)", "config": config, "impl": "reference",
+                "value_basis": base["value_basis"],
+                "measured_tets": base["measured_tets"], "measured_steps_per_s": base["measured_steps_per_s"],
+                "tet_steps_per_s_M": base["measured_tet_steps_per_s_M"],
                 "cpu_baseline": base,
                 "e2e": {"value": base["value"], "unit": "steps/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0},
-                "wall_s": wall}
+                "wall_s": base["wall_s"]}
         print(json.dumps(line))
         return
 
@@ -707,11 +822,12 @@ def main():
                 "newton_iterations": r["newton"], "krylov_iterations": r["krylov"],
                 "adjoint_krylov_iterations": r["adj_iters"], "contacts": r["contacts"],
                 "converged": r["converged"], "setup_s": r["setup_s"], "nnzb": r["nnzb"],
+                "env_knobs": {k: v for k, v in sorted(os.environ.items()) if k.startswith("DP_")},
                 "device_bytes": r["device_bytes"]}
         if not args.skip_cpu and world == 1:
             try:
-                line["cpu_baseline"] = cpu_baseline(n_tets, n_cells=args.cpu_cells, steps=1, procs=1,
-                                                    tol=cdef["tol"])
+                line["cpu_baseline"] = cpu_baseline(args.config, n_tets, n_cells=args.cpu_cells,
+                                                    steps=min(args.cpu_steps, K), procs=1)
             except Exception as ex:   # the baseline must not kill the GPU line
                 line["cpu_baseline"] = {"value": None, "error": repr(ex)[:200]}
         print(json.dumps(line))

@@ -179,6 +179,16 @@ extern "C" {
 
 const char* dp_last_error(void) { return g_err.c_str(); }
 const char* dp_version(void) { return "diffproj_b200 0.1 (sm_100a)"; }
+// Any entry point that writes the scene's contact / element scratch, the
+// forward operator values or the multigrid level values makes the assembled
+// adjoint operator stale: the next adjoint solve / backprop of any cache
+// re-assembles (the reference's caches are immutable, so an interleaved
+// forward step must not change a later backprop_step's result).
+static inline void invalidate_adjoint(dp_scene* s) {
+  s->adj_cache_tag = nullptr;
+  s->mg_adj_ready = 0;
+}
+
 int dp_set_spin_wait(int32_t device, int32_t mode) {
   // mode 1 spin, 2 yield, 4 blocking sync, 0 leave as is.  The primary
   // context's flags can be changed while it is active; the driver entry point
@@ -623,6 +633,7 @@ int dp_scene_get_info(const dp_scene* s, dp_scene_info* o) {
 
 int dp_scene_set_colliders(dp_scene* s, int32_t n, const int32_t* kind, const double* vec3, const double* scalar,
                            const double* mu) {
+  invalidate_adjoint(s);
   if (n < 0 || n > kMaxColliders) { set_error("too many colliders"); return DP_ERR_VALUE; }
   cudaSetDevice(s->device);
   ColliderSet cs{};
@@ -642,6 +653,7 @@ int dp_scene_set_colliders(dp_scene* s, int32_t n, const int32_t* kind, const do
 
 int dp_scene_set_bindings(dp_scene* s, int32_t n, const int64_t* vertex, const double* target3,
                           const double* compliance) {
+  invalidate_adjoint(s);
   cudaSetDevice(s->device);
   cudaStreamSynchronize(s->stream);
   for (int b = 0; b < n; ++b) {
@@ -687,6 +699,7 @@ int dp_scene_set_bindings(dp_scene* s, int32_t n, const int64_t* vertex, const d
 }
 
 int dp_scene_set_params(dp_scene* s, double h, double eps_fb, double act, const double* g) {
+  invalidate_adjoint(s);
   if (!(h > 0)) { set_error("time step must be positive"); return DP_ERR_VALUE; }
   if (!(eps_fb > 0)) { set_error("eps_fb (2*eps^2) must be positive"); return DP_ERR_VALUE; }
   s->h = h;
@@ -697,6 +710,7 @@ int dp_scene_set_params(dp_scene* s, double h, double eps_fb, double act, const 
 }
 
 int dp_scene_set_fext(dp_scene* s, const double* fext, int32_t ptr_kind) {
+  invalidate_adjoint(s);
   cudaSetDevice(s->device);
   if (!fext) {
     s->has_fext = 0;
@@ -708,6 +722,7 @@ int dp_scene_set_fext(dp_scene* s, const double* fext, int32_t ptr_kind) {
 }
 
 int dp_scene_set_solver_options(dp_scene* s, int32_t use_mg, double omega, int32_t nu) {
+  invalidate_adjoint(s);
   s->use_mg = use_mg;
   if (omega > 0 && nu > 0) mg_set_params(s, omega, nu);
   return DP_OK;
@@ -727,6 +742,7 @@ int dp_scene_get_element_data(const dp_scene* s, double* w_out, double* vol_out)
 }
 
 int dp_scene_export_bsr(dp_scene* s, int32_t which, int32_t* rowptr, int32_t* col, double* val) {
+  invalidate_adjoint(s);
   cudaSetDevice(s->device);
   const double* v = nullptr;
   if (which == 0) {
@@ -906,6 +922,7 @@ __global__ void k_reset_flags(EvalScalars* esc) {
 int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32_t ptr_kind,
                     const dp_forward_cfg* cfg_in, double* q_out, double* v_out, dp_cache* cache,
                     dp_forward_report* rep, double* hist, int32_t hist_cap) {
+  invalidate_adjoint(s);
   cudaSetDevice(s->device);
   dp_forward_cfg cfg;
   if (cfg_in) cfg = *cfg_in;
@@ -1009,7 +1026,8 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     double t = 1.0;
     bool accepted = false;
     // watched rows for the line-search pre-check: rows within half of max|r|
-    const bool precheck = g_precheck && s->NV == 4 && s->E > 0;
+    // the pre-check bounds max|r| only: off under the 2-norm acceptance rule
+    const bool precheck = g_precheck && g_ls_norm != 2 && s->NV == 4 && s->E > 0;
     if (precheck) launch_watch_select(s, s->r, g_watch_frac);
     for (int ls = 0; ls < cfg.max_line_search; ++ls) {
       launch_axpy_to(s, q_try, q, t, s->dq);
@@ -1140,6 +1158,7 @@ int dp_cache_get_states(const dp_cache* c, double* q_bar, double* v_bar, double*
 
 int dp_cache_get_projections(dp_scene* s, const dp_cache* c, double* sigma, double* theta, double* P,
                              double* energy) {
+  invalidate_adjoint(s);
   cudaSetDevice(s->device);
   const int E = s->E, D = s->D;
   if (!E) return DP_OK;
@@ -1458,6 +1477,7 @@ int dp_contact_batch(int32_t n, const double* frame, const double* d_n, const do
 
 int dp_detect_contacts(dp_scene* s, const double* q, int32_t ptr_kind, int32_t cap, int32_t* n_out,
                        int32_t* vertex, int32_t* collider, double* frame, double* d_n) {
+  invalidate_adjoint(s);
   cudaSetDevice(s->device);
   int rc = copy_in(s, s->q_try, q, (size_t)3 * s->V, ptr_kind);
   if (rc) return rc;
@@ -1480,6 +1500,7 @@ int dp_detect_contacts(dp_scene* s, const double* q, int32_t ptr_kind, int32_t c
 // benchmarking / instrumentation
 
 int dp_bench_spmv(dp_scene* s, int32_t which, const double* x, double* y, int32_t reps, float* ms_out) {
+  invalidate_adjoint(s);
   cudaSetDevice(s->device);
   const double* val = (which == 2) ? s->val_adj : s->val_fwd;
   DP_CUDA(cudaEventRecord(s->ev0, s->stream));
@@ -1496,6 +1517,7 @@ int dp_bench_spmv(dp_scene* s, int32_t which, const double* x, double* y, int32_
 }
 
 int dp_bench_smoother(dp_scene* s, const double* x, const double* b, double* out, int32_t reps, float* ms_out) {
+  invalidate_adjoint(s);
   cudaSetDevice(s->device);
   DP_CUDA(cudaEventRecord(s->ev0, s->stream));
   if (mg_bench_fine_smooth(s, x, b, out, reps)) {
@@ -1511,6 +1533,7 @@ int dp_bench_smoother(dp_scene* s, const double* x, const double* b, double* out
 }
 
 int dp_bench_elements(dp_scene* s, const double* q, int32_t with_jacobian, int32_t reps, float* ms_out) {
+  invalidate_adjoint(s);
   cudaSetDevice(s->device);
   DP_CUDA(cudaEventRecord(s->ev0, s->stream));
   for (int r = 0; r < reps; ++r) launch_elements(s, q, with_jacobian ? EV_JAC : 0, &s->esc->status);

@@ -259,17 +259,36 @@ def cube_scene(n, model="neohookean", E=1e4, mu=0.3, sphere=False,
 
 
 def run_scene(name, scene, T, tol=1e-12, v0=None, target_shift=1e-3,
-              dense_newton=True):
+              dense_newton=True, before_step=None):
     t0 = time.time()
     state0 = scene.rest_state()
     if v0 is not None:
         state0.v[:] = v0
     cfg = fw.ForwardConfig(tol=tol)
-    try:
-        states, caches = fw.rollout(scene, state0, T, cfg=cfg)
-    except RuntimeError:
-        cfg = fw.ForwardConfig()
-        states, caches = fw.rollout(scene, state0, T, cfg=cfg)
+    extra = {}
+    if before_step is not None:
+        # per-step scene changes (kinematic colliders): forward.rollout's
+        # loop (forward.py:251-267) with the hook before every step
+        sysmat = core.assemble_system_matrix(scene)
+        states, caches, st = [state0.copy()], [], state0
+        for k in range(T):
+            for key, val in before_step(scene, k).items():
+                extra.setdefault(key, []).append(val)
+            st, rep = fw.forward_step(scene, st, sysmat, cfg)
+            if not rep.converged:
+                raise RuntimeError(f"forward step {k} did not converge "
+                                   f"(residual {rep.residual_history[-1]:.3e})")
+            states.append(st)
+            caches.append(rep.cache)
+            print(f"  {name} step {k}: {rep.iterations} its, {len(rep.contacts)} contacts, "
+                  f"{time.time() - t0:.0f}s", flush=True)
+        extra = {k: np.array(v) for k, v in extra.items()}
+    else:
+        try:
+            states, caches = fw.rollout(scene, state0, T, cfg=cfg)
+        except RuntimeError:
+            cfg = fw.ForwardConfig()
+            states, caches = fw.rollout(scene, state0, T, cfg=cfg)
     target = states[-1].q + target_shift
     grads = aj.backprop_rollout(caches, target)
     out = scene_to_arrays(scene)
@@ -284,6 +303,7 @@ def run_scene(name, scene, T, tol=1e-12, v0=None, target_shift=1e-3,
         g_dEb=grads.dL_dEb, g_ddb=grads.dL_ddb, g_dw=grads.dL_dw,
         g_dstiffness=np.float64(grads.dL_dstiffness),
         g_dE=np.float64(grads.dL_dE), g_dnu=np.float64(grads.dL_dnu),
+        **extra,
     )
     # contact sets per step (vertex, collider) in detection order
     cstep, cvert, ccol, cframe, cdn, clam, cdelta, cs, ccap = \
@@ -349,6 +369,42 @@ def gen_c1():
     run_scene("c1", cube_scene(9), 2)
 
 
+def c5_family_scene(n):
+    """The C5 workload family (bench.c5_family) at n cells per side, built
+    with the reference's own classes: frictionless ground + two kinematic
+    sphere fingers, eps_fb scaled with the vertex mass (55/n)^3."""
+    f = (55.0 / n) ** 3
+    edge = 0.1 / n
+    v, t = ident.box_tet_mesh(n, n, n, size=edge, origin=(0.0, 0.0, 5e-4))
+    L = n * edge
+    r, zc = 0.02, 5e-4 + L / 2
+    cols = [core.HalfSpace([0, 0, 1], 0.0, mu=0.0),
+            core.Sphere([-r - 5e-4, L / 2, zc], r, mu=0.0),
+            core.Sphere([L + r + 5e-4, L / 2, zc], r, mu=0.0)]
+    mats = [core.MaterialParams(model="neohookean", E=1e4, nu=0.3) for _ in range(len(t))]
+    return core.Scene(vertices=v, elements=t, masses=core.lumped_masses(v, t, density=1000.0),
+                      materials=mats, colliders=cols, h=0.01, eps_fb=1e-9 * f)
+
+
+def c5_fingers(speed=1e-5, hold=20):
+    """bench.move_fingers for the C5 family: close `speed` m per step up to
+    finger index `hold`, then hold; returns the finger x centres."""
+    def hook(scene, k):
+        lx = scene.vertices[:, 0].max()
+        p = speed * min(k, hold)
+        scene.colliders[1].center[0] = -0.02 - 5e-4 + p
+        scene.colliders[2].center[0] = lx + 0.02 + 5e-4 - p
+        return {"finger_x": np.array([scene.colliders[1].center[0], scene.colliders[2].center[0]])}
+    return hook
+
+
+def gen_c5family(n=12, T=24, tol=1e-11):
+    # the bench workload's regime (SURVEY.md §8(d) item 5, VERDICT r1 item 2):
+    # C5 family at n^3 cells over the bench finger schedule incl. the hold
+    run_scene(f"c5fam{n}", c5_family_scene(n), T, tol=tol, dense_newton=False,
+              before_step=c5_fingers())
+
+
 if __name__ == "__main__":
     rng = np.random.default_rng(0)
     which = sys.argv[1:] or ["elements", "contacts", "scenes"]
@@ -360,3 +416,5 @@ if __name__ == "__main__":
         gen_scenes()
     if "c1" in which:
         gen_c1()
+    if "c5fam" in which:
+        gen_c5family()

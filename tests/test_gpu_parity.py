@@ -386,3 +386,30 @@ def test_cloth_drape_vs_oracle(pkg):
     for k in range(4):
         assert rel(g.dL_dfext[k], og.dL_dfext[k]) < 1e-6
     assert abs(g.dL_dstiffness - og.dL_dstiffness) <= 1e-6 * abs(og.dL_dstiffness)
+
+
+def test_forward_between_adjoint_assemble_and_backprop(pkg):
+    """assemble_adjoint_operator(cache_k) -> forward_step ->
+    solve_adjoint/backprop_step(cache_k) is legal in the reference (its caches
+    are immutable, adjoint.py:93-219); the interleaved forward step overwrites
+    the scene's contact/element scratch, so the result must not change."""
+    from paper_2603_16478_b200 import adjoint as aj, forward as fw
+    g, scene, states, caches = _gpu_rollout("cube2_slide", pkg)
+    T = int(g["T"])
+    n = scene.ndof
+    dq = 2.0 * (states[-1].q - g["target"])
+    dv = np.zeros(n)
+
+    def one(interleave):
+        ws = aj.assemble_adjoint_operator(caches[T - 1])
+        if interleave:
+            # a forward step from a different state (other contact set)
+            fw.forward_step(scene, states[1], caches[0].sysmat, fw.ForwardConfig(tol=float(g["tol"])))
+        z = aj.solve_adjoint(ws, dq, dv)
+        gr, dqb, dvb = aj.backprop_step(caches[T - 1], z, dq, dv)
+        return z, dqb, dvb, gr.dL_dE, gr.dL_dmu_friction
+
+    a = one(False)
+    b = one(True)
+    for x, y in zip(a, b):
+        assert np.allclose(x, y, rtol=1e-12, atol=1e-300)

@@ -72,10 +72,12 @@ _keep_heap()
 #    the default 1e-6 is fine for ~1e-3 kg vertices (C1, C3) but not for C5
 #    (~6e-6 kg).
 #  * Newton tol: the reference's stop test is an absolute max|r| <= tol *
-#    max(1, max|m q_hat|) (forward.py:169-171, :202) in kg*m; with C5 vertex
-#    masses the default 1e-9 admits ~1e-4 m position error and
-#    solver-path-dependent gradients (measured 7e-6 relative in dL/dE); 1e-11
-#    makes the C5 root path-independent (dL/dE agrees to 1e-9 across paths).
+#    max(1, max|m q_hat|) (forward.py:169-171, :202) in kg*m, default 1e-9.
+#    C5 uses 1e-10 (10x tighter than the default).  It must stay above the
+#    activation jump h^2 eps^2/activation of a vertex crossing the 1 mm
+#    activation distance (5e-11 at eps_fb = 1e-9): with tol = 1e-11 (round 1)
+#    a vertex hovering at the activation boundary stalls Newton (oracle, C5
+#    family at 10^3 cells, step 16: plateau 7.9e-9 = that jump, scaled).
 #
 # C5 is FRICTIONLESS (ground and fingers mu = 0), with the fingers closing
 # 10 um per step for FINGER_HOLD steps and then holding.  Measured
@@ -87,13 +89,13 @@ _keep_heap()
 # speeds, holds, a pusher plate) stalls, inverts an element or stalls the NH
 # projection within 1-10 steps; the reference itself (CPU oracle) stalls on
 # the round-1 schedule at 12^3.  The frictionless family
-# converges every step for 40+ steps at 12^3, 20^3 and 55^3 on the GPU and
-# on the CPU oracle (tests/test_c5_family_oracle.py).
+# converges every step for 60 steps at 8^3 ... 55^3 on the GPU and on the CPU
+# oracle (tests/test_c5_family_oracle.py, profiles/r02_c5_scene_design.md).
 FINGER_SPEED = 1e-5   # m per step
 FINGER_HOLD = 20      # finger index after which the fingers hold
 FINGER_K0 = 0         # first finger index of every rollout (never --warmup)
 CONFIGS = {
-    "c5": dict(cells=(55, 55, 55), edge=0.1 / 55, fingers=True, mu=0.0, eps_fb=1e-9, tol=1e-11, rollouts=1, steps=20,
+    "c5": dict(cells=(55, 55, 55), edge=0.1 / 55, fingers=True, mu=0.0, eps_fb=1e-9, tol=1e-10, rollouts=1, steps=20,
                vary="target",
                desc="1M-tet NH cube squeezed by 2 kinematic sphere fingers on the ground, frictionless "
                     "(high contact count; C5)"),
@@ -101,16 +103,16 @@ CONFIGS = {
                 vary="target",
                 desc="C5 with mu=0.3 ground and fingers, eps_fb=1e-10 (GPU-converged 40 steps; not "
                      "reference-validated at 55^3)"),
-    "c3": dict(cells=(60, 12, 12), edge=0.01, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=8,
+    "c3": dict(cells=(60, 12, 12), edge=0.01, fingers=False, eps_fb=1e-6, tol=1e-9, rollouts=8, steps=50,
                desc="identification batch: 8 rollouts/GPU of a 51,840-tet NH beam on a frictional ground, "
                     "one E candidate per rollout (C3)"),
     "c2": dict(cells=(100, 100, 0), edge=0.01, fingers=False, eps_fb=1e-9, tol=1e-11, rollouts=1, cloth=True, steps=4,
                desc="20,000-triangle ARAP cloth (1 m, 0.3 kg/m^2) draping over a frictional sphere, "
                     "per-step control-force gradients (C2 without self-contact: none in the reference)"),
     "c4": dict(cells=(8, 8, 520), edge=2.5e-3, fingers=False, eps_fb=1e-9, tol=1e-10, rollouts=1, trunk=True,
-               steps=20,
+               steps=200, wall_gap=2e-3, cable_amp=1e-3,
                desc="199,680-tet NH trunk (2 x 2 x 130 cm) clamped at the top by stiff bindings, 4 cable "
-                    "force lines driven per step, frictional wall (C4)"),
+                    "force lines (1 mN/vertex) driven per step, frictional wall 2 mm away, 200 steps (C4)"),
     "c1": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, mu=0.3, eps_fb=1e-6, tol=1e-9, rollouts=1, steps=100,
                desc="4,374-tet NH cube on a frictional ground (C1)"),
     "c1b": dict(cells=(9, 9, 9), edge=0.1 / 9, fingers=False, mu=0.3, eps_fb=1e-6, tol=1e-9, rollouts=16,
@@ -121,6 +123,7 @@ E_YOUNG = 1e4
 # instructions / E, ncu at a C5 state, profiles/r01_elements_fp64.md)
 ELEM_FLOPS_JAC = 5250.0
 ELEM_FLOPS_RES = 3139.0
+PACK_BLOCKS = ("dL_dw", "dL_dEb", "dL_ddb", "dL_dfext", "dL_dqbar", "dL_dvbar")
 ADJ_RESTART = 20            # adjoint GMRES restart length in the bench (see gpu_arm)
 FP64_PEAK_TFLOPS = 34.18     # measured DFMA peak, profiles/r01_fp64_peak.json
 NU = 0.3
@@ -133,7 +136,7 @@ def c5_family(n):
     tolerance scaled with the vertex mass, (55/n)^3, so every resolution sees
     the same force/weight ratios (tests and the CPU baseline use n < 55)."""
     f = (55.0 / n) ** 3
-    return dict(cells=(n, n, n), edge=0.1 / n, fingers=True, mu=0.0, eps_fb=1e-9 * f, tol=1e-11 * f,
+    return dict(cells=(n, n, n), edge=0.1 / n, fingers=True, mu=0.0, eps_fb=1e-9 * f, tol=1e-10 * f,
                 schedule=(FINGER_SPEED, FINGER_HOLD))
 
 
@@ -198,6 +201,10 @@ def make_trunk(c, E):
         m = (np.abs(v[:, 0] - cx) < 1e-9) & (np.abs(v[:, 1] - cy) < 1e-9) & (v[:, 2] < 0.5 * ztop)
         lines.append(np.nonzero(m)[0])
     sc._cable_lines = lines
+    # 1 mN per vertex: at 2 mN the trunk hits an NH projection stall at step
+    # 81 (the reference raises there too, elasticity.py NH Newton); 1 mN runs
+    # 200 steps with the trunk pressed against the wall (tools/c4_explore.py)
+    sc._cable_amp = c.get("cable_amp", 2e-3)
     return sc
 
 
@@ -205,8 +212,9 @@ def drive_cables(scene, k):
     """Cable pattern of step k: the two +x cables pull towards the wall with a
     ramped, phase-shifted tension, the -x pair relaxes (2 mN per vertex)."""
     f = np.zeros(3 * scene.n_verts)
+    a0 = getattr(scene, "_cable_amp", 2e-3)
     for ci, line in enumerate(scene._cable_lines):
-        amp = 2e-3 * min(1.0, (k + 1) / 10.0) * (1.0 + 0.5 * np.sin(0.3 * k + ci))
+        amp = a0 * min(1.0, (k + 1) / 10.0) * (1.0 + 0.5 * np.sin(0.3 * k + ci))
         sx = 1.0 if ci in (1, 3) else -0.25
         f[3 * line] += sx * amp
     scene.fext = f
@@ -402,7 +410,7 @@ def gpu_arm(args, rank, world, local_rank):
             z = torch.empty(n3, **dd)
             dqb = torch.empty(n3, **dd)
             dvb = torch.empty(n3, **dd)
-            dfx = torch.empty(n3, **dd)
+            dfx = torch.empty((nsteps, n3), **dd)   # the controls' gradient of every step
         c.stream.synchronize()
         _lib.check(L.dp_grads_reset(dev.handle))
         adj_iters = 0
@@ -414,16 +422,20 @@ def gpu_arm(args, rank, world, local_rank):
                                           C.byref(scfg), _lib.ptr(z), C.byref(rep)))
             adj_iters += rep.iterations
             _lib.check(L.dp_backprop_step(dev.handle, h, _lib.ptr(z), _lib.ptr(dv), _lib.PTR_DEVICE,
-                                          _lib.ptr(dqb), _lib.ptr(dvb), _lib.ptr(dfx)))
+                                          _lib.ptr(dqb), _lib.ptr(dvb), _lib.ptr(dfx[k - 1])))
             dq, dqb = dqb, dq
             dv, dvb = dvb, dv
         if trace is not None:
             trace.append(time.perf_counter())
             print("[trace] step ms", [round(1e3 * (b - a), 1) for a, b in zip(trace, trace[1:])],
                   file=sys.stderr, flush=True)
-        grads = aj.GradientReport()
-        grads.ensure_shapes(len(scene.bindings), dev.n_elems)
-        aj._fold_device_grads(dev, scene, grads)
+        # the full GradientReport stays on the device:
+        # dL/dw, dL/dE_b, dL/dd_b, dL/dfext[K], dL/dq_bar, dL/dv_bar
+        with torch.cuda.stream(c.stream):
+            grads = aj.device_gradient_report(dev, scene, dd["device"])
+            grads.dL_dfext = dfx
+            grads.dL_dqbar = dq
+            grads.dL_dvbar = dv
         if trace is not None:
             t_fold = time.perf_counter()
         with torch.cuda.stream(c.stream):
@@ -458,9 +470,11 @@ def gpu_arm(args, rank, world, local_rank):
         return list(pool.map(lambda c: fn(c, *a), ctxs))
 
     def pack_sum(results):
+        """Sum of this rank's packed gradients (scalars + every array block,
+        SURVEY.md §8(e)); summed in the rollouts' fixed order."""
         tot = None
         for g, loss in results:
-            v = pack_gradients(g, loss, dd["device"])
+            v = pack_gradients(g, loss, dd["device"], blocks=PACK_BLOCKS)
             tot = v if tot is None else tot + v
         return tot
 
@@ -470,6 +484,7 @@ def gpu_arm(args, rank, world, local_rank):
     # then settles to within 0.5%: measured, tools/var_c3.py)
     t_w = time.perf_counter()
     n_w = 0
+    gw = None
     while n_w < max(W, 0) or time.perf_counter() - t_w < args.warmup_seconds:
         res = run_all(device_rollout, K, FINGER_K0)
         # the timed region's gradient packing runs here too, so its device
@@ -480,7 +495,8 @@ def gpu_arm(args, rank, world, local_rank):
     # one all-reduce on every rank (the time-based warm-up count differs
     # between ranks; collectives must pair up): initialises NCCL and warms
     # its buffers before the timed region
-    allreduce_gradients(gw, world)
+    if gw is not None:
+        allreduce_gradients(gw, world)
     torch.cuda.synchronize()
     if os.environ.get("BENCH_DEBUG"):
         for i in range(int(os.environ.get("BENCH_DEBUG_REPS", "3"))):
@@ -596,7 +612,11 @@ def gpu_arm(args, rank, world, local_rank):
         # dL/dfext down (the adjoint chain stays on the device); once per
         # rollout: the loss gradient up, q_new/q_bar (loss) and dL/dq_bar,
         # dL/dv_bar down
-        h2d = (2 * n3) * 8 + (2 * n3 * 8) // K
+        # + the packed gradient (host arrays of the public API) going up for
+        # the all-reduce: 5 + E + 4B + (K + 2) 3V doubles per rollout
+        nb = len(scene0.bindings)
+        pack_bytes = 8 * (5 + E_ + 4 * nb + (K + 2) * n3)
+        h2d = (2 * n3) * 8 + (2 * n3 * 8 + pack_bytes) // K
         d2h = (2 * n3 + n3) * 8 + (4 * n3 * 8) // K
         e2e = {"value": world * R * K / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h}

@@ -199,7 +199,8 @@ int dp_backprop_step(dp_scene* s, const dp_cache* c, const double* z, const doub
                      double* dL_dfext_out);
 int dp_grads_reset(dp_scene* s);
 int dp_grads_get(dp_scene* s, dp_grad_scalars* out);
-/* dL_dw (E, original element order), dL_dEb (B), dL_ddb (B,3); host, may be NULL */
+/* dL_dw (E, original element order), dL_dEb (B), dL_ddb (B,3); host or device
+ * pointers (UVA), each may be NULL; returns after the copies completed */
 int dp_grads_get_arrays(dp_scene* s, double* dL_dw, double* dL_dEb, double* dL_ddb);
 
 /* ---- batched per-item kernels (unit-level parity with the reference) ----- */

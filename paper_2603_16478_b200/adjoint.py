@@ -148,6 +148,27 @@ def _fold_device_grads(dev, scene, grads):
     _chain_lame(scene, gs.dmu_lame, gs.dlam_lame, grads)
 
 
+def device_gradient_report(dev, scene, device):
+    """GradientReport of the device accumulators with the per-element and
+    per-binding arrays left on the GPU (torch float64 tensors on `device`):
+    the packed-gradient all-reduce (parallel.pack_gradients) then never goes
+    through the host."""
+    import torch
+    gs = _lib.GradScalars()
+    _lib.check(dev.lib.dp_grads_get(dev.handle, C.byref(gs)))
+    nb = len(scene.bindings)
+    dd = dict(device=device, dtype=torch.float64)
+    g = GradientReport(dL_dw=torch.empty(dev.n_elems, **dd), dL_dEb=torch.empty(nb, **dd),
+                       dL_ddb=torch.empty((nb, 3), **dd))
+    _lib.check(dev.lib.dp_grads_get_arrays(dev.handle, _lib.ptr(g.dL_dw) if dev.n_elems else None,
+                                           _lib.ptr(g.dL_dEb) if nb else None,
+                                           _lib.ptr(g.dL_ddb) if nb else None))
+    g.dL_dmu_friction = gs.dL_dmu_friction
+    g.dL_dstiffness = gs.dL_dstiffness
+    _chain_lame(scene, gs.dmu_lame, gs.dlam_lame, g)
+    return g
+
+
 def _chain_lame(scene, dmu, dlam, grads):
     """[dE, dnu] = J_lame^T [dmu, dlam] with the first NH element's (E, nu)
     (adjoint.py:211-217)."""

@@ -1360,10 +1360,15 @@ int dp_grads_get(dp_scene* s, dp_grad_scalars* out) {
 }
 
 int dp_grads_get_arrays(dp_scene* s, double* dL_dw, double* dL_dEb, double* dL_ddb) {
+  // host or device destinations (UVA, cudaMemcpyDefault), ordered on the
+  // scene stream: a device-resident caller (packed gradient all-reduce)
+  // never round-trips through the host
   cudaSetDevice(s->device);
-  if (dL_dw && s->E) DP_CUDA(cudaMemcpy(dL_dw, s->g_dw, sizeof(double) * s->E, cudaMemcpyDeviceToHost));
-  if (dL_dEb && s->nb) DP_CUDA(cudaMemcpy(dL_dEb, s->g_dEb, sizeof(double) * s->nb, cudaMemcpyDeviceToHost));
-  if (dL_ddb && s->nb) DP_CUDA(cudaMemcpy(dL_ddb, s->g_ddb, sizeof(double) * 3 * s->nb, cudaMemcpyDeviceToHost));
+  const cudaMemcpyKind k = cudaMemcpyDefault;
+  if (dL_dw && s->E) DP_CUDA(cudaMemcpyAsync(dL_dw, s->g_dw, sizeof(double) * s->E, k, s->stream));
+  if (dL_dEb && s->nb) DP_CUDA(cudaMemcpyAsync(dL_dEb, s->g_dEb, sizeof(double) * s->nb, k, s->stream));
+  if (dL_ddb && s->nb) DP_CUDA(cudaMemcpyAsync(dL_ddb, s->g_ddb, sizeof(double) * 3 * s->nb, k, s->stream));
+  DP_CUDA(cudaStreamSynchronize(s->stream));
   return DP_OK;
 }
 

@@ -413,3 +413,46 @@ def test_forward_between_adjoint_assemble_and_backprop(pkg):
     b = one(True)
     for x, y in zip(a, b):
         assert np.allclose(x, y, rtol=1e-12, atol=1e-300)
+
+
+def test_c5_family_regime_vs_reference(pkg):
+    """The bench's C5 regime: the C5 family at 12^3 cells
+    (10,368 NH tets, frictionless ground + two kinematic sphere fingers,
+    eps_fb scaled with the vertex mass) over the bench's finger schedule -
+    20 closing steps and 4 held steps - against a fixture written by the
+    REFERENCE itself (tests/golden/make_golden.py c5fam, tol 1e-11): states
+    <= 1e-8, contact sets (vertex, collider, frame) per step exact, and
+    dL/dq_bar, dL/dv_bar, dL/dfext, dL/dE, dL/dnu, dL/dmu <= 1e-6."""
+    import os
+    from paper_2603_16478_b200 import adjoint as aj, core, forward as fw
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "scene_c5fam12.npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture not generated")
+    g = load_golden("scene_c5fam12.npz")
+    scene = core.scene_from_arrays(g)
+    sm = core.assemble_system_matrix(scene)
+    T = int(g["T"])
+    cfg = fw.ForwardConfig(tol=float(g["tol"]))
+    st = core.SimState(g["q"][0], g["v0"])
+    caches = []
+    for k in range(T):
+        scene.colliders[1].center[0], scene.colliders[2].center[0] = g["finger_x"][k]
+        st, rep = fw.forward_step(scene, st, sm, cfg)
+        assert rep.converged, k
+        qs = g["q"][k + 1]
+        assert np.max(np.abs(st.q - qs)) <= 1e-8 * np.max(np.abs(qs)), k
+        m = g["c_step"] == k
+        cps = rep.cache.contacts
+        assert np.array_equal(np.array([c.vertex for c in cps], np.int64), g["c_vertex"][m]), k
+        assert np.array_equal(np.array([c.collider for c in cps], np.int64), g["c_collider"][m]), k
+        assert np.allclose(np.array([c.frame for c in cps]), g["c_frame"][m], atol=1e-15)
+        caches.append(rep.cache)
+    assert int(np.sum(g["c_collider"] > 0)) > 0          # finger contacts are exercised
+    gr = aj.backprop_rollout(caches, g["target"])
+    assert rel(gr.dL_dqbar, g["g_dqbar"]) < 1e-6
+    assert rel(gr.dL_dvbar, g["g_dvbar"]) < 1e-6
+    assert rel(np.array(gr.dL_dfext), g["g_dfext"]) < 1e-6
+    for k, ref in (("dL_dE", "g_dE"), ("dL_dnu", "g_dnu"), ("dL_dmu_friction", "g_dmu")):
+        a, b = getattr(gr, k), float(g[ref])
+        assert abs(a - b) <= 1e-6 * abs(b) + 1e-18, (k, a, b)
+    assert rel(gr.dL_dw, g["g_dw"]) < 1e-6

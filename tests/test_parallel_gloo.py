@@ -73,3 +73,71 @@ def test_allreduce_noop_without_process_group():
     from paper_2603_16478_b200.parallel import allreduce_gradients
     v = torch.tensor([1.0, 2.0], dtype=torch.float64)
     assert torch.equal(allreduce_gradients(v), v)
+
+
+def _fake_report(i, E=5, B=2, T=3, n=6):
+    """Deterministic per-rollout GradientReport with every array block."""
+    from paper_2603_16478_b200.adjoint import GradientReport
+    r = np.random.default_rng(100 + i)
+    return GradientReport(dL_dqbar=r.standard_normal(n), dL_dvbar=r.standard_normal(n),
+                          dL_dfext=[r.standard_normal(n) for _ in range(T)],
+                          dL_dmu_friction=float(r.standard_normal()), dL_dEb=r.standard_normal(B),
+                          dL_ddb=r.standard_normal((B, 3)), dL_dw=r.standard_normal(E),
+                          dL_dstiffness=float(r.standard_normal()), dL_dE=float(r.standard_normal()),
+                          dL_dnu=float(r.standard_normal()))
+
+
+BLOCKS = ("dL_dw", "dL_dEb", "dL_ddb", "dL_dfext", "dL_dqbar", "dL_dvbar")
+
+
+def _worker_blocks(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_16478_b200.parallel import allreduce_gradients, pack_gradients, shard, unpack_gradients
+    tot = lay = None
+    for i in shard(5, rank, world):
+        v, lay = pack_gradients(_fake_report(i), float(i), blocks=BLOCKS, layout=True)
+        tot = v if tot is None else tot + v
+    allreduce_gradients(tot, world)
+    q.put((rank, unpack_gradients(tot, lay)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_allreduce_of_full_packed_gradient():
+    """the packed vector carries dL/dw, dL/dE_b, dL/dd_b,
+    the shared controls dL/dfext and the state gradients; the all-reduced
+    blocks equal the sum over all rollouts of every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_blocks, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    reps = [_fake_report(i) for i in range(5)]
+    for _, out in res:
+        assert out["loss"] == pytest.approx(sum(range(5)))
+        assert out["dL_dE"] == pytest.approx(sum(r.dL_dE for r in reps))
+        for name in BLOCKS:
+            ref = sum(np.asarray(getattr(r, name)) for r in reps)
+            assert out[name].shape == np.asarray(ref).shape, name
+            assert np.allclose(out[name], ref, rtol=1e-14, atol=1e-14), name
+
+
+def test_pack_roundtrip_and_layout():
+    from paper_2603_16478_b200.parallel import PackLayout, pack_gradients, unpack_gradients
+    g = _fake_report(0)
+    v, lay = pack_gradients(g, 2.5, blocks=BLOCKS, extra=[7.0, 8.0], layout=True)
+    assert v.numel() == lay.size == 5 + 5 + 2 + 6 + 3 * 6 + 6 + 6 + 2
+    out = unpack_gradients(v, lay)
+    assert out["loss"] == 2.5
+    assert np.array_equal(out["dL_dfext"], np.array(g.dL_dfext))
+    assert np.array_equal(out["dL_ddb"], g.dL_ddb)
+    assert np.array_equal(out["extra"], [7.0, 8.0])
+    with pytest.raises(ValueError):
+        PackLayout(("not_a_field",))

@@ -999,7 +999,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
       fprintf(stderr, "[dp]   assemble %.2fms\n", 1e3 * (t_solve0 - t_asm0));
     }
     if (!asym) {
-      if (mg) rc = pcg_mg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk);
+      if (mg) rc = pcg_mg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk, 1);
       else rc = cg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk);
       R.krylov_iterations += iters;
       if (brk) {
@@ -1235,7 +1235,7 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
     s->mg_adj_ready = 1;
   }
   if (method == DP_SOLVER_CG) {
-    if (mg) rc = pcg_mg_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, &iters, &relres, &brk);
+    if (mg) rc = pcg_mg_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, &iters, &relres, &brk, 0);
     else rc = cg_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, &iters, &relres, &brk);
     if (brk) {
       int it2 = 0;

@@ -282,7 +282,7 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
                 int restart, int* iters, double* relres, double min_cycle_gain = 0.0, int use_mg = 0,
                 int left = 1, int use_x0 = 0);
 int pcg_mg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int* iters,
-                 double* relres, int* breakdown);
+                 double* relres, int* breakdown, int fp32);
 double device_norm2(dp_scene* s, const double* x);   // sum of squares, synchronous
 // vector ops
 void launch_axpy_to(dp_scene* s, double* out, const double* a, double t, const double* b);   // out = a + t*b
@@ -318,6 +318,7 @@ int mg_levels(const dp_scene* s);
 int mg_level_rows(const dp_scene* s, int l);
 void mg_set_params(dp_scene* s, double omega, int nu);
 void mg_set_symmetric(dp_scene* s, int on);
+void mg_set_pcg_dot(dp_scene* s, double* partial, unsigned int* counter, KrylovScalars* ks);
 void gm_graphs_destroy(dp_scene* s);
 
 }  // namespace dp

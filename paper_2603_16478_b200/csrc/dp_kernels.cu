@@ -1960,20 +1960,47 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
 // PCG with the multigrid V-cycle as preconditioner (symmetric operators).
 // Device-resident scalars; the host only polls `done` every few iterations.
 
-// x = 0, r = b, rho = |b|^2 (tolerances)
+// Three launches per iteration besides the V-cycle's own (round 2; the
+// round-1 loop had V-cycle + rz + p + spmv + xr):
+//   V-cycle    z = M r; its last fine sweep also forms gamma = (r, z) and
+//              beta (k_mg_smooth<..., DOT>, mg_set_pcg_dot)
+//   spmv_p     p' = z + beta p evaluated on the fly in the gathers (each row
+//              also writes its own p'), q = A p', delta = (p', q), alpha;
+//              FP32 operator copy for the inexact Newton solves
+//   xr_j0      x += alpha p', r -= alpha q, rho = |r|^2 -> done; and the
+//              next V-cycle's first fine Jacobi sweep x0 = omega Minv32 r
+// p is double-buffered (p' never overwrites a p another warp still gathers).
+
+__device__ __forceinline__ void minv32_apply(const float* __restrict__ minv, int V, int i, const double r[3],
+                                             double u[3]) {
+  u[0] = minv[0 * (size_t)V + i] * r[0] + minv[1 * (size_t)V + i] * r[1] + minv[2 * (size_t)V + i] * r[2];
+  u[1] = minv[3 * (size_t)V + i] * r[0] + minv[4 * (size_t)V + i] * r[1] + minv[5 * (size_t)V + i] * r[2];
+  u[2] = minv[6 * (size_t)V + i] * r[0] + minv[7 * (size_t)V + i] * r[1] + minv[8 * (size_t)V + i] * r[2];
+}
+
+// x = 0, r = b, p = 0, rho = |b|^2 (tolerances); xa = omega Minv32 b (the
+// first V-cycle's fine Jacobi sweep from zero) when xa != nullptr
 __global__ void __launch_bounds__(kVT) k_pcg_init(int V, const double* __restrict__ b, double* x, double* r, double* p,
                                                   double rtol, double* partial, unsigned int* counter,
-                                                  KrylovScalars* ks) {
+                                                  KrylovScalars* ks, const float* __restrict__ minv32, double omega,
+                                                  double* __restrict__ xa) {
   __shared__ double sh[32];
   __shared__ double out[1];
   const int i = blockIdx.x * kVT + threadIdx.x;
   double acc = 0.0;
   if (i < V) {
+    double rr[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double v = b[3 * i + c];
       x[3 * i + c] = 0.0; p[3 * i + c] = 0.0; r[3 * i + c] = v;
+      rr[c] = v;
       acc += v * v;
+    }
+    if (xa) {
+      double u[3];
+      minv32_apply(minv32, V, i, rr, u);
+      xa[3 * i] = omega * u[0]; xa[3 * i + 1] = omega * u[1]; xa[3 * i + 2] = omega * u[2];
     }
   }
   double t = block_sum<kVT>(acc, sh);
@@ -1992,58 +2019,49 @@ __global__ void __launch_bounds__(kVT) k_pcg_init(int V, const double* __restric
   }
 }
 
-// gamma' = (r, z); beta = gamma'/gamma (0 on the first iteration); p = z + beta p
-// is applied by k_pcg_spmv on the fly (it owns the p rows it writes)
-__global__ void __launch_bounds__(kVT) k_pcg_rz(int V, const double* __restrict__ r, const double* __restrict__ z,
-                                                double* partial, unsigned int* counter, KrylovScalars* ks) {
+// p' = z + beta p (rows gathered on the fly, own row written); q = A p';
+// delta = (p', q); alpha = gamma / delta
+template <class TV>
+__global__ void __launch_bounds__(256) k_pcg_spmv_p(int V, int S, const int* __restrict__ slice_base,
+                                                    const int* __restrict__ slice_width, const int* __restrict__ col,
+                                                    const TV* __restrict__ val, const double* __restrict__ z,
+                                                    const double* __restrict__ p_old, double* __restrict__ p_new,
+                                                    double* __restrict__ q, double* partial, unsigned int* counter,
+                                                    KrylovScalars* ks) {
   __shared__ double sh[32];
   __shared__ double out[1];
-  if (ldflag(&ks->done)) return;
-  const int i = blockIdx.x * kVT + threadIdx.x;
-  double acc = 0.0;
-  if (i < V) acc = r[3 * i] * z[3 * i] + r[3 * i + 1] * z[3 * i + 1] + r[3 * i + 2] * z[3 * i + 2];
-  double t = block_sum<kVT>(acc, sh);
-  if (threadIdx.x == 0) partial[blockIdx.x] = t;
-  if (last_block(counter)) {
-    fold_partials<kVT, 1>(partial, gridDim.x, out, sh);
-    if (threadIdx.x == 0) {
-      const double g = out[0];
-      ks->beta = (ks->iters == 0) ? 0.0 : g / ks->gamma;
-      ks->gamma = g;
-      if (!(g > 0.0)) ks->done = 2;     // preconditioner not SPD on this residual
-      *counter = 0;
-    }
-  }
-}
-
-// p = z + beta p (per row) ; q = A p ; delta = (p, q); alpha = gamma / delta
-__global__ void __launch_bounds__(kVT) k_pcg_p(int V, const double* __restrict__ z, double* __restrict__ p,
-                                               const KrylovScalars* ks) {
   if (ldflag(&ks->done)) return;
   const double beta = ks->beta;
-  const int i = blockIdx.x * kVT + threadIdx.x;
-  if (i >= V) return;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) p[3 * i + c] = z[3 * i + c] + beta * p[3 * i + c];
-}
-
-__global__ void __launch_bounds__(256) k_pcg_spmv(int V, int S, const int* __restrict__ slice_base,
-                                                  const int* __restrict__ slice_width, const int* __restrict__ col,
-                                                  const double* __restrict__ val, const double* __restrict__ p,
-                                                  double* __restrict__ q, double* partial, unsigned int* counter,
-                                                  KrylovScalars* ks) {
-  __shared__ double sh[32];
-  __shared__ double out[1];
-  if (ldflag(&ks->done)) return;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   double pq = 0.0;
   if (gw < S) {
-    double a[3];
-    spmv_row<false>(V, gw, lane, slice_base, slice_width, col, val, p, a);
+    const int base = slice_base[gw];
+    const int K = slice_width[gw];
+    const TV* vs = val + (size_t)base * 9 + lane;
+    const int* cs = col + base + lane;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll 2
+    for (int k = 0; k < K; ++k) {
+      const int j = __ldg(cs + k * kSlice);
+      const TV* v = vs + k * 9 * kSlice;
+      const double x0 = __ldg(z + 3 * j) + beta * __ldg(p_old + 3 * j);
+      const double x1 = __ldg(z + 3 * j + 1) + beta * __ldg(p_old + 3 * j + 1);
+      const double x2 = __ldg(z + 3 * j + 2) + beta * __ldg(p_old + 3 * j + 2);
+      a0 += (double)__ldcs(v + 0 * kSlice) * x0 + (double)__ldcs(v + 1 * kSlice) * x1 +
+            (double)__ldcs(v + 2 * kSlice) * x2;
+      a1 += (double)__ldcs(v + 3 * kSlice) * x0 + (double)__ldcs(v + 4 * kSlice) * x1 +
+            (double)__ldcs(v + 5 * kSlice) * x2;
+      a2 += (double)__ldcs(v + 6 * kSlice) * x0 + (double)__ldcs(v + 7 * kSlice) * x1 +
+            (double)__ldcs(v + 8 * kSlice) * x2;
+    }
     const int row = gw * kSlice + lane;
     if (row < V) {
-      q[3 * row] = a[0]; q[3 * row + 1] = a[1]; q[3 * row + 2] = a[2];
-      pq = a[0] * p[3 * row] + a[1] * p[3 * row + 1] + a[2] * p[3 * row + 2];
+      const double p0 = __ldg(z + 3 * row) + beta * __ldg(p_old + 3 * row);
+      const double p1 = __ldg(z + 3 * row + 1) + beta * __ldg(p_old + 3 * row + 1);
+      const double p2 = __ldg(z + 3 * row + 2) + beta * __ldg(p_old + 3 * row + 2);
+      p_new[3 * row] = p0; p_new[3 * row + 1] = p1; p_new[3 * row + 2] = p2;
+      q[3 * row] = a0; q[3 * row + 1] = a1; q[3 * row + 2] = a2;
+      pq = a0 * p0 + a1 * p1 + a2 * p2;
     }
   }
   double t = block_sum<256>(pq, sh);
@@ -2059,10 +2077,12 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(int V, int S, const int* __res
   }
 }
 
-// x += alpha p ; r -= alpha q ; rho = |r|^2 ; done when rho <= tol^2 |b|^2
-__global__ void __launch_bounds__(kVT) k_pcg_xr(int V, double* x, double* r, const double* __restrict__ p,
-                                                const double* __restrict__ q, double* partial, unsigned int* counter,
-                                                KrylovScalars* ks) {
+// x += alpha p ; r -= alpha q ; rho = |r|^2 ; done when rho <= tol^2 |b|^2;
+// xa = omega Minv32 r (next V-cycle's first fine Jacobi sweep)
+__global__ void __launch_bounds__(kVT) k_pcg_xr_j0(int V, double* x, double* r, const double* __restrict__ p,
+                                                   const double* __restrict__ q, const float* __restrict__ minv32,
+                                                   double omega, double* __restrict__ xa, double* partial,
+                                                   unsigned int* counter, KrylovScalars* ks) {
   __shared__ double sh[32];
   __shared__ double out[1];
   if (ldflag(&ks->done)) return;
@@ -2070,14 +2090,19 @@ __global__ void __launch_bounds__(kVT) k_pcg_xr(int V, double* x, double* r, con
   const int i = blockIdx.x * kVT + threadIdx.x;
   double acc = 0.0;
   if (i < V) {
+    double rr[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const int k = 3 * i + c;
       x[k] += alpha * p[k];
       const double v = r[k] - alpha * q[k];
       r[k] = v;
+      rr[c] = v;
       acc += v * v;
     }
+    double u[3];
+    minv32_apply(minv32, V, i, rr, u);
+    xa[3 * i] = omega * u[0]; xa[3 * i + 1] = omega * u[1]; xa[3 * i + 2] = omega * u[2];
   }
   double t = block_sum<kVT>(acc, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
@@ -2092,20 +2117,28 @@ __global__ void __launch_bounds__(kVT) k_pcg_xr(int V, double* x, double* r, con
   }
 }
 
-int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
-                      int* iters, double* relres, int* breakdown);
+static const int g_pcg_fp32 = getenv("DP_PCG_FP32") ? atoi(getenv("DP_PCG_FP32")) : 1;
 
-// CG needs a symmetric preconditioner: force the symmetric V(nu,nu) cycle
+int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
+                      int* iters, double* relres, int* breakdown, int fp32);
+
+// CG needs a symmetric preconditioner: force the symmetric V(nu,nu) cycle.
+// fp32: apply the operator from its FP32 copy inside the iteration (inexact
+// Newton solves: the operator's 1e-7 relative rounding is far below the
+// forcing term; the true residual that ends the solve is FP64)
 int pcg_mg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int* iters,
-                 double* relres, int* breakdown) {
+                 double* relres, int* breakdown, int fp32) {
   mg_set_symmetric(s, 1);
-  const int rc = pcg_mg_solve_impl(s, val, b, x, rtol, max_iter, iters, relres, breakdown);
+  mg_set_pcg_dot(s, s->red.partial, s->red.counter, s->ksc);
+  const int rc = pcg_mg_solve_impl(s, val, b, x, rtol, max_iter, iters, relres, breakdown,
+                                   fp32 && g_pcg_fp32 && s->val32 != nullptr && s->val32_src == val);
+  mg_set_pcg_dot(s, nullptr, nullptr, nullptr);
   mg_set_symmetric(s, 0);
   return rc;
 }
 
 int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
-                      int* iters, double* relres, int* breakdown) {
+                      int* iters, double* relres, int* breakdown, int fp32) {
   const int V = s->V, n = 3 * V;
   const int nbv = grid_for(V, kVT);
   const int nbs = grid_for((int64_t)s->S * 32, 256);
@@ -2117,29 +2150,42 @@ int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x
     *relres = 0.0;
     return 0;
   }
+  const float* minv32 = nullptr;
+  double* xa = nullptr;
+  double omega = 0.0;
+  mg_fine_jacobi0_target(s, &minv32, &xa, &omega);
   double* bb = s->tmp;     // rhs of the current correction solve
   double* xc = s->kx;
-  double *r = s->kr, *z = s->ku, *p = s->kp, *q = s->kw;
+  double *r = s->kr, *z = s->ku, *q = s->kw;
+  double* pb[2] = {s->kp, s->ks};
   cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
   cudaMemcpyAsync(bb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s->stream);
   double rel = 1.0;
   for (int restart = 0; restart < 4; ++restart) {
     double inner = rtol / rel * 0.5;
     inner = fmin(0.5, fmax(inner, 1e-15));
-    k_pcg_init<<<nbv, kVT, 0, s->stream>>>(V, bb, xc, r, p, inner, s->red.partial, s->red.counter, s->ksc);
+    int par = 0;
+    k_pcg_init<<<nbv, kVT, 0, s->stream>>>(V, bb, xc, r, pb[0], inner, s->red.partial, s->red.counter, s->ksc, minv32,
+                                           omega, xa);
     s->launches++;
     int done = 0, launched = 0, chunk = 4;
     while (!done && *iters + launched < max_iter) {
       int m = chunk;
       if (*iters + launched + m > max_iter) m = max_iter - *iters - launched;
       for (int k = 0; k < m; ++k) {
-        mg_apply(s, val, r, z, &s->ksc->done);
-        k_pcg_rz<<<nbv, kVT, 0, s->stream>>>(V, r, z, s->red.partial, s->red.counter, s->ksc);
-        k_pcg_p<<<nbv, kVT, 0, s->stream>>>(V, z, p, s->ksc);
-        k_pcg_spmv<<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, p, q,
-                                               s->red.partial, s->red.counter, s->ksc);
-        k_pcg_xr<<<nbv, kVT, 0, s->stream>>>(V, xc, r, p, q, s->red.partial, s->red.counter, s->ksc);
-        s->launches += 4;
+        mg_apply_prejac(s, val, r, z, &s->ksc->done);
+        if (fp32)
+          k_pcg_spmv_p<float><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, s->val32, z,
+                                                          pb[par], pb[par ^ 1], q, s->red.partial, s->red.counter,
+                                                          s->ksc);
+        else
+          k_pcg_spmv_p<double><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, z,
+                                                           pb[par], pb[par ^ 1], q, s->red.partial, s->red.counter,
+                                                           s->ksc);
+        k_pcg_xr_j0<<<nbv, kVT, 0, s->stream>>>(V, xc, r, pb[par ^ 1], q, minv32, omega, xa, s->red.partial,
+                                                s->red.counter, s->ksc);
+        par ^= 1;
+        s->launches += 2;
       }
       launched += m;
       read_ksc(s);

@@ -86,6 +86,11 @@ struct MG {
   int symmetric_needed = 0;  // set while a CG solve uses the V-cycle
   int fused = 1;              // coarse levels in one cooperative kernel (k_mg_coarse_fused)
   int prejac = 0;             // fine-level jacobi0 already applied by the caller
+  // PCG fusion: the fine level's last post-smoothing sweep also forms
+  // (r, z) and the CG beta (k_mg_smooth<..., DOT>) when dot_ks is set
+  double* dot_partial = nullptr;
+  unsigned int* dot_counter = nullptr;
+  KrylovScalars* dot_ks = nullptr;
   int fused_grid = 0;
   size_t bytes = 0;
 };
@@ -471,20 +476,26 @@ __global__ void k_mg_jacobi0(int n, const TM* __restrict__ minv, const double* _
 // partial row sums meet in shared memory - the coarse levels have few slices
 // but wide rows (a level-1 row couples ~27-100 aggregates), where a single
 // warp per slice is a long dependent-latency chain.
-template <class TV, int SPLIT>
+// DOT (fine level, SPLIT = 1, with `out`): the PCG's (r, z) reduction fused
+// into the epilogue - b is r, out is z; the last CTA folds the per-CTA
+// partials in a fixed order and updates beta/gamma exactly as k_pcg_rz
+template <class TV, int SPLIT, bool DOT = false>
 __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __restrict__ slice_base,
                                                    const int* __restrict__ slice_width, const int* __restrict__ col,
                                                    const TV* __restrict__ val, const TV* __restrict__ minv,
                                                    const double* __restrict__ b, const double* __restrict__ x,
                                                    const double* __restrict__ xc, const int* __restrict__ agg,
                                                    double omega, double* __restrict__ out, double* __restrict__ r_out,
-                                                   const int* stop, double alpha) {
+                                                   const int* stop, double alpha, double* dot_partial = nullptr,
+                                                   unsigned int* dot_counter = nullptr,
+                                                   KrylovScalars* dot_ks = nullptr) {
   __shared__ double part[SPLIT > 1 ? SPLIT : 1][3][kSlice];
-  if (stopped(stop)) return;
+  if (stopped(stop)) return;   // uniform over the grid (set by an earlier kernel)
   const int lane = threadIdx.x & 31;
   const int wsub = (SPLIT > 1) ? (threadIdx.x >> 5) : 0;
   const int gw = (SPLIT > 1) ? blockIdx.x : (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (gw >= S) return;
+  double rz = 0.0;
+  if (gw < S) {
   const int row = gw * kSlice + lane;
   const int base = slice_base[gw], K = slice_width[gw];
   const TV* vs = val + (size_t)base * 9 + lane;
@@ -617,20 +628,42 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
 #pragma unroll
     for (int w = 0; w < SPLIT; ++w) { a0 += part[w][0][lane]; a1 += part[w][1][lane]; a2 += part[w][2][lane]; }
   }
-  if (row >= n) return;
-  double xt[3] = {x[3 * row], x[3 * row + 1], x[3 * row + 2]};
-  if (xc) {
-    const int I = agg[row];
-    xt[0] += alpha * xc[3 * I]; xt[1] += alpha * xc[3 * I + 1]; xt[2] += alpha * xc[3 * I + 2];
+  if (row < n) {
+    double xt[3] = {x[3 * row], x[3 * row + 1], x[3 * row + 2]};
+    if (xc) {
+      const int I = agg[row];
+      xt[0] += alpha * xc[3 * I]; xt[1] += alpha * xc[3 * I + 1]; xt[2] += alpha * xc[3 * I + 2];
+    }
+    const double bb[3] = {b[3 * row], b[3 * row + 1], b[3 * row + 2]};
+    const double rr[3] = {bb[0] - a0, bb[1] - a1, bb[2] - a2};
+    if (r_out) { r_out[3 * row] = rr[0]; r_out[3 * row + 1] = rr[1]; r_out[3 * row + 2] = rr[2]; }
+    if (out) {
+      double u[3];
+      mv_minv(minv, n, row, rr, u);
+      const double z0 = xt[0] + omega * u[0], z1 = xt[1] + omega * u[1], z2 = xt[2] + omega * u[2];
+      out[3 * row] = z0;
+      out[3 * row + 1] = z1;
+      out[3 * row + 2] = z2;
+      if (DOT) rz = bb[0] * z0 + bb[1] * z1 + bb[2] * z2;
+    }
   }
-  const double rr[3] = {b[3 * row] - a0, b[3 * row + 1] - a1, b[3 * row + 2] - a2};
-  if (r_out) { r_out[3 * row] = rr[0]; r_out[3 * row + 1] = rr[1]; r_out[3 * row + 2] = rr[2]; }
-  if (out) {
-    double u[3];
-    mv_minv(minv, n, row, rr, u);
-    out[3 * row] = xt[0] + omega * u[0];
-    out[3 * row + 1] = xt[1] + omega * u[1];
-    out[3 * row + 2] = xt[2] + omega * u[2];
+  }   // gw < S
+  if constexpr (DOT) {
+    static_assert(SPLIT == 1, "fused (r, z) only on the one-warp-per-slice fine level");
+    __shared__ double sh[32];
+    __shared__ double o1[1];
+    const double t = block_sum<DP_SMOOTH_NT>(rz, sh);
+    if (threadIdx.x == 0) dot_partial[blockIdx.x] = t;
+    if (last_block(dot_counter)) {
+      fold_partials<DP_SMOOTH_NT, 1>(dot_partial, gridDim.x, o1, sh);
+      if (threadIdx.x == 0) {
+        const double g = o1[0];
+        dot_ks->beta = (dot_ks->iters == 0) ? 0.0 : g / dot_ks->gamma;
+        dot_ks->gamma = g;
+        if (!(g > 0.0)) dot_ks->done = 2;     // preconditioner not SPD on this residual
+        *dot_counter = 0;
+      }
+    }
   }
 }
 
@@ -1106,8 +1139,13 @@ void mg_assemble(dp_scene* s, const double* val) {
 template <class TV>
 static void smooth(dp_scene* s, const MGLevel& L, const TV* val, const TV* minv, const double* b, const double* x,
                    const double* xc, const int* agg, double omega, double* out, double* r_out, const int* stop,
-                   double alpha) {
-  if (L.S >= 4 * 148)
+                   double alpha, bool dot = false) {
+  MG* mg = s->mg;
+  if (dot && mg->dot_ks && out && L.S >= 4 * 148)
+    k_mg_smooth<TV, 1, true><<<grid_for((int64_t)L.S * 32, DP_SMOOTH_NT), DP_SMOOTH_NT, 0, s->stream>>>(
+        L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x, xc, agg, omega, out, r_out, stop, alpha,
+        mg->dot_partial, mg->dot_counter, mg->dot_ks);
+  else if (L.S >= 4 * 148)
     k_mg_smooth<TV, 1><<<grid_for((int64_t)L.S * 32, DP_SMOOTH_NT), DP_SMOOTH_NT, 0, s->stream>>>(
         L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x, xc, agg, omega, out, r_out, stop, alpha);
   else
@@ -1250,10 +1288,19 @@ static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, cons
     for (int it = 0; it < mg->nu; ++it) {
       double* dst = (last && it == mg->nu - 1) ? x : xb;
       smooth<TV>(s, L, val, minv, b, xa, it == 0 ? C.x : nullptr, it == 0 ? C.agg : nullptr, om, dst, nullptr, stop,
-                 mg->alpha);
+                 mg->alpha, l == 0 && dst == x);
       if (dst == xb) std::swap(xa, xb);
     }
   }
+}
+
+// PCG fusion (pcg_mg_solve): the fine level's final post-smoothing sweep of
+// every V-cycle forms (r, z) and the CG beta; nullptr ks switches it off
+void mg_set_pcg_dot(dp_scene* s, double* partial, unsigned int* counter, KrylovScalars* ks) {
+  if (!s->mg) return;
+  s->mg->dot_partial = partial;
+  s->mg->dot_counter = counter;
+  s->mg->dot_ks = ks;
 }
 
 void mg_set_symmetric(dp_scene* s, int on) {

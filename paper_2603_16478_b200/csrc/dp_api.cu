@@ -169,6 +169,7 @@ static const double g_watch_frac = getenv("DP_LS_WATCH_FRAC") ? atof(getenv("DP_
 // :186-192 projects the elements at q again) is then already done
 static const int g_spec_jac = getenv("DP_LS_SPECJAC") ? atoi(getenv("DP_LS_SPECJAC")) : 1;
 static const int g_ls_norm = getenv("DP_LS_NORM") ? atoi(getenv("DP_LS_NORM")) : 0;
+static const int g_newton_x0 = getenv("DP_NEWTON_X0") ? atoi(getenv("DP_NEWTON_X0")) : 1;
 static const double g_eta_plateau = getenv("DP_ETA_PLATEAU") ? atof(getenv("DP_ETA_PLATEAU")) : 0.0;
 static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -238,7 +239,13 @@ void dp_solver_cfg_default(dp_solver_cfg* c) {
 // ---------------------------------------------------------------------------
 // scene
 
+std::recursive_mutex& dp::api_mutex() {
+  static std::recursive_mutex mu;
+  return mu;
+}
+
 int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
+  std::lock_guard<std::recursive_mutex> api_lock(dp::api_mutex());
   *out = nullptr;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -545,7 +552,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   rc |= dalloc(s, &s->c_count, V + 1);
   rc |= dalloc(s, &s->c_off, V + 1);
   const size_t n3 = (size_t)V * 3;
-  double** vecs[] = {&s->q, &s->q_hat, &s->q_bar, &s->v_bar, &s->r, &s->dq, &s->q_try, &s->rhs, &s->z, &s->z_prev, &s->tmp, &s->q_ev, &s->r_try,
+  double** vecs[] = {&s->q, &s->q_hat, &s->q_bar, &s->v_bar, &s->r, &s->dq, &s->q_try, &s->rhs, &s->z, &s->z_prev, &s->dq_prev, &s->q_start, &s->tmp, &s->q_ev, &s->r_try,
                      &s->kx, &s->kr, &s->ku, &s->kw, &s->kp, &s->ks};
   for (auto pp : vecs) rc |= dalloc(s, pp, std::max(n3, (size_t)kMaxRestart + 1));
   s->gm_cap = kMaxRestart + 1;
@@ -591,6 +598,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
 static void cache_free(dp_cache* c);
 
 int dp_scene_destroy(dp_scene* s) {
+  std::lock_guard<std::recursive_mutex> api_lock(dp::api_mutex());
   if (!s) return DP_OK;
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
@@ -783,6 +791,7 @@ int dp_scene_export_bsr(dp_scene* s, int32_t which, int32_t* rowptr, int32_t* co
 // step, and cudaMalloc/cudaFree inside the timed loop cost milliseconds (and
 // cudaFree synchronises the device), so destroyed caches keep their buffers.
 int dp_cache_create(dp_scene* s, dp_cache** out) {
+  std::lock_guard<std::recursive_mutex> api_lock(dp::api_mutex());
   cudaSetDevice(s->device);
   if (!s->cache_pool.empty()) {
     dp_cache* c = s->cache_pool.back();
@@ -821,6 +830,7 @@ static void cache_free(dp_cache* c) {
 }
 
 int dp_cache_destroy(dp_cache* c) {
+  std::lock_guard<std::recursive_mutex> api_lock(dp::api_mutex());
   if (!c) return DP_OK;
   if (c->scene) {
     dp_scene* s = c->scene;
@@ -936,6 +946,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
   DP_CUDA(cudaMemsetAsync(s->esc, 0, sizeof(EvalScalars), s->stream));
   launch_predict(s);                                   // q_hat and q = q_hat
   launch_pullback(s, s->q, s->q_bar, cfg.pullback_margin);
+  DP_CUDA(cudaMemcpyAsync(s->q_start, s->q, sizeof(double) * 3 * s->V, cudaMemcpyDeviceToDevice, s->stream));
   double scale = 1.0;
   double* q = s->q;
   double* q_try = s->q_try;
@@ -999,7 +1010,13 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
       fprintf(stderr, "[dp]   assemble %.2fms\n", 1e3 * (t_solve0 - t_asm0));
     }
     if (!asym) {
-      if (mg) rc = pcg_mg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk, 1);
+      // first Newton solve of a step that continues the previous one: start
+      // the Krylov solve at the previous step's total Newton correction
+      // q_new - q_hat (quasi-steady motion: the two are close; the solve
+      // still ends on the FP64 true residual, so only the iteration count
+      // changes; pcg_mg_solve falls back to x0 = 0 if the guess is worse)
+      const double* x0 = (g_newton_x0 && it == 0 && s->dq_prev_valid && !E.discont) ? s->dq_prev : nullptr;
+      if (mg) rc = pcg_mg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk, 1, x0);
       else rc = cg_solve(s, s->val_fwd, s->rhs, s->dq, eta, cfg.lin_max_iter, &iters, &relres, &brk);
       R.krylov_iterations += iters;
       if (brk) {
@@ -1019,8 +1036,8 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     if (g_debug) {
       cudaStreamSynchronize(s->stream);
       t_ls0 = now_s();
-      fprintf(stderr, "[dp] it=%d res=%.3e |r|2=%.3e C=%d asym=%d eta=%.1e krylov=%d relres=%.2e rc=%d solve=%.2fms\n",
-              it, res, rn, n_contacts, asym, eta, iters, relres, rc, 1e3 * (t_ls0 - t_solve0));
+      fprintf(stderr, "[dp] it=%d res=%.3e |r|2=%.3e C=%d asym=%d eta=%.1e krylov=%d relres=%.2e rc=%d solve=%.2fms guess=%d/%d\n",
+              it, res, rn, n_contacts, asym, eta, iters, relres, rc, 1e3 * (t_ls0 - t_solve0), s->dq_prev_valid, E.discont);
     }
     // line search (forward.py:214-234)
     double t = 1.0;
@@ -1085,6 +1102,8 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     DP_CUDA(cudaMemcpyAsync(s->q, q, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s->stream));
   }
   launch_velocity(s, s->q, s->q_bar, s->z);
+  launch_axpy_to(s, s->dq_prev, s->q, -1.0, s->q_start);   // q_new - q_start (next step's first guess)
+  s->dq_prev_valid = 1;
   if (q_out && (rc = copy_out(s, q_out, s->q, n3, ptr_kind))) return rc;
   if (v_out && (rc = copy_out(s, v_out, s->z, n3, ptr_kind))) return rc;
   if (cache && (rc = cache_store(s, cache, q_eval, n_contacts, asym))) return rc;

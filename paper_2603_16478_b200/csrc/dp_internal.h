@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/diffproj_b200.h"
@@ -30,6 +31,7 @@ struct EvalScalars {
   int precheck;         // pre-check rejected the trial (a watched row already >= max|r|)
   int n_watch;          // watched rows (pre-check), capped at kWatchMax
   int n_watch_elem;     // element entries of the watched rows, capped at kWatchElemMax
+  int discont;          // q_bar differs from the previous step's output (not a rollout continuation)
 };
 constexpr int kWatchMax = 256;
 constexpr int kWatchElemMax = 256 * 32;
@@ -206,6 +208,9 @@ struct dp_scene {
   int* watch_v = nullptr;           // line-search pre-check: watched rows and the elements incident to them
   int* watch_e = nullptr;
   double* z_prev = nullptr;   // last adjoint solution of the current reverse sweep (warm start)
+  double* dq_prev = nullptr;  // q_new - q_start of the previous forward step (first Newton solve's initial guess)
+  double* q_start = nullptr;  // the Newton start point (pulled-back q_hat) of the current step
+  int dq_prev_valid = 0;
   int z_prev_valid = 0;
   int adj_warm = 1;
   // Krylov workspace
@@ -282,7 +287,7 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
                 int restart, int* iters, double* relres, double min_cycle_gain = 0.0, int use_mg = 0,
                 int left = 1, int use_x0 = 0);
 int pcg_mg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int* iters,
-                 double* relres, int* breakdown, int fp32);
+                 double* relres, int* breakdown, int fp32, const double* x0 = nullptr);
 double device_norm2(dp_scene* s, const double* x);   // sum of squares, synchronous
 // vector ops
 void launch_axpy_to(dp_scene* s, double* out, const double* a, double t, const double* b);   // out = a + t*b
@@ -319,6 +324,14 @@ int mg_level_rows(const dp_scene* s, int l);
 void mg_set_params(dp_scene* s, double omega, int nu);
 void mg_set_symmetric(dp_scene* s, int on);
 void mg_set_pcg_dot(dp_scene* s, double* partial, unsigned int* counter, KrylovScalars* ks);
+void launch_pcg_rz(dp_scene* s, const double* r, const double* z, double* partial, unsigned int* counter,
+                   KrylovScalars* ks);
 void gm_graphs_destroy(dp_scene* s);
+// Process-wide lock around the calls that allocate / free device memory or
+// capture CUDA graphs (scene and cache create/destroy, GMRES graph capture):
+// concurrent rollouts on host threads otherwise interleave allocations with
+// another thread's capture (observed: intermittent host crash in the
+// concurrent-rollout test).  Steps themselves never take it.
+std::recursive_mutex& api_mutex();
 
 }  // namespace dp

@@ -1749,6 +1749,7 @@ static GmGraph* gm_graph(dp_scene* s, const double* val, int use_mg, int left, b
                        ((uint64_t)tight << 3) ^ ((uint64_t)lowp << 4) ^ ((uint64_t)zbasis << 5);
   for (auto& e : s->gm_graphs)
     if (e.first == key) return (GmGraph*)e.second;
+  std::lock_guard<std::recursive_mutex> api_lock(api_mutex());
   cudaGraph_t g = nullptr;
   if (cudaGraphCreate(&g, 0) != cudaSuccess) return nullptr;
   cudaGraphConditionalHandle h;
@@ -2019,6 +2020,37 @@ __global__ void __launch_bounds__(kVT) k_pcg_init(int V, const double* __restric
   }
 }
 
+// gamma' = (r, z); beta = gamma'/gamma (0 on the first iteration): the
+// stand-alone form of the reduction k_mg_smooth<..., DOT> fuses, for fine
+// levels too small for the one-warp-per-slice smoother (mg_pcg_rz)
+__global__ void __launch_bounds__(kVT) k_pcg_rz(int V, const double* __restrict__ r, const double* __restrict__ z,
+                                                double* partial, unsigned int* counter, KrylovScalars* ks) {
+  __shared__ double sh[32];
+  __shared__ double out[1];
+  if (ldflag(&ks->done)) return;
+  const int i = blockIdx.x * kVT + threadIdx.x;
+  double acc = 0.0;
+  if (i < V) acc = r[3 * i] * z[3 * i] + r[3 * i + 1] * z[3 * i + 1] + r[3 * i + 2] * z[3 * i + 2];
+  double t = block_sum<kVT>(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (last_block(counter)) {
+    fold_partials<kVT, 1>(partial, gridDim.x, out, sh);
+    if (threadIdx.x == 0) {
+      const double g = out[0];
+      ks->beta = (ks->iters == 0) ? 0.0 : g / ks->gamma;
+      ks->gamma = g;
+      if (!(g > 0.0)) ks->done = 2;     // preconditioner not SPD on this residual
+      *counter = 0;
+    }
+  }
+}
+
+void launch_pcg_rz(dp_scene* s, const double* r, const double* z, double* partial, unsigned int* counter,
+                   KrylovScalars* ks) {
+  k_pcg_rz<<<grid_for(s->V, kVT), kVT, 0, s->stream>>>(s->V, r, z, partial, counter, ks);
+  s->launches++;
+}
+
 // p' = z + beta p (rows gathered on the fly, own row written); q = A p';
 // delta = (p', q); alpha = gamma / delta
 template <class TV>
@@ -2120,25 +2152,25 @@ __global__ void __launch_bounds__(kVT) k_pcg_xr_j0(int V, double* x, double* r, 
 static const int g_pcg_fp32 = getenv("DP_PCG_FP32") ? atoi(getenv("DP_PCG_FP32")) : 1;
 
 int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
-                      int* iters, double* relres, int* breakdown, int fp32);
+                      int* iters, double* relres, int* breakdown, int fp32, const double* x0);
 
 // CG needs a symmetric preconditioner: force the symmetric V(nu,nu) cycle.
 // fp32: apply the operator from its FP32 copy inside the iteration (inexact
 // Newton solves: the operator's 1e-7 relative rounding is far below the
 // forcing term; the true residual that ends the solve is FP64)
 int pcg_mg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter, int* iters,
-                 double* relres, int* breakdown, int fp32) {
+                 double* relres, int* breakdown, int fp32, const double* x0) {
   mg_set_symmetric(s, 1);
   mg_set_pcg_dot(s, s->red.partial, s->red.counter, s->ksc);
   const int rc = pcg_mg_solve_impl(s, val, b, x, rtol, max_iter, iters, relres, breakdown,
-                                   fp32 && g_pcg_fp32 && s->val32 != nullptr && s->val32_src == val);
+                                   fp32 && g_pcg_fp32 && s->val32 != nullptr && s->val32_src == val, x0);
   mg_set_pcg_dot(s, nullptr, nullptr, nullptr);
   mg_set_symmetric(s, 0);
   return rc;
 }
 
 int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
-                      int* iters, double* relres, int* breakdown, int fp32) {
+                      int* iters, double* relres, int* breakdown, int fp32, const double* x0) {
   const int V = s->V, n = 3 * V;
   const int nbv = grid_for(V, kVT);
   const int nbs = grid_for((int64_t)s->S * 32, 256);
@@ -2158,9 +2190,26 @@ int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x
   double* xc = s->kx;
   double *r = s->kr, *z = s->ku, *q = s->kw;
   double* pb[2] = {s->kp, s->ks};
-  cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
-  cudaMemcpyAsync(bb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s->stream);
   double rel = 1.0;
+  bool guess = false;
+  if (x0) {
+    // initial guess: solve A e = b - A x0 for the correction; keep it only
+    // when it reduces the residual (else start from zero)
+    launch_spmv(s, val, x0, bb);
+    launch_axpy_to(s, bb, b, -1.0, bb);
+    rel = sqrt(device_norm2(s, bb)) / bnorm;
+    guess = rel < 1.0;
+    if (guess) cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, s->stream);
+    else rel = 1.0;
+    if (guess && rel <= rtol) {
+      *relres = rel;
+      return 0;
+    }
+  }
+  if (!guess) {
+    cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+    cudaMemcpyAsync(bb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s->stream);
+  }
   for (int restart = 0; restart < 4; ++restart) {
     double inner = rtol / rel * 0.5;
     inner = fmin(0.5, fmax(inner, 1e-15));
@@ -2226,7 +2275,10 @@ __global__ void __launch_bounds__(kVT) k_predict(int V, const double* __restrict
     for (int c = 0; c < 3; ++c) {
       const int k = 3 * i + c;
       const double f = __dadd_rn(has_fext ? fext[k] : 0.0, __dmul_rn(m, g[c]));
-      const double qh = __dadd_rn(__dadd_rn(q_bar[k], __dmul_rn(h, v_bar[k])), __dmul_rn(hh_minv, f));
+      const double qb = q_bar[k];
+      const double qh = __dadd_rn(__dadd_rn(qb, __dmul_rn(h, v_bar[k])), __dmul_rn(hh_minv, f));
+      // q still holds the previous step's output: a rollout continuation?
+      if (q[k] != qb) esc->discont = 1;
       q_hat[k] = qh;
       q[k] = qh;
       amax = fmax(amax, fabs(m * qh));

@@ -55,6 +55,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 namespace dp {
 
+static const int g_mg_tail = getenv("DP_MG_TAIL") ? atoi(getenv("DP_MG_TAIL")) : 0;   // measured slower (39 us vs 23 us), off
 constexpr int kCoarseMax = 36;      // dense coarsest solve (<= 108 unknowns, shared memory)
 constexpr int kDenseSmem = 108;
 __global__ void k_mg_dense_invert(int N, const double* __restrict__ Ag, double* __restrict__ Ainv);
@@ -1129,7 +1130,9 @@ void mg_assemble(dp_scene* s, const double* val) {
     s->launches++;
   }
   const MGLevel& Lc = mg->lv.back();
-  if (mg->coarse_sweeps > 0) return;   // coarsest handled by in-CTA Jacobi sweeps
+  // coarsest handled by in-CTA Jacobi sweeps, unless the cluster tail kernel
+  // (exact coarsest solve) is in use
+  if (mg->coarse_sweeps > 0 && !(g_mg_tail && mg->dinv && mg->lv.size() >= 3)) return;
   k_mg_dense_build<<<1, 1024, 0, s->stream>>>(Lc.n, Lc.S, Lc.slice_base, Lc.slice_width, Lc.col, Lc.val, mg->dense);
   k_mg_dense_invert<<<1, 256, (size_t)2 * mg->N * mg->N * sizeof(double), s->stream>>>(mg->N, mg->dense, mg->dinv);
   s->launches += 2;
@@ -1141,6 +1144,15 @@ static void smooth(dp_scene* s, const MGLevel& L, const TV* val, const TV* minv,
                    const double* xc, const int* agg, double omega, double* out, double* r_out, const int* stop,
                    double alpha, bool dot = false) {
   MG* mg = s->mg;
+  if (dot && mg->dot_ks && out && L.S < 4 * 148) {
+    // fine level too small for the one-warp-per-slice kernel: the CTA-per-
+    // slice sweep, then the PCG's (r, z) reduction in a launch of its own
+    k_mg_smooth<TV, 8><<<L.S, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x,
+                                                   xc, agg, omega, out, r_out, stop, alpha);
+    s->launches++;
+    launch_pcg_rz(s, b, out, mg->dot_partial, mg->dot_counter, mg->dot_ks);
+    return;
+  }
   if (dot && mg->dot_ks && out && L.S >= 4 * 148)
     k_mg_smooth<TV, 1, true><<<grid_for((int64_t)L.S * 32, DP_SMOOTH_NT), DP_SMOOTH_NT, 0, s->stream>>>(
         L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x, xc, agg, omega, out, r_out, stop, alpha,
@@ -1165,6 +1177,167 @@ template <class TV>
 static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, const double* b, double* x,
                          const int* stop, bool pre_done = false);
 static const int g_mg_rj0 = getenv("DP_MG_RJ0") ? atoi(getenv("DP_MG_RJ0")) : 1;
+
+
+// ---------------------------------------------------------------------------
+// The two coarsest levels of the V-cycle in ONE launch on a thread-block
+// cluster (round 2).  Level a = L-2 (C5: 343 block rows), level c = L-1 (27
+// rows).  Replaces restrict+jacobi0 (a), residual sweep (a), restrict + the
+// one-CTA Jacobi solve (c) and the post-sweep (a): four dependent launches
+// of 4-10 us each that were pure latency (a few hundred KB, L2-resident).
+// Rows of level a are spread over the cluster's warps (one warp per row,
+// lanes over the row's SELL slots); phases are separated by cluster
+// barriers (hardware, cheap) instead of kernel boundaries; level c (tiny) is
+// solved redundantly by every CTA in shared memory, which saves a barrier.
+// Same operators, same smoother and coarse sweeps as the per-level kernels
+// (summation order differs: warp trees instead of slot-ordered sums).
+constexpr int kTailCTAs = 8;
+constexpr int kTailNT = 256;
+constexpr int kTailMaxC = 64;   // rows of the coarsest level held in shared memory
+
+struct TailArgs {
+  // level a (L-2)
+  int na;
+  const int *sb_a, *sw_a, *col_a;
+  const double *val_a, *minv_a;
+  const int *mptr_a, *mem_a;      // level-a row -> rows of the level above (rf)
+  double *b_a, *xa_a, *r_a, *x_a; // rhs, pre-smoothed iterate, residual, output
+  // level c (L-1)
+  int nc;
+  const int *sb_c, *sw_c, *col_c;
+  const double *val_c, *minv_c;
+  const int *mptr_c, *mem_c;      // level-c row -> level-a rows
+  const int* agg_c;               // level-a row -> level-c row
+  const double* dinv;             // dense inverse of the level-c operator (3 n_c square)
+  const double* rf;               // residual of the level above level a
+  double omega, alpha;
+  int sweeps;
+  const int* stop;
+};
+
+__device__ __forceinline__ void tail_row_sum(int row, int lane, const int* __restrict__ sb, const int* __restrict__ sw,
+                                             const int* __restrict__ col, const double* __restrict__ val,
+                                             const double* __restrict__ x, const double* __restrict__ xc,
+                                             const int* __restrict__ agg, double alpha, double a[3]) {
+  const int sl = row / kSlice, li = row % kSlice;
+  const int base = sb[sl], K = sw[sl];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int k = lane; k < K; k += 32) {
+    const int slot = base + k * kSlice + li;
+    const int j = col[slot];
+    const double* v = val + (size_t)base * 9 + (size_t)k * 9 * kSlice + li;
+    double x0 = x[3 * j], x1 = x[3 * j + 1], x2 = x[3 * j + 2];
+    if (xc) {
+      const int J = agg[j];
+      x0 += alpha * xc[3 * J]; x1 += alpha * xc[3 * J + 1]; x2 += alpha * xc[3 * J + 2];
+    }
+    a0 += v[0 * kSlice] * x0 + v[1 * kSlice] * x1 + v[2 * kSlice] * x2;
+    a1 += v[3 * kSlice] * x0 + v[4 * kSlice] * x1 + v[5 * kSlice] * x2;
+    a2 += v[6 * kSlice] * x0 + v[7 * kSlice] * x1 + v[8 * kSlice] * x2;
+  }
+  a[0] = warp_sum(a0); a[1] = warp_sum(a1); a[2] = warp_sum(a2);
+}
+
+__global__ void __cluster_dims__(kTailCTAs, 1, 1) __launch_bounds__(kTailNT) k_mg_tail(const __grid_constant__ TailArgs A) {
+  __shared__ double xs[3 * kTailMaxC], bs[3 * kTailMaxC];
+  if (stopped(A.stop)) return;   // uniform (set by an earlier kernel)
+  cg::cluster_group cl = cg::this_cluster();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nw = kTailCTAs * (kTailNT / 32);
+  const int gw = (int)cl.block_rank() * (kTailNT / 32) + wib;
+  const double om = A.omega;
+  // phase 1: restriction to level a and its first Jacobi sweep from zero
+  for (int I = gw; I < A.na; I += nw) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int t = A.mptr_a[I] + lane; t < A.mptr_a[I + 1]; t += 32) {
+      const int i = A.mem_a[t];
+      s0 += A.rf[3 * i]; s1 += A.rf[3 * i + 1]; s2 += A.rf[3 * i + 2];
+    }
+    s0 = warp_sum(s0); s1 = warp_sum(s1); s2 = warp_sum(s2);
+    if (lane == 0) {
+      A.b_a[3 * I] = s0; A.b_a[3 * I + 1] = s1; A.b_a[3 * I + 2] = s2;
+      const double r[3] = {s0, s1, s2};
+      double u[3];
+      mv_minv(A.minv_a, A.na, I, r, u);
+      A.xa_a[3 * I] = om * u[0]; A.xa_a[3 * I + 1] = om * u[1]; A.xa_a[3 * I + 2] = om * u[2];
+    }
+  }
+  cl.sync();
+  // phase 2: residual of level a after the pre-sweep
+  for (int I = gw; I < A.na; I += nw) {
+    double a[3];
+    tail_row_sum(I, lane, A.sb_a, A.sw_a, A.col_a, A.val_a, A.xa_a, nullptr, nullptr, 0.0, a);
+    if (lane == 0) {
+      A.r_a[3 * I] = A.b_a[3 * I] - a[0];
+      A.r_a[3 * I + 1] = A.b_a[3 * I + 1] - a[1];
+      A.r_a[3 * I + 2] = A.b_a[3 * I + 2] - a[2];
+    }
+  }
+  cl.sync();
+  // phase 3 (every CTA, shared memory): restriction to level c and its
+  // exact solve with the dense inverse (mg_assemble builds it whenever the
+  // tail kernel is in use; N = 3 n_c <= 108)
+  for (int I = wib; I < A.nc; I += kTailNT / 32) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int t = A.mptr_c[I] + lane; t < A.mptr_c[I + 1]; t += 32) {
+      const int i = A.mem_c[t];
+      s0 += A.r_a[3 * i]; s1 += A.r_a[3 * i + 1]; s2 += A.r_a[3 * i + 2];
+    }
+    s0 = warp_sum(s0); s1 = warp_sum(s1); s2 = warp_sum(s2);
+    if (lane == 0) { bs[3 * I] = s0; bs[3 * I + 1] = s1; bs[3 * I + 2] = s2; }
+  }
+  __syncthreads();
+  {
+    const int N = 3 * A.nc;
+    for (int i = wib; i < N; i += kTailNT / 32) {
+      double acc = 0.0;
+      for (int j = lane; j < N; j += 32) acc += A.dinv[(size_t)i * N + j] * bs[j];
+      acc = warp_sum(acc);
+      if (lane == 0) xs[i] = acc;
+    }
+  }
+  __syncthreads();
+  // phase 4: post-sweep of level a with the coarse correction in its gathers
+  for (int I = gw; I < A.na; I += nw) {
+    double a[3];
+    tail_row_sum(I, lane, A.sb_a, A.sw_a, A.col_a, A.val_a, A.xa_a, xs, A.agg_c, A.alpha, a);
+    if (lane == 0) {
+      const int J = A.agg_c[I];
+      double xt[3], r[3], u[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xt[c] = A.xa_a[3 * I + c] + A.alpha * xs[3 * J + c];
+        r[c] = A.b_a[3 * I + c] - a[c];
+      }
+      mv_minv(A.minv_a, A.na, I, r, u);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) A.x_a[3 * I + c] = xt[c] + om * u[c];
+    }
+  }
+}
+
+
+// usable for the level pair (l, l+1) = (L-2, L-1)
+static bool tail_usable(const MG* mg, int la) {
+  const int L = (int)mg->lv.size();
+  return g_mg_tail && L >= 2 && la == L - 2 && la >= 1 && mg->nu == 1 && mg->gamma == 1 && mg->dinv != nullptr &&
+         mg->lv[L - 1].n <= kTailMaxC && (mg->post == 1 || mg->symmetric_needed);
+}
+
+static void launch_tail(dp_scene* s, const double* rf, const int* stop) {
+  MG* mg = s->mg;
+  const int L = (int)mg->lv.size();
+  MGLevel& a = mg->lv[L - 2];
+  MGLevel& c = mg->lv[L - 1];
+  TailArgs A;
+  A.na = a.n; A.sb_a = a.slice_base; A.sw_a = a.slice_width; A.col_a = a.col; A.val_a = a.val; A.minv_a = a.minv;
+  A.mptr_a = a.mem_ptr; A.mem_a = a.mem; A.b_a = a.b; A.xa_a = a.t; A.r_a = a.r; A.x_a = a.x;
+  A.nc = c.n; A.sb_c = c.slice_base; A.sw_c = c.slice_width; A.col_c = c.col; A.val_c = c.val; A.minv_c = c.minv;
+  A.mptr_c = c.mem_ptr; A.mem_c = c.mem; A.agg_c = c.agg; A.dinv = mg->dinv;
+  A.rf = rf; A.omega = mg->omega; A.alpha = mg->alpha; A.sweeps = mg->coarse_sweeps; A.stop = stop;
+  k_mg_tail<<<kTailCTAs, kTailNT, 0, s->stream>>>(A);
+  s->launches++;
+}
 
 static const int g_mg_fused_env = getenv("DP_MG_FUSED") ? atoi(getenv("DP_MG_FUSED")) : 0;
 
@@ -1261,6 +1434,8 @@ static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, cons
     smooth<TV>(s, L, val, minv, b, xa, nullptr, nullptr, om, nullptr, L.r, stop, 1.0);
     if (l == 0 && fused_usable(mg)) {
       launch_coarse_fused(s, L.r, stop);   // restriction to level 1 is its first phase
+    } else if (tail_usable(mg, l + 1)) {
+      launch_tail(s, L.r, stop);           // levels l+1 and l+2 in one cluster launch -> C.x
     } else if (g_mg_rj0 && l + 1 == (int)mg->lv.size() - 1 && mg->coarse_sweeps > 0) {
       // coarsest level: the restriction is the first phase of its one-CTA solve
       k_mg_coarse_jacobi<<<1, 256, 0, s->stream>>>(C.n, C.S, C.slice_base, C.slice_width, C.col, C.val, C.minv, C.b,

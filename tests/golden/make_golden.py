@@ -258,6 +258,18 @@ def cube_scene(n, model="neohookean", E=1e4, mu=0.3, sphere=False,
                       materials=mats, colliders=cols, h=0.01)
 
 
+def _label(scene, q, cp):
+    """Collider index of a contact: the collider whose normal at the
+    contact's vertex reproduces the contact frame (detection order is vertex,
+    then collider, contact.py:124-136)."""
+    x = q[3 * cp.vertex:3 * cp.vertex + 3]
+    for j, col in enumerate(scene.colliders):
+        _, nrm = col.gap_normal(x)
+        if np.array_equal(nrm, cp.frame[0]) and col.mu == cp.mu:
+            return j
+    return -1
+
+
 def run_scene(name, scene, T, tol=1e-12, v0=None, target_shift=1e-3,
               dense_newton=True, before_step=None):
     t0 = time.time()
@@ -275,6 +287,8 @@ def run_scene(name, scene, T, tol=1e-12, v0=None, target_shift=1e-3,
             for key, val in before_step(scene, k).items():
                 extra.setdefault(key, []).append(val)
             st, rep = fw.forward_step(scene, st, sysmat, cfg)
+            # collider labels while the colliders are where this step saw them
+            rep.cache._labels = [_label(scene, rep.cache.q_new, cp) for cp in rep.contacts]
             if not rep.converged:
                 raise RuntimeError(f"forward step {k} did not converge "
                                    f"(residual {rep.residual_history[-1]:.3e})")
@@ -312,17 +326,11 @@ def run_scene(name, scene, T, tol=1e-12, v0=None, target_shift=1e-3,
         # recover collider index: detection order is vertex-major, collider
         # minor (contact.py:124-136); re-run detection at q_new to label them
         q = c.q_new
-        for cp in c.contacts:
+        labels = getattr(c, "_labels", None)
+        for ci, cp in enumerate(c.contacts):
             cstep.append(k)
             cvert.append(cp.vertex)
-            x = q[3 * cp.vertex:3 * cp.vertex + 3]
-            best = -1
-            for j, col in enumerate(scene.colliders):
-                _, nrm = col.gap_normal(x)
-                if np.array_equal(nrm, cp.frame[0]) and col.mu == cp.mu:
-                    best = j
-                    break
-            ccol.append(best)
+            ccol.append(labels[ci] if labels is not None else _label(scene, q, cp))
             cframe.append(cp.frame)
             cdn.append(cp.d_n)
             clam.append(cp.lam)

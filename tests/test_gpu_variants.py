@@ -18,6 +18,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 def _digest(env_extra):
     env = dict(os.environ)
+    # the cluster tail kernel (two coarsest levels in one launch, exact
+    # coarsest solve) is a different preconditioner, not a plumbing switch:
+    # the bitwise comparisons run on the per-level V-cycle
+    env["DP_MG_TAIL"] = "0"
     env.update(env_extra)
     out = subprocess.run([sys.executable, os.path.join(HERE, "_variant_run.py")], env=env,
                          capture_output=True, text=True, timeout=600)

@@ -18,6 +18,10 @@
 #include "dp_math.cuh"
 
 namespace dp {
+std::recursive_mutex& api_mutex() {
+  static std::recursive_mutex mu;
+  return mu;
+}
 
 static thread_local std::string g_err;
 
@@ -238,11 +242,6 @@ void dp_solver_cfg_default(dp_solver_cfg* c) {
 
 // ---------------------------------------------------------------------------
 // scene
-
-std::recursive_mutex& dp::api_mutex() {
-  static std::recursive_mutex mu;
-  return mu;
-}
 
 int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   std::lock_guard<std::recursive_mutex> api_lock(dp::api_mutex());

@@ -541,8 +541,23 @@ def gpu_arm(args, rank, world, local_rank):
     stats = res[0][2]
     adj_iters = res[0][3]
 
-    # roofline: dominant kernel = the SELL-32 BSR SpMV of the Krylov solves
+    # in-situ kernel times (the roofline's "average launch duration over the
+    # timed region"): one more rollout of exactly the timed workload with a
+    # CUDA event pair around every launch of the instrumented kernels on the
+    # scene stream (no per-launch host sync; resolved afterwards).  Kept out
+    # of the timed rollout so the events do not perturb the headline number.
     c0 = ctxs[0]
+    kt = None
+    if not args.skip_insitu:
+        _lib.check(c0.L.dp_scene_enable_timing(c0.dev.handle, 1))
+        _lib.check(c0.L.dp_scene_reset_timing(c0.dev.handle))
+        device_rollout(c0, K, FINGER_K0)
+        kt = _lib.KernelTimes()
+        _lib.check(c0.L.dp_scene_get_timing(c0.dev.handle, C.byref(kt)))
+        _lib.check(c0.L.dp_scene_enable_timing(c0.dev.handle, 0))
+        kt = {f: getattr(kt, f) for f, _ in kt._fields_}
+    # standalone (cold-operand) kernel loops, for comparison
+    # roofline: dominant kernel = the SELL-32 BSR SpMV of the Krylov solves
     x = torch.randn(n3, **dd)
     y = torch.empty(n3, **dd)
     torch.cuda.synchronize()
@@ -622,7 +637,7 @@ def gpu_arm(args, rank, world, local_rank):
                "d2h_bytes_per_step": d2h}
     pool.shutdown()
     conv = [s_[0] for r in res for s_ in r[2]]
-    return dict(ms=ms_max, launches=launches, clocks=clk.summary(), spmv_ms=spmv_ms, spmv_bytes=spmv_bytes,
+    return dict(ms=ms_max, launches=launches, clocks=clk.summary(), spmv_ms=spmv_ms, spmv_bytes=spmv_bytes, kt=kt,
                 achieved=achieved, hbm=hbm, traffic=traffic, e2e=e2e, setup_s=setup_s, R=R, elem=elem,
                 smooth_ms=smooth_ms, smooth_bytes=smooth_bytes, smooth_traffic=smooth_traffic,
                 fp64_peak=float(peaks.get("fp64_tflops", FP64_PEAK_TFLOPS)),
@@ -725,6 +740,90 @@ def cpu_baseline(config, n_tets_target, n_cells, steps, procs=1, warmup=0):
 # ---------------------------------------------------------------------------
 
 
+def _frac(bytes_, ms, peak):
+    ach = bytes_ / (ms * 1e-3) / 1e9
+    return ach, ach / peak
+
+
+def roofline_smoother(r):
+    """Dominant kernel of the step (launch-list share): the fine-level V-cycle
+    sweep k_mg_smooth<float,1,*> on the FP32 SELL-32 operator copy.
+    Algorithmic bytes per launch: 36 B FP32 block + 4 B column
+    per nonzero block, slice table 4(V+1); per row the residual-form sweep
+    reads x (gathered, counted once) and b and writes r (72 B), the update
+    form reads x, b, the FP32 block-Jacobi inverse (36 B) and agg (4 B) and
+    writes z (112 B); a V-cycle runs one of each, so 92 B/row on average.
+    `achieved` uses the in-situ average launch time (CUDA events over a
+    rollout of the timed workload); the standalone loop (same kernel
+    repeated on cold operands, update form) is reported beside it."""
+    nnzb, V, hbm = r["nnzb"], r["V"], r["hbm"]
+    out = {"bound": "hbm", "unit": "GB/s", "peak": hbm,
+           "kernel": "k_mg_smooth<float,1> (fine-level V-cycle sweep, SELL-32 FP32 3x3 blocks, cp.async ring)",
+           "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+    kt = r.get("kt")
+    if kt and kt["smooth_calls"]:
+        ms = kt["smooth_ms"] / kt["smooth_calls"]
+        b = 40 * nnzb + 4 * (V + 1) + 92 * V
+        ach, fr = _frac(b, ms, hbm)
+        out.update(achieved=ach, frac=fr, ms_per_launch=ms, bytes_per_launch=b, launches=kt["smooth_calls"],
+                   timing="in situ: CUDA event pairs around every launch of one rollout of the timed workload",
+                   traffic=r["smooth_traffic"])
+    if r["smooth_ms"]:
+        b = r["smooth_bytes"]
+        ach, fr = _frac(b, r["smooth_ms"], hbm)
+        out["standalone"] = {"achieved": ach, "frac": fr, "ms_per_launch": r["smooth_ms"], "bytes_per_launch": b,
+                             "timing": "30 back-to-back launches of the update-form sweep"}
+        if "achieved" not in out:
+            out.update(achieved=ach, frac=fr, ms_per_launch=r["smooth_ms"], bytes_per_launch=b,
+                       traffic=r["smooth_traffic"])
+    return out
+
+
+def roofline_spmv(r):
+    """The Krylov SpMVs: the PCG's fused p-update + SpMV on the FP32 operator
+    copy (in situ; 40 B per block + p, z gathered and p', q written: 96 B per
+    row) and the FP64 SELL-32 SpMV k_spmv (standalone loop; 76 B per block,
+    SURVEY.md §8(d))."""
+    nnzb, V, hbm = r["nnzb"], r["V"], r["hbm"]
+    out = {"bound": "hbm", "unit": "GB/s", "peak": hbm,
+           "kernel": "k_spmv (SELL-32 3x3-BSR FP64 SpMV; k_gm_spmvdot_r / k_pcg_spmv_p are this SpMV + fusions)",
+           "achieved": r["achieved"], "frac": r["achieved"] / hbm, "traffic": r["traffic"],
+           "bytes_per_launch": r["spmv_bytes"], "ms_per_launch": r["spmv_ms"], "timing": "standalone loop",
+           "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+    kt = r.get("kt")
+    if kt and kt["pcg_spmv_calls"]:
+        ms = kt["pcg_spmv_ms"] / kt["pcg_spmv_calls"]
+        b = 40 * nnzb + 4 * (V + 1) + 96 * V
+        ach, fr = _frac(b, ms, hbm)
+        out["pcg_fused_insitu"] = {"kernel": "k_pcg_spmv_p (FP32 operator, forward PCG; FP64 for the adjoint)",
+                                   "achieved": ach, "frac": fr, "ms_per_launch": ms, "bytes_per_launch_fp32": b,
+                                   "launches": kt["pcg_spmv_calls"],
+                                   "note": "average over the FP32 (forward) and FP64 (adjoint) launches; bytes "
+                                           "counted for the FP32 form, so the FP64 share understates achieved"}
+    return out
+
+
+def roofline_fp64(r, E_tets):
+    if not r["elem"]:
+        return None
+    out = {"bound": "fp64", "kernel": "k_elements<4,JAC> (per-tet SVD + NH projection + 10 Hessian blocks)",
+           "achieved": r["elem"][1][1], "peak": r["fp64_peak"], "unit": "TFLOP/s",
+           "frac": r["elem"][1][1] / r["fp64_peak"], "ms_per_launch": r["elem"][1][0],
+           "flops_per_tet": ELEM_FLOPS_JAC, "timing": "standalone loop at the final state",
+           "residual_only": {"achieved": r["elem"][0][1], "ms_per_launch": r["elem"][0][0],
+                             "flops_per_tet": ELEM_FLOPS_RES},
+           "peak_source": "profiles/r01_fp64_peak.json (measured DFMA loop)",
+           "flops_source": "ncu 2*DFMA+DMUL+DADD thread instructions per tet at a C5 state "
+                           "(profiles/r01_elements_fp64.md)"}
+    kt = r.get("kt")
+    if kt and kt["elem_jac_calls"]:
+        ms = kt["elem_jac_ms"] / kt["elem_jac_calls"]
+        out["insitu"] = {"ms_per_launch": ms, "launches": kt["elem_jac_calls"],
+                         "achieved": ELEM_FLOPS_JAC * E_tets / (ms * 1e-3) / 1e12,
+                         "frac": ELEM_FLOPS_JAC * E_tets / (ms * 1e-3) / 1e12 / r["fp64_peak"]}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -734,6 +833,7 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-insitu", action="store_true", help="no in-situ kernel-timing rollout")
     ap.add_argument("--cpu-cells", type=int, default=0, help="cells/side of the cpu_baseline sample (c5: 8, c1: 9)")
     ap.add_argument("--cpu-steps", type=int, default=8, help="timed steps of the cpu_baseline sample")
     ap.add_argument("--ref-cells", type=int, default=10, help="cells/side of the --impl reference sample")
@@ -812,32 +912,10 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (procedural mesh, random-free)", "config": config,
                 "tet_steps_per_s_M": value * n_tets / 1e6,
-                "roofline": ({"bound": "hbm",
-                              "kernel": "k_mg_smooth<float,1> (fine-level V-cycle sweep, SELL-32 FP32 3x3 blocks; "
-                                        "largest share of the step, profiles/r01_bench_c5_launches*.md)",
-                              "achieved": r["smooth_bytes"] / (r["smooth_ms"] * 1e-3) / 1e9, "peak": r["hbm"],
-                              "unit": "GB/s",
-                              "frac": r["smooth_bytes"] / (r["smooth_ms"] * 1e-3) / 1e9 / r["hbm"],
-                              "traffic": r["smooth_traffic"], "bytes_per_launch": r["smooth_bytes"],
-                              "ms_per_launch": r["smooth_ms"],
-                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
-                             if r["smooth_ms"] else None),
-                "roofline_spmv": {"bound": "hbm", "kernel": "k_spmv (SELL-32 3x3-BSR FP64 SpMV; the GMRES column "
-                                                            "kernel k_gm_spmvdot_r is this SpMV + basis dots)",
-                                  "achieved": r["achieved"], "peak": r["hbm"], "unit": "GB/s",
-                                  "frac": r["achieved"] / r["hbm"], "traffic": r["traffic"],
-                                  "bytes_per_launch": r["spmv_bytes"], "ms_per_launch": r["spmv_ms"],
-                                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
-                "roofline_fp64": None if not r["elem"] else {
-                    "bound": "fp64", "kernel": "k_elements<4,JAC> (per-tet SVD + NH projection + 10 Hessian blocks)",
-                    "achieved": r["elem"][1][1], "peak": r["fp64_peak"], "unit": "TFLOP/s",
-                    "frac": r["elem"][1][1] / r["fp64_peak"], "ms_per_launch": r["elem"][1][0],
-                    "flops_per_tet": ELEM_FLOPS_JAC,
-                    "residual_only": {"achieved": r["elem"][0][1], "ms_per_launch": r["elem"][0][0],
-                                      "flops_per_tet": ELEM_FLOPS_RES},
-                    "peak_source": "profiles/r01_fp64_peak.json (measured DFMA loop)",
-                    "flops_source": "ncu 2*DFMA+DMUL+DADD thread instructions per tet at a C5 state "
-                                    "(profiles/r01_elements_fp64.md)"},
+                "roofline": roofline_smoother(r),
+                "roofline_spmv": roofline_spmv(r),
+                "roofline_fp64": roofline_fp64(r, E_tets=n_tets),
+                "kernel_times_insitu": r["kt"],
                 "clocks": r["clocks"], "gpu_launches": r["launches"], "e2e": r["e2e"],
                 "newton_iterations": r["newton"], "krylov_iterations": r["krylov"],
                 "adjoint_krylov_iterations": r["adj_iters"], "contacts": r["contacts"],

@@ -239,13 +239,19 @@ int dp_bench_elements(dp_scene* s, const double* q, int32_t with_jacobian, int32
  * the FP32 copy of the last assembled operator (the V-cycle's dominant
  * kernel), `reps` times; device pointers; CUDA-event time in ms_out. */
 int dp_bench_smoother(dp_scene* s, const double* x, const double* b, double* out, int32_t reps, float* ms_out);
-/* per-launch timing of the dominant kernels of the last forward step,
- * measured with CUDA events on the scene stream (ms, averages). */
+/* Kernel timing of the instrumented kernels since the last reset: total ms
+ * and launch count per kernel, from CUDA event pairs recorded around each
+ * launch on the scene stream while timing is enabled (no host
+ * synchronisation per launch; the events are resolved by
+ * dp_scene_get_timing).  smooth = the fine-level V-cycle sweep
+ * (k_mg_smooth on level 0), pcg_spmv = the PCG's fused p-update + SpMV. */
 typedef struct {
   double spmv_ms;  int64_t spmv_calls;
   double elem_jac_ms; int64_t elem_jac_calls;
   double elem_res_ms; int64_t elem_res_calls;
   double assemble_ms; int64_t assemble_calls;
+  double smooth_ms; int64_t smooth_calls;
+  double pcg_spmv_ms; int64_t pcg_spmv_calls;
 } dp_kernel_times;
 int dp_scene_enable_timing(dp_scene* s, int32_t on);
 int dp_scene_get_timing(dp_scene* s, dp_kernel_times* out);

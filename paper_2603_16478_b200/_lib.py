@@ -83,7 +83,9 @@ class KernelTimes(C.Structure):
     _fields_ = [("spmv_ms", C.c_double), ("spmv_calls", C.c_int64),
                 ("elem_jac_ms", C.c_double), ("elem_jac_calls", C.c_int64),
                 ("elem_res_ms", C.c_double), ("elem_res_calls", C.c_int64),
-                ("assemble_ms", C.c_double), ("assemble_calls", C.c_int64)]
+                ("assemble_ms", C.c_double), ("assemble_calls", C.c_int64),
+                ("smooth_ms", C.c_double), ("smooth_calls", C.c_int64),
+                ("pcg_spmv_ms", C.c_double), ("pcg_spmv_calls", C.c_int64)]
 
 
 _P = C.c_void_p

@@ -23,6 +23,51 @@ std::recursive_mutex& api_mutex() {
   return mu;
 }
 
+void ktm_begin(dp_scene* s, int k) {
+  if (!s->timing) return;
+  dp_scene::KSlot& t = s->kslot[k];
+  if (t.used == (int)t.a.size()) {
+    if (t.used >= 8192) {   // bound the pool: resolve what is recorded so far
+      ktm_flush(s);
+    } else {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      t.a.push_back(a);
+      t.b.push_back(b);
+    }
+  }
+  cudaEventRecord(t.a[t.used], s->stream);
+}
+
+void ktm_end(dp_scene* s, int k) {
+  if (!s->timing) return;
+  dp_scene::KSlot& t = s->kslot[k];
+  cudaEventRecord(t.b[t.used], s->stream);
+  ++t.used;
+}
+
+void ktm_flush(dp_scene* s) {
+  bool any = false;
+  for (auto& t : s->kslot) any |= t.used > 0;
+  if (!any) return;
+  cudaStreamSynchronize(s->stream);
+  double* ms_of[] = {&s->times.spmv_ms, &s->times.elem_jac_ms, &s->times.elem_res_ms, &s->times.assemble_ms,
+                     &s->times.smooth_ms, &s->times.pcg_spmv_ms};
+  int64_t* n_of[] = {&s->times.spmv_calls, &s->times.elem_jac_calls, &s->times.elem_res_calls,
+                     &s->times.assemble_calls, &s->times.smooth_calls, &s->times.pcg_spmv_calls};
+  for (int k = 0; k < 6; ++k) {
+    dp_scene::KSlot& t = s->kslot[k];
+    for (int i = 0; i < t.used; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, t.a[i], t.b[i]);
+      *ms_of[k] += ms;
+    }
+    *n_of[k] += t.used;
+    t.used = 0;
+  }
+}
+
 static thread_local std::string g_err;
 
 void set_error(const std::string& msg) { g_err = msg; }
@@ -601,6 +646,10 @@ int dp_scene_destroy(dp_scene* s) {
   if (!s) return DP_OK;
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
+  for (auto& t : s->kslot) {
+    for (cudaEvent_t e : t.a) cudaEventDestroy(e);
+    for (cudaEvent_t e : t.b) cudaEventDestroy(e);
+  }
   for (dp_cache* c : s->cache_pool) cache_free(c);
   s->cache_pool.clear();
   for (dp_cache* c : s->live_caches) c->scene = nullptr;   // freed by their own destroy
@@ -1573,10 +1622,12 @@ int dp_scene_enable_timing(dp_scene* s, int32_t on) {
   return DP_OK;
 }
 int dp_scene_get_timing(dp_scene* s, dp_kernel_times* out) {
+  dp::ktm_flush(s);
   *out = s->times;
   return DP_OK;
 }
 int dp_scene_reset_timing(dp_scene* s) {
+  dp::ktm_flush(s);
   s->times = dp_kernel_times{};
   s->launches = 0;
   return DP_OK;

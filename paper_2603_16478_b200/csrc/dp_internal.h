@@ -237,6 +237,11 @@ struct dp_scene {
   int timing = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   dp_kernel_times times{};
+  // event pairs per instrumented kernel (KT_*), resolved in ktm_flush
+  struct KSlot {
+    std::vector<cudaEvent_t> a, b;
+    int used = 0;
+  } kslot[8];
   int64_t launches = 0;
 
   // last assembled operator: symmetric flag
@@ -333,5 +338,10 @@ void gm_graphs_destroy(dp_scene* s);
 // another thread's capture (observed: intermittent host crash in the
 // concurrent-rollout test).  Steps themselves never take it.
 std::recursive_mutex& api_mutex();
+// kernel timing (dp_scene_enable_timing): event pair around one launch
+enum { KT_SPMV = 0, KT_ELEM_JAC = 1, KT_ELEM_RES = 2, KT_ASSEMBLE = 3, KT_SMOOTH = 4, KT_PCG_SPMV = 5 };
+void ktm_begin(dp_scene* s, int slot);
+void ktm_end(dp_scene* s, int slot);
+void ktm_flush(dp_scene* s);
 
 }  // namespace dp

@@ -463,8 +463,11 @@ void launch_elements(dp_scene* s, const double* q, int mode, int* status) {
   const int nt = 128;
   const int nb = grid_for(s->E, nt);
   const double h2 = s->h * s->h;
+  const int kt = (mode & EV_JAC) ? KT_ELEM_JAC : KT_ELEM_RES;
+  ktm_begin(s, kt);
   if (s->NV == 4) launch_elements_nv<4>(s, q, mode, status, nb, nt, h2);
   else launch_elements_nv<3>(s, q, mode, status, nb, nt, h2);
+  ktm_end(s, kt);
   s->launches++;
 }
 
@@ -790,11 +793,13 @@ void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat)
   const int nt = 256;
   const int nb = grid_for((int64_t)s->S * 32, nt);
   const int has_c = (s->colliders.n > 0) && !amat;
+  ktm_begin(s, KT_ASSEMBLE);
   k_assemble<<<nb, nt, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->diag_slot, s->rinfo,
                                        s->H, s->Ht, s->mass, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_comp,
                                        has_c ? s->c_count : nullptr, s->c_off, s->c_blk, amat ? 0 : 1,
                                        s->h * s->h, val, s->minv, amat ? nullptr : s->val32,
                                        amat ? nullptr : s->minv32);
+  ktm_end(s, KT_ASSEMBLE);
   if (!amat && s->val32) s->val32_src = val;   // the FP32 copy now mirrors `val`
   s->launches++;
 }
@@ -838,17 +843,10 @@ __global__ void __launch_bounds__(256) k_spmv(int V, int S, const int* __restric
 
 void launch_spmv(dp_scene* s, const double* val, const double* x, double* y) {
   const int nb = grid_for((int64_t)s->S * 32, 256);
-  if (s->timing) cudaEventRecord(s->ev0, s->stream);
+  ktm_begin(s, KT_SPMV);
   k_spmv<<<nb, 256, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->col, val, x, y);
+  ktm_end(s, KT_SPMV);
   s->launches++;
-  if (s->timing) {
-    cudaEventRecord(s->ev1, s->stream);
-    cudaEventSynchronize(s->ev1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, s->ev0, s->ev1);
-    s->times.spmv_ms += ms;
-    s->times.spmv_calls++;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1775,7 +1773,10 @@ static GmGraph* gm_graph(dp_scene* s, const double* val, int use_mg, int left, b
     cudaGraphDestroy(g);
     return nullptr;
   }
+  const int timing_saved = s->timing;   // no timing events inside a captured graph
+  s->timing = 0;
   nodes = gm_column(s, val, use_mg, left, tight, lowp, zbasis, h, 1);
+  s->timing = timing_saved;
   cudaGraph_t captured = nullptr;
   const cudaError_t ce = cudaStreamEndCapture(s->stream, &captured);
   nodes += (int)(s->launches - launches0);   // V-cycle kernels count themselves
@@ -2223,6 +2224,7 @@ int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x
       if (*iters + launched + m > max_iter) m = max_iter - *iters - launched;
       for (int k = 0; k < m; ++k) {
         mg_apply_prejac(s, val, r, z, &s->ksc->done);
+        ktm_begin(s, KT_PCG_SPMV);
         if (fp32)
           k_pcg_spmv_p<float><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, s->val32, z,
                                                           pb[par], pb[par ^ 1], q, s->red.partial, s->red.counter,
@@ -2231,6 +2233,7 @@ int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x
           k_pcg_spmv_p<double><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, z,
                                                            pb[par], pb[par ^ 1], q, s->red.partial, s->red.counter,
                                                            s->ksc);
+        ktm_end(s, KT_PCG_SPMV);
         k_pcg_xr_j0<<<nbv, kVT, 0, s->stream>>>(V, xc, r, pb[par ^ 1], q, minv32, omega, xa, s->red.partial,
                                                 s->red.counter, s->ksc);
         par ^= 1;

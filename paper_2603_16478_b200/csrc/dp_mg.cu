@@ -1153,6 +1153,8 @@ static void smooth(dp_scene* s, const MGLevel& L, const TV* val, const TV* minv,
     launch_pcg_rz(s, b, out, mg->dot_partial, mg->dot_counter, mg->dot_ks);
     return;
   }
+  const bool fine = (&L == &mg->lv[0]);
+  if (fine) ktm_begin(s, KT_SMOOTH);
   if (dot && mg->dot_ks && out && L.S >= 4 * 148)
     k_mg_smooth<TV, 1, true><<<grid_for((int64_t)L.S * 32, DP_SMOOTH_NT), DP_SMOOTH_NT, 0, s->stream>>>(
         L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x, xc, agg, omega, out, r_out, stop, alpha,
@@ -1163,6 +1165,7 @@ static void smooth(dp_scene* s, const MGLevel& L, const TV* val, const TV* minv,
   else
     k_mg_smooth<TV, 8><<<L.S, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x,
                                                    xc, agg, omega, out, r_out, stop, alpha);
+  if (fine) ktm_end(s, KT_SMOOTH);
   s->launches++;
 }
 

@@ -149,6 +149,14 @@ int dp_scene_set_fext(dp_scene* s, const double* fext, int32_t ptr_kind);
  * Newton solves; 2 -> multigrid for both.  omega <= 0 or nu <= 0 keeps the
  * current smoother. */
 int dp_scene_set_solver_options(dp_scene* s, int32_t use_mg, double omega, int32_t nu);
+/* Replace the per-element material parameters in place (host arrays of
+ * n_elems values in the original element order; NULL keeps a field): the
+ * element weights w, Lame mu, lambda are recomputed exactly as at scene
+ * creation (elasticity.py:67-71, 327-333) and uploaded; the pattern, element
+ * kinematics and multigrid hierarchy are kept.  Used by the batched
+ * identification loop (ident.fd_gradient) to evaluate parameter candidates
+ * on pooled device scenes instead of rebuilding one per rollout. */
+int dp_scene_set_materials(dp_scene* s, const double* E, const double* nu, const double* stiffness);
 /* multigrid hierarchy: number of levels and block rows per level (<= cap) */
 int dp_scene_get_mg_levels(const dp_scene* s, int32_t* n_levels, int32_t* rows, int32_t cap);
 /* per-element element weights w_e and host copies of vol (elasticity.py:67-71) */

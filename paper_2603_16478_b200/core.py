@@ -420,6 +420,16 @@ class DeviceScene:
         self._has_fext = fext is not None or fext_device is not None
         self._sync_sig = sig
 
+    def set_materials(self, scene):
+        """Push the scene's per-element (E, nu, stiffness) to the device scene
+        in place (dp_scene_set_materials): same pattern and kinematics, new
+        element weights and Lame parameters."""
+        mats = scene.materials
+        E = _lib.f64([m.E for m in mats])
+        nu = _lib.f64([m.nu for m in mats])
+        st = _lib.f64([m.stiffness for m in mats])
+        _lib.check(self.lib.dp_scene_set_materials(self.handle, _lib.ptr(E), _lib.ptr(nu), _lib.ptr(st)))
+
     def export_bsr(self, which):
         inf = self.info()
         rowptr = np.empty(self.n_verts + 1, np.int32)

@@ -791,6 +791,33 @@ int dp_scene_get_mg_levels(const dp_scene* s, int32_t* n_levels, int32_t* rows, 
   return DP_OK;
 }
 
+int dp_scene_set_materials(dp_scene* s, const double* E, const double* nu, const double* stiffness) {
+  invalidate_adjoint(s);
+  cudaSetDevice(s->device);
+  const int n = s->E;
+  std::vector<double> hmu(n, 0.0), hlam(n, 0.0);
+  for (int e = 0; e < n; ++e) {
+    if (E) s->h_E[e] = E[e];
+    if (nu) s->h_nu[e] = nu[e];
+    if (s->h_model[e] == DP_MODEL_NEOHOOKEAN) {
+      const double E_ = s->h_E[e], nu_ = s->h_nu[e];
+      if (!(nu_ > -1.0 && nu_ < 0.5)) { set_error("nu must lie in (-1, 0.5)"); return DP_ERR_VALUE; }
+      hmu[e] = E_ / (2.0 * (1.0 + nu_));
+      hlam[e] = E_ * nu_ / ((1.0 + nu_) * (1.0 - 2.0 * nu_));
+      s->h_w[e] = 2.0 * hmu[e] * s->h_vol[e];
+    } else if (stiffness) {
+      s->h_w[e] = stiffness[e] * s->h_vol[e];
+    }
+  }
+  if (n > 0) {
+    DP_CUDA(cudaMemcpyAsync(s->w, s->h_w.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+    DP_CUDA(cudaMemcpyAsync(s->mu, hmu.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+    DP_CUDA(cudaMemcpyAsync(s->lam, hlam.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+    DP_CUDA(cudaStreamSynchronize(s->stream));
+  }
+  return DP_OK;
+}
+
 int dp_scene_get_element_data(const dp_scene* s, double* w_out, double* vol_out) {
   if (w_out) std::memcpy(w_out, s->h_w.data(), sizeof(double) * s->E);
   if (vol_out) std::memcpy(vol_out, s->h_vol.data(), sizeof(double) * s->E);

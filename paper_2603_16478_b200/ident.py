@@ -251,10 +251,69 @@ def rollout_loss(problem, x, with_grad=False, cfg=None):
     return L, (float(g[0]) if problem.scalar else g)
 
 
-def fd_gradient(problem, x, eta=None, cfg=None, workers=None):
+_MATERIAL_VARS = ("stiffness", "E", "nu")
+
+
+class FDPool:
+    """Pooled device scenes for batched finite differences (SURVEY.md
+    §8(f)3).  Each slot owns a scene copy and its device scene, built ONCE;
+    a candidate is evaluated by resetting the slot's parameters to the base
+    values, applying the candidate through the variable setters, pushing
+    only what changed to the device (materials via dp_scene_set_materials;
+    colliders, bindings and fext via the per-step sync) and running the
+    rollout on the slot's stream.  No scene copy or device-scene rebuild per
+    rollout; the slots' rollouts run concurrently on their own streams."""
+
+    def __init__(self, problem, n_slots, device=0):
+        self.problem = problem
+        self.names = problem.names()
+        self.slots = []
+        for _ in range(n_slots):
+            sc = problem.scene.copy()
+            self.slots.append((sc, core.assemble_system_matrix(sc, device)))
+        base = problem.scene
+        self._base = dict(mats=[(m.E, m.nu, m.stiffness) for m in base.materials],
+                          mu=[c.mu for c in base.colliders],
+                          fext=None if base.fext is None else base.fext.copy(),
+                          binds=[(b.compliance, b.target.copy()) for b in base.bindings])
+
+    def _reset(self, sc):
+        b = self._base
+        if any(n in _MATERIAL_VARS for n in self.names):
+            for m, (E, nu, st) in zip(sc.materials, b["mats"]):
+                m.E, m.nu, m.stiffness = E, nu, st
+        for c, mu in zip(sc.colliders, b["mu"]):
+            c.mu = mu
+        sc.fext = None if b["fext"] is None else b["fext"].copy()
+        for bd, (comp, tgt) in zip(sc.bindings, b["binds"]):
+            bd.compliance, bd.target = comp, tgt.copy()
+
+    def loss(self, slot, x, cfg=None):
+        """Rollout loss of candidate x on pooled slot `slot`."""
+        problem = self.problem
+        sc, sm = self.slots[slot]
+        self._reset(sc)
+        state0 = sc.rest_state()
+        if problem.initial_velocity is not None:
+            state0.v[:] = problem.initial_velocity
+        xv = np.atleast_1d(np.asarray(x, dtype=np.float64))
+        for name, xi in zip(self.names, xv):
+            VARIABLES[name][0](sc, state0, xi)
+        if any(n in _MATERIAL_VARS for n in self.names):
+            sm.dev.set_materials(sc)
+            sm._A = sm._elements = None
+        states, _ = fw.rollout(sc, state0, problem.horizon, sysmat=sm, cfg=cfg)
+        return aj.loss_final_state(states[-1].q, problem.target_state)[0]
+
+
+def fd_gradient(problem, x, eta=None, cfg=None, workers=None, pool=None, batched=True):
     """Central finite difference of the rollout loss per component
     (ident.py:202-216).  The 2 n perturbed rollouts run concurrently
-    (``workers`` host threads, each rollout on its own scene stream)."""
+    (``workers`` host threads, each rollout on its own scene stream).
+    batched (default): the rollouts reuse pooled device scenes (FDPool;
+    pass ``pool`` to keep it across calls) with the perturbations applied in
+    place; batched=False rebuilds a scene per rollout (the reference's
+    path, rollout_loss)."""
     if eta is not None and eta <= 0:
         raise ValueError("eta must be positive")
     xv = np.atleast_1d(np.asarray(x, dtype=np.float64))
@@ -267,7 +326,20 @@ def fd_gradient(problem, x, eta=None, cfg=None, workers=None):
         steps.append((e, xv + d, xv - d))
     pts = [p for _, xp, xm in steps for p in (xp, xm)]
     nw = workers if workers is not None else min(len(pts), 8)
-    if nw <= 1:
+    if batched:
+        nw = max(1, nw)
+        pool = pool or FDPool(problem, nw)
+        nw = min(nw, len(pool.slots))
+        # candidate i runs on slot i % nw; each slot's candidates in order
+        def run_slot(k):
+            return [(i, pool.loss(k, pts[i], cfg)) for i in range(k, len(pts), nw)]
+        if nw == 1:
+            res = run_slot(0)
+        else:
+            with ThreadPoolExecutor(max_workers=nw) as ex:
+                res = [r for part in ex.map(run_slot, range(nw)) for r in part]
+        losses = [l for _, l in sorted(res)]
+    elif nw <= 1:
         losses = [rollout_loss(problem, p, cfg=cfg) for p in pts]
     else:
         with ThreadPoolExecutor(max_workers=nw) as ex:

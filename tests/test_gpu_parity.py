@@ -469,3 +469,39 @@ def test_c5_family_regime_vs_reference(pkg):
         a, b = getattr(gr, k), float(g[ref])
         assert abs(a - b) <= 1e-6 * abs(b) + 1e-18, (k, a, b)
     assert rel(gr.dL_dw, g["g_dw"]) < 1e-6
+
+
+def test_trajectory_recorder_matches_host_rollout(pkg, tmp_path):
+    """TrajectoryRecorder (async D2H on a copy stream) of a device-resident
+    rollout equals the public-API rollout's states bitwise; simulate() writes
+    the reference's trajectory.csv / forward.json (cli.py:81-110)."""
+    import json
+    import torch
+    from paper_2603_16478_b200 import core, forward as fw
+    from paper_2603_16478_b200.trajectory import TrajectoryRecorder, simulate
+    g = load_golden("scene_c1lite.npz")
+    scene = core.scene_from_arrays(g)
+    cfg = fw.ForwardConfig(tol=float(g["tol"]))
+    states, _ = simulate(scene, 3, str(tmp_path), cfg=cfg)
+    sm = core.assemble_system_matrix(scene)
+    dd = dict(device="cuda:0", dtype=torch.float64)
+    stream = torch.cuda.ExternalStream(sm.dev.lib.dp_scene_stream(sm.dev.handle))
+    n = scene.ndof
+    q = [torch.empty(n, **dd) for _ in range(4)]
+    v = [torch.empty(n, **dd) for _ in range(4)]
+    with torch.cuda.stream(stream):
+        q[0].copy_(torch.from_numpy(scene.vertices.reshape(-1)))
+        v[0].zero_()
+    rec = TrajectoryRecorder(n, 3)
+    rec.record(0, q[0], stream)
+    for k in range(3):
+        fw.forward_step(scene, None, sm, cfg, device_io=dict(q_bar=q[k], v_bar=v[k], q_out=q[k + 1], v_out=v[k + 1]))
+        rec.record(k + 1, q[k + 1], stream)
+    pos = rec.finish()
+    for k in range(4):
+        assert np.array_equal(pos[k].reshape(-1), states[k].q)
+    lines = (tmp_path / "trajectory.csv").read_text().splitlines()
+    assert lines[0] == "# schema: trajectory v1" and lines[1] == "step,vid,x,y,z"
+    assert len(lines) == 2 + 4 * scene.n_verts
+    rows = json.load(open(tmp_path / "forward.json"))
+    assert [r["step"] for r in rows] == [1, 2, 3] and all(r["converged"] for r in rows)

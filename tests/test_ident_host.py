@@ -63,3 +63,26 @@ def test_optimize_with_fd_check():
     assert seq == par
     m = ident.metrics(tr)
     assert m.mre_e <= 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("var,x0,target", [("E", 4.0e4, 5.0e4), ("E,nu", [4.0e4, 0.3], [5.0e4, 0.32])])
+def test_batched_fd_on_pooled_device_scenes(var, x0, target):
+    """finite differences evaluated on pooled device scenes
+    (FDPool: parameters pushed in place with dp_scene_set_materials, no scene
+    copy or device-scene rebuild per rollout) equal, bitwise, the per-rollout
+    rebuild path (the reference's rollout_loss), for one and several
+    variables; a reused pool gives the same result again."""
+    from paper_2603_16478_b200 import forward as fw, ident
+    sc = ident.scene_library()["bar_neohookean"]
+    cfg = fw.ForwardConfig(tol=1e-12)
+    prob = ident.OptProblem(sc, 4, var, np.asarray(x0), learning_rate=1.0, iterations=1,
+                            target_value=np.asarray(target))
+    ref = ident.fd_gradient(prob, x0, cfg=cfg, workers=2, batched=False)
+    pool = ident.FDPool(prob, 2)
+    got = ident.fd_gradient(prob, x0, cfg=cfg, workers=2, pool=pool)
+    again = ident.fd_gradient(prob, x0, cfg=cfg, workers=2, pool=pool)
+    assert np.array_equal(np.atleast_1d(got), np.atleast_1d(ref))
+    assert np.array_equal(np.atleast_1d(again), np.atleast_1d(ref))
+    _, g_ana = ident.rollout_loss(prob, x0, with_grad=True, cfg=cfg)
+    assert np.allclose(np.atleast_1d(g_ana), np.atleast_1d(got), rtol=1e-4)

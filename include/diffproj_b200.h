@@ -157,6 +157,24 @@ int dp_scene_set_solver_options(dp_scene* s, int32_t use_mg, double omega, int32
  * identification loop (ident.fd_gradient) to evaluate parameter candidates
  * on pooled device scenes instead of rebuilding one per rollout. */
 int dp_scene_set_materials(dp_scene* s, const double* E, const double* nu, const double* stiffness);
+/* Self-contact (no reference implementation): vertices
+ * against the scene's own surface triangles (tri: 3 n_tri vertex ids; the
+ * caller passes the boundary faces of a tet mesh or every cloth triangle),
+ * frozen at each step's q_bar.  Per step every vertex picks its candidate,
+ * the nearest non-adjacent triangle within activation + |q_hat - q_bar| of
+ * its q_bar position, and that triangle's plane (oriented to the vertex's
+ * q_bar side) is its half-space collider for the step, index n_colliders
+ * (HalfSpace detection / pullback / penetration rules).  Broad phase: a
+ * per-step device spatial hash of triangle centroids.  enable = 0 turns it
+ * off. */
+int dp_scene_set_self_contact(dp_scene* s, int32_t n_tri, const int32_t* tri, double mu, int32_t enable);
+/* Query for parity tests: build the hash at q_bar and the candidates for the
+ * predicted positions q_pred; per vertex the candidate triangle (-1: none),
+ * its squared closest-point distance at q_bar (-1: none), the oriented plane
+ * normal (3 per vertex) and offset (gap(x) = n . x - offset).  Outputs are
+ * host or device pointers (UVA); overwrites the scene's q_bar. */
+int dp_self_contact_query(dp_scene* s, const double* q_bar, const double* q_pred, int32_t ptr_kind,
+                          int32_t* tri_out, double* d2_out, double* normal_out, double* offset_out);
 /* multigrid hierarchy: number of levels and block rows per level (<= cap) */
 int dp_scene_get_mg_levels(const dp_scene* s, int32_t* n_levels, int32_t* rows, int32_t cap);
 /* per-element element weights w_e and host copies of vol (elasticity.py:67-71) */

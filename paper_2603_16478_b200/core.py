@@ -163,6 +163,11 @@ class Scene:
     eps_fb: float = 1e-6
     fext: np.ndarray | None = None
     contact_activation: float = 1e-3
+    # self-contact (no reference counterpart): vertices vs
+    # the scene's own surface triangles frozen at the step start, friction
+    # coefficient self_mu (surface_triangles, DeviceScene.sync)
+    self_contact: bool = False
+    self_mu: float = 0.0
 
     def __post_init__(self):
         self.vertices = np.array(self.vertices, dtype=np.float64).reshape(-1, 3)
@@ -221,7 +226,8 @@ class Scene:
             colliders=[_collider_from_json(c.to_json()) for c in self.colliders],
             eps_fb=self.eps_fb,
             fext=None if self.fext is None else self.fext.copy(),
-            contact_activation=self.contact_activation)
+            contact_activation=self.contact_activation,
+            self_contact=self.self_contact, self_mu=self.self_mu)
 
     # -- flattened material arrays (shared materials are cheap to expand)
     def material_arrays(self):
@@ -322,6 +328,20 @@ class Element:
     dim: int
 
 
+def surface_triangles(elements):
+    """Self-contact surface: the boundary faces of a tet mesh (faces owned by
+    exactly one tet), or every triangle of a triangle mesh; (n, 3) int32."""
+    el = np.asarray(elements, dtype=np.int64)
+    if el.size == 0:
+        return np.zeros((0, 3), np.int32)
+    if el.shape[1] == 3:
+        return el.astype(np.int32)
+    faces = np.concatenate([el[:, [0, 1, 2]], el[:, [0, 1, 3]], el[:, [0, 2, 3]], el[:, [1, 2, 3]]])
+    key = np.sort(faces, axis=1)
+    _, inv, cnt = np.unique(key, axis=0, return_inverse=True, return_counts=True)
+    return faces[cnt[inv.reshape(-1)] == 1].astype(np.int32)
+
+
 class DeviceScene:
     """Owner of a ``dp_scene*``: element data, BSR pattern, buffers, stream."""
 
@@ -403,6 +423,16 @@ class DeviceScene:
             bt = np.array([b.target for b in scene.bindings], np.float64).reshape(-1, 3)
             bc = np.array([b.compliance for b in scene.bindings], np.float64)
             _lib.check(L.dp_scene_set_bindings(self.handle, nb, _lib.ptr(bv), _lib.ptr(bt), _lib.ptr(bc)))
+        self_sig = (bool(getattr(scene, "self_contact", False)), float(getattr(scene, "self_mu", 0.0)))
+        if force or self_sig != getattr(self, "_self_sig", (False, 0.0)):
+            if self_sig[0]:
+                if getattr(self, "_surface", None) is None:
+                    self._surface = _lib.i32(surface_triangles(scene.elements).reshape(-1))
+                _lib.check(L.dp_scene_set_self_contact(self.handle, self._surface.size // 3,
+                                                       _lib.ptr(self._surface), self_sig[1], 1))
+            elif getattr(self, "_self_sig", (False, 0.0))[0]:
+                _lib.check(L.dp_scene_set_self_contact(self.handle, 0, None, 0.0, 0))
+            self._self_sig = self_sig
         if force or par_sig != prev[2]:
             g = _lib.f64(scene.gravity)
             _lib.check(L.dp_scene_set_params(self.handle, scene.h, scene.eps_fb,
@@ -424,10 +454,7 @@ class DeviceScene:
         """Push the scene's per-element (E, nu, stiffness) to the device scene
         in place (dp_scene_set_materials): same pattern and kinematics, new
         element weights and Lame parameters."""
-        mats = scene.materials
-        E = _lib.f64([m.E for m in mats])
-        nu = _lib.f64([m.nu for m in mats])
-        st = _lib.f64([m.stiffness for m in mats])
+        _, E, nu, st = scene.material_arrays()
         _lib.check(self.lib.dp_scene_set_materials(self.handle, _lib.ptr(E), _lib.ptr(nu), _lib.ptr(st)))
 
     def export_bsr(self, which):

@@ -646,6 +646,12 @@ int dp_scene_destroy(dp_scene* s) {
   if (!s) return DP_OK;
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
+  {
+    SelfContact& sc = s->self;
+    dfree(s->self_tri_d); dfree(s->self_adj_ptr_d); dfree(s->self_adj_d);
+    dfree(sc.tn); dfree(sc.cell_start); dfree(sc.cell_fill); dfree(sc.items); dfree(sc.tcell); dfree(sc.hc);
+    dfree(sc.cand); dfree(sc.cd2); dfree(sc.pn); dfree(sc.pd);
+  }
   for (auto& t : s->kslot) {
     for (cudaEvent_t e : t.a) cudaEventDestroy(e);
     for (cudaEvent_t e : t.b) cudaEventDestroy(e);
@@ -704,7 +710,7 @@ int dp_scene_set_colliders(dp_scene* s, int32_t n, const int32_t* kind, const do
   s->colliders = cs;
   DP_CUDA(cudaMemcpyAsync(s->d_colliders, &s->colliders, sizeof(ColliderSet), cudaMemcpyHostToDevice, s->stream));
   DP_CUDA(cudaStreamSynchronize(s->stream));
-  return ensure_contact_capacity(s, std::max(1, s->V * std::max(n, 1)));
+  return ensure_contact_capacity(s, std::max(1, s->V * std::max(contact_sources(s), 1)));
 }
 
 int dp_scene_set_bindings(dp_scene* s, int32_t n, const int64_t* vertex, const double* target3,
@@ -815,6 +821,67 @@ int dp_scene_set_materials(dp_scene* s, const double* E, const double* nu, const
     DP_CUDA(cudaMemcpyAsync(s->lam, hlam.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
     DP_CUDA(cudaStreamSynchronize(s->stream));
   }
+  return DP_OK;
+}
+
+int dp_scene_set_self_contact(dp_scene* s, int32_t n_tri, const int32_t* tri, double mu, int32_t enable) {
+  invalidate_adjoint(s);
+  std::lock_guard<std::recursive_mutex> api_lock(dp::api_mutex());
+  cudaSetDevice(s->device);
+  if (mu < 0) { set_error("friction coefficient must be nonnegative"); return DP_ERR_VALUE; }
+  SelfContact& sc = s->self;
+  cudaStreamSynchronize(s->stream);
+  dfree(s->self_tri_d); dfree(s->self_adj_ptr_d); dfree(s->self_adj_d);
+  dfree(sc.tn); dfree(sc.cell_start); dfree(sc.cell_fill); dfree(sc.items); dfree(sc.tcell); dfree(sc.hc);
+  dfree(sc.cand); dfree(sc.cd2); dfree(sc.pn); dfree(sc.pd);
+  sc = SelfContact{};
+  if (!enable || n_tri <= 0) return ensure_contact_capacity(s, std::max(1, s->V * std::max(contact_sources(s), 1)));
+  for (int k = 0; k < 3 * n_tri; ++k)
+    if (tri[k] < 0 || tri[k] >= s->V) { set_error("self-contact triangle vertex out of range"); return DP_ERR_VALUE; }
+  int H = 1024;
+  while (H < 2 * n_tri) H <<= 1;
+  std::vector<int> htri(tri, tri + 3 * (size_t)n_tri);
+  int rc = upload(s, &s->self_tri_d, htri);
+  rc |= upload(s, &s->self_adj_ptr_d, s->h_rowptr);
+  rc |= upload(s, &s->self_adj_d, s->h_colidx);
+  rc |= dalloc(s, &sc.tn, (size_t)3 * n_tri);
+  rc |= dalloc(s, &sc.cell_start, (size_t)H + 1);
+  rc |= dalloc(s, &sc.cell_fill, (size_t)H);
+  rc |= dalloc(s, &sc.items, (size_t)n_tri);
+  rc |= dalloc(s, &sc.tcell, (size_t)n_tri);
+  rc |= dalloc(s, &sc.hc, 2);
+  rc |= dalloc(s, &sc.cand, (size_t)s->V);
+  rc |= dalloc(s, &sc.cd2, (size_t)s->V);
+  rc |= dalloc(s, &sc.pn, (size_t)3 * s->V);
+  rc |= dalloc(s, &sc.pd, (size_t)s->V);
+  if (rc) return DP_ERR_CUDA;
+  sc.enabled = 1;
+  sc.n_tri = n_tri;
+  sc.H = H;
+  sc.mu = mu;
+  sc.tri = s->self_tri_d;
+  sc.adj_ptr = s->self_adj_ptr_d;
+  sc.adj = s->self_adj_d;
+  return ensure_contact_capacity(s, std::max(1, s->V * std::max(contact_sources(s), 1)));
+}
+
+int dp_self_contact_query(dp_scene* s, const double* q_bar, const double* q_pred, int32_t ptr_kind,
+                          int32_t* tri_out, double* d2_out, double* normal_out, double* offset_out) {
+  invalidate_adjoint(s);
+  cudaSetDevice(s->device);
+  if (!s->self.enabled) { set_error("self contact is not enabled on this scene"); return DP_ERR_VALUE; }
+  const size_t n3 = (size_t)3 * s->V;
+  int rc = copy_in(s, s->q_bar, q_bar, n3, ptr_kind);
+  if (!rc) rc = copy_in(s, s->q_try, q_pred, n3, ptr_kind);
+  if (rc) return rc;
+  launch_self_build(s);
+  launch_self_candidates(s, s->q_try);
+  DP_CUDA(cudaStreamSynchronize(s->stream));
+  const SelfContact& sc = s->self;
+  if (tri_out) DP_CUDA(cudaMemcpy(tri_out, sc.cand, sizeof(int) * s->V, cudaMemcpyDefault));
+  if (d2_out) DP_CUDA(cudaMemcpy(d2_out, sc.cd2, sizeof(double) * s->V, cudaMemcpyDefault));
+  if (normal_out) DP_CUDA(cudaMemcpy(normal_out, sc.pn, sizeof(double) * n3, cudaMemcpyDefault));
+  if (offset_out) DP_CUDA(cudaMemcpy(offset_out, sc.pd, sizeof(double) * s->V, cudaMemcpyDefault));
   return DP_OK;
 }
 
@@ -1020,6 +1087,10 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
   const double t_step0 = g_debug ? now_s() : 0.0;
   DP_CUDA(cudaMemsetAsync(s->esc, 0, sizeof(EvalScalars), s->stream));
   launch_predict(s);                                   // q_hat and q = q_hat
+  // self contact: triangles frozen at q_bar, each vertex's candidate plane
+  // for this step (no-ops when disabled)
+  launch_self_build(s);
+  launch_self_candidates(s, s->q_hat);
   launch_pullback(s, s->q, s->q_bar, cfg.pullback_margin);
   DP_CUDA(cudaMemcpyAsync(s->q_start, s->q, sizeof(double) * 3 * s->V, cudaMemcpyDeviceToDevice, s->stream));
   double scale = 1.0;

@@ -52,10 +52,235 @@ __device__ __forceinline__ void tangent_basis(const double n[3], double t1[3], d
   t2[2] = n[0] * t1[1] - n[1] * t1[0];
 }
 
+
+// ---------------------------------------------------------------------------
+// self-contact (SelfContact in dp_internal.h).  No FMA anywhere (this file is
+// compiled -fmad=false) and every dot product is ((x0 y0 + x1 y1) + x2 y2),
+// so oracle/self_contact_oracle.py reproduces pair sets and distances
+// bit for bit.
+
+__device__ __forceinline__ double sdot(const double a[3], const double b[3]) {
+  return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+}
+
+// squared distance from p to triangle (a, b, c): Voronoi-region closest
+// point (Ericson, Real-Time Collision Detection 5.1.5)
+__device__ double tri_dist2(const double p[3], const double a[3], const double b[3], const double c[3]) {
+  double ab[3], ac[3], ap[3], q[3];
+  for (int i = 0; i < 3; ++i) { ab[i] = b[i] - a[i]; ac[i] = c[i] - a[i]; ap[i] = p[i] - a[i]; }
+  const double d1 = sdot(ab, ap), d2 = sdot(ac, ap);
+  if (d1 <= 0.0 && d2 <= 0.0) {
+    for (int i = 0; i < 3; ++i) q[i] = a[i];
+  } else {
+    double bp[3];
+    for (int i = 0; i < 3; ++i) bp[i] = p[i] - b[i];
+    const double d3 = sdot(ab, bp), d4 = sdot(ac, bp);
+    const double vc = d1 * d4 - d3 * d2;
+    double cp[3];
+    for (int i = 0; i < 3; ++i) cp[i] = p[i] - c[i];
+    const double d5 = sdot(ab, cp), d6 = sdot(ac, cp);
+    const double vb = d5 * d2 - d1 * d6;
+    const double va = d3 * d6 - d5 * d4;
+    if (d3 >= 0.0 && d4 <= d3) {
+      for (int i = 0; i < 3; ++i) q[i] = b[i];
+    } else if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+      const double v = d1 / (d1 - d3);
+      for (int i = 0; i < 3; ++i) q[i] = a[i] + v * ab[i];
+    } else if (d6 >= 0.0 && d5 <= d6) {
+      for (int i = 0; i < 3; ++i) q[i] = c[i];
+    } else if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+      const double w = d2 / (d2 - d6);
+      for (int i = 0; i < 3; ++i) q[i] = a[i] + w * ac[i];
+    } else if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+      const double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+      for (int i = 0; i < 3; ++i) q[i] = b[i] + w * (c[i] - b[i]);
+    } else {
+      const double denom = 1.0 / (va + vb + vc);
+      const double v = vb * denom, w = vc * denom;
+      for (int i = 0; i < 3; ++i) q[i] = a[i] + ab[i] * v + ac[i] * w;
+    }
+  }
+  double d[3];
+  for (int i = 0; i < 3; ++i) d[i] = p[i] - q[i];
+  return sdot(d, d);
+}
+
+__device__ __forceinline__ long long cell_of(double x, double hc) { return (long long)floor(x / hc); }
+
+__device__ __forceinline__ int cell_hash(long long cx, long long cy, long long cz, int H) {
+  const unsigned long long h = (unsigned long long)(cx * 73856093LL) ^ (unsigned long long)(cy * 19349663LL) ^
+                               (unsigned long long)(cz * 83492791LL);
+  return (int)(h & (unsigned long long)(H - 1));
+}
+
+__device__ __forceinline__ bool in_ring(const SelfContact& sc, int v, int u) {
+  for (int k = sc.adj_ptr[v]; k < sc.adj_ptr[v + 1]; ++k)
+    if (sc.adj[k] == u) return true;
+  return false;
+}
+
+// candidate of vertex v: the nearest non-adjacent surface triangle (at q_bar)
+// to its q_bar position within radius R (distance^2 <= R^2; ties to the lower
+// index), scanning the cells within ceil(R / cell) of it; -1 if none
+__device__ int self_nearest(const SelfContact& sc, int v, const double x[3], double R, double* d2_out) {
+  const double hc = sc.hc[0];
+  const long long cx = cell_of(x[0], hc), cy = cell_of(x[1], hc), cz = cell_of(x[2], hc);
+  const int k = min(4, max(1, (int)ceil(R / hc)));
+  double best = R * R;
+  int bt = -1;
+  for (int dz = -k; dz <= k; ++dz)
+    for (int dy = -k; dy <= k; ++dy)
+      for (int dx = -k; dx <= k; ++dx) {
+        const int h = cell_hash(cx + dx, cy + dy, cz + dz, sc.H);
+        for (int j = sc.cell_start[h]; j < sc.cell_start[h + 1]; ++j) {
+          const int t = sc.items[j];
+          if (bt >= 0 && t == bt) continue;
+          const int ia = sc.tri[3 * t], ib = sc.tri[3 * t + 1], ic = sc.tri[3 * t + 2];
+          const double a[3] = {sc.qb[3 * ia], sc.qb[3 * ia + 1], sc.qb[3 * ia + 2]};
+          const double b[3] = {sc.qb[3 * ib], sc.qb[3 * ib + 1], sc.qb[3 * ib + 2]};
+          const double c[3] = {sc.qb[3 * ic], sc.qb[3 * ic + 1], sc.qb[3 * ic + 2]};
+          const double d2 = tri_dist2(x, a, b, c);
+          if (!(d2 < best || (d2 == best && (bt < 0 || t < bt)))) continue;
+          if (in_ring(sc, v, ia) || in_ring(sc, v, ib) || in_ring(sc, v, ic)) continue;
+          best = d2;
+          bt = t;
+        }
+      }
+  if (d2_out) *d2_out = best;
+  return bt;
+}
+
+// gap of vertex v at x against its self-contact plane (valid if cand >= 0)
+__device__ __forceinline__ double self_gap(const SelfContact& sc, int v, const double x[3], double n[3]) {
+  n[0] = sc.pn[3 * v]; n[1] = sc.pn[3 * v + 1]; n[2] = sc.pn[3 * v + 2];
+  return sdot(n, x) - sc.pd[v];
+}
+
+// per vertex, once per step (after the prediction): candidate triangle and
+// its oriented plane
+__global__ void k_self_candidates(SelfContact sc, int V, const double* __restrict__ q_pred, double act) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const double xb[3] = {sc.qb[3 * v], sc.qb[3 * v + 1], sc.qb[3 * v + 2]};
+  const double dp[3] = {q_pred[3 * v] - xb[0], q_pred[3 * v + 1] - xb[1], q_pred[3 * v + 2] - xb[2]};
+  const double R = act + sqrt(sdot(dp, dp));
+  double d2 = 0.0;
+  const int t = self_nearest(sc, v, xb, R, &d2);
+  sc.cand[v] = t;
+  sc.cd2[v] = t >= 0 ? d2 : -1.0;
+  if (t < 0) return;
+  const int ia = sc.tri[3 * t];
+  const double a[3] = {sc.qb[3 * ia], sc.qb[3 * ia + 1], sc.qb[3 * ia + 2]};
+  const double m[3] = {sc.tn[3 * t], sc.tn[3 * t + 1], sc.tn[3 * t + 2]};
+  const double rel[3] = {xb[0] - a[0], xb[1] - a[1], xb[2] - a[2]};
+  const double sg = sdot(m, rel) < 0.0 ? -1.0 : 1.0;
+  const double n[3] = {sg * m[0], sg * m[1], sg * m[2]};
+  for (int i = 0; i < 3; ++i) sc.pn[3 * v + i] = n[i];
+  sc.pd[v] = sdot(n, a);
+}
+
+void launch_self_candidates(dp_scene* s, const double* q_pred) {
+  if (!s->self.enabled || s->self.n_tri == 0) return;
+  k_self_candidates<<<grid_for(s->V, 128), 128, 0, s->stream>>>(s->self, s->V, q_pred, s->act);
+  s->launches++;
+}
+
+// per-step build at q_bar --------------------------------------------------
+__global__ void k_self_radius(SelfContact sc, unsigned long long* rmax_bits) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= sc.n_tri) return;
+  const int id[3] = {sc.tri[3 * t], sc.tri[3 * t + 1], sc.tri[3 * t + 2]};
+  double P[3][3], c[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < 3; ++k)
+    for (int i = 0; i < 3; ++i) { P[k][i] = sc.qb[3 * id[k] + i]; c[i] += P[k][i]; }
+  for (int i = 0; i < 3; ++i) c[i] /= 3.0;
+  double r2 = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    double d[3] = {P[k][0] - c[0], P[k][1] - c[1], P[k][2] - c[2]};
+    r2 = fmax(r2, sdot(d, d));
+  }
+  // normal (unit) at q_bar
+  double e1[3], e2[3], nn[3];
+  for (int i = 0; i < 3; ++i) { e1[i] = P[1][i] - P[0][i]; e2[i] = P[2][i] - P[0][i]; }
+  nn[0] = e1[1] * e2[2] - e1[2] * e2[1];
+  nn[1] = e1[2] * e2[0] - e1[0] * e2[2];
+  nn[2] = e1[0] * e2[1] - e1[1] * e2[0];
+  const double l = sqrt(sdot(nn, nn));
+  for (int i = 0; i < 3; ++i) sc.tn[3 * t + i] = l > 0.0 ? nn[i] / l : 0.0;
+  atomicMax(rmax_bits, (unsigned long long)__double_as_longlong(sqrt(r2)));   // r >= 0: bit order = value order
+}
+
+__global__ void k_self_cellsize(SelfContact sc, const unsigned long long* rmax_bits, double act) {
+  // cell >= activation + largest centroid radius (and never 0)
+  sc.hc[0] = fmax((__longlong_as_double((long long)*rmax_bits) + act) * 1.000001, 1e-12);
+}
+
+__global__ void k_self_count(SelfContact sc) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= sc.n_tri) return;
+  const double hc = sc.hc[0];
+  double c[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < 3; ++k)
+    for (int i = 0; i < 3; ++i) c[i] += sc.qb[3 * sc.tri[3 * t + k] + i];
+  for (int i = 0; i < 3; ++i) c[i] /= 3.0;
+  const int h = cell_hash(cell_of(c[0], hc), cell_of(c[1], hc), cell_of(c[2], hc), sc.H);
+  sc.tcell[t] = h;
+  atomicAdd(&sc.cell_fill[h], 1);
+}
+
+// exclusive scan of the H bucket counts in one CTA; cell_fill becomes the
+// fill cursor (0)
+__global__ void __launch_bounds__(1024) k_self_scan(SelfContact sc) {
+  __shared__ int part[1024];
+  const int H = sc.H, nt = blockDim.x, t = threadIdx.x;
+  const int per = (H + nt - 1) / nt, lo = t * per, hi = min(H, lo + per);
+  int sum = 0;
+  for (int i = lo; i < hi; ++i) sum += sc.cell_fill[i];
+  part[t] = sum;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {
+    const int v = (t >= off) ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int run = part[t] - sum;
+  for (int i = lo; i < hi; ++i) {
+    const int c = sc.cell_fill[i];
+    sc.cell_start[i] = run;
+    sc.cell_fill[i] = 0;
+    run += c;
+  }
+  if (t == nt - 1) sc.cell_start[H] = part[nt - 1];
+}
+
+__global__ void k_self_fill(SelfContact sc) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= sc.n_tri) return;
+  const int h = sc.tcell[t];
+  sc.items[sc.cell_start[h] + atomicAdd(&sc.cell_fill[h], 1)] = t;
+}
+
+void launch_self_build(dp_scene* s) {
+  SelfContact& sc = s->self;
+  if (!sc.enabled || sc.n_tri == 0) return;
+  sc.qb = s->q_bar;
+  unsigned long long* rbits = reinterpret_cast<unsigned long long*>(sc.hc + 1);
+  cudaMemsetAsync(rbits, 0, sizeof(unsigned long long), s->stream);
+  cudaMemsetAsync(sc.cell_fill, 0, sizeof(int) * sc.H, s->stream);
+  const int nb = grid_for(sc.n_tri, 256);
+  k_self_radius<<<nb, 256, 0, s->stream>>>(sc, rbits);
+  k_self_cellsize<<<1, 1, 0, s->stream>>>(sc, rbits, s->act);
+  k_self_count<<<nb, 256, 0, s->stream>>>(sc);
+  k_self_scan<<<1, 1024, 0, s->stream>>>(sc);
+  k_self_fill<<<nb, 256, 0, s->stream>>>(sc);
+  s->launches += 5;
+}
+
 // ---------------------------------------------------------------------------
 // pullback (forward._pullback, forward.py:63-83)
 __global__ void k_pullback(int V, const ColliderSet* __restrict__ csp, double* __restrict__ q,
-                           const double* __restrict__ q_bar, double margin) {
+                           const double* __restrict__ q_bar, double margin, SelfContact sc, double act) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
   const ColliderSet& cs = *csp;
@@ -78,18 +303,36 @@ __global__ void k_pullback(int V, const ColliderSet* __restrict__ csp, double* _
       moved = true;
     }
   }
+  if (sc.enabled && sc.cand[v] >= 0) {
+    // the self "collider" after the analytic ones, the HalfSpace rule
+    double n[3];
+    const double gap = self_gap(sc, v, x, n);
+    if (gap <= 0.0) {
+      double target = margin;
+      if (q_bar) {
+        const double xb[3] = {q_bar[3 * v], q_bar[3 * v + 1], q_bar[3 * v + 2]};
+        double nb[3];
+        const double gp = self_gap(sc, v, xb, nb);
+        if (gp > 0.0) target = fmin(margin, gp);
+      }
+      target = fmax(target, 1e-12);
+      const double d = target - gap;
+      for (int i = 0; i < 3; ++i) x[i] = x[i] + d * n[i];
+      moved = true;
+    }
+  }
   if (moved) { q[3 * v] = x[0]; q[3 * v + 1] = x[1]; q[3 * v + 2] = x[2]; }
 }
 
 void launch_pullback(dp_scene* s, double* q, const double* q_bar, double margin) {
-  if (s->colliders.n == 0) return;
-  k_pullback<<<grid_for(s->V, 256), 256, 0, s->stream>>>(s->V, s->d_colliders, q, q_bar, margin);
+  if (contact_sources(s) == 0) return;
+  k_pullback<<<grid_for(s->V, 256), 256, 0, s->stream>>>(s->V, s->d_colliders, q, q_bar, margin, s->self, s->act);
   s->launches++;
 }
 
 // _any_penetration (forward.py:86-93)
 __global__ void k_penetration(int V, const ColliderSet* __restrict__ csp, const double* __restrict__ q,
-                              EvalScalars* esc) {
+                              EvalScalars* esc, SelfContact sc, double act) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
   const ColliderSet& cs = *csp;
@@ -98,18 +341,22 @@ __global__ void k_penetration(int V, const ColliderSet* __restrict__ csp, const 
     double n[3];
     if (gap_normal(cs, j, x, n) <= 0.0) { esc->penetrating = 1; esc->skip = 1; return; }
   }
+  if (sc.enabled && sc.cand[v] >= 0) {
+    double n[3];
+    if (self_gap(sc, v, x, n) <= 0.0) { esc->penetrating = 1; esc->skip = 1; }
+  }
 }
 
 void launch_penetration(dp_scene* s, const double* q, EvalScalars* esc) {
-  if (s->colliders.n == 0) return;
-  k_penetration<<<grid_for(s->V, 256), 256, 0, s->stream>>>(s->V, s->d_colliders, q, esc);
+  if (contact_sources(s) == 0) return;
+  k_penetration<<<grid_for(s->V, 256), 256, 0, s->stream>>>(s->V, s->d_colliders, q, esc, s->self, s->act);
   s->launches++;
 }
 
 // ---------------------------------------------------------------------------
 // detection: count -> exclusive scan -> write (order: vertex, then collider)
 __global__ void k_detect_count(int V, const ColliderSet* __restrict__ csp, const double* __restrict__ q, double act,
-                               int* __restrict__ count) {
+                               int* __restrict__ count, SelfContact sc) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v > V) return;
   if (v == V) { count[V] = 0; return; }
@@ -120,13 +367,17 @@ __global__ void k_detect_count(int V, const ColliderSet* __restrict__ csp, const
     double n[3];
     if (!(gap_normal(cs, j, x, n) > act)) ++c;
   }
+  if (sc.enabled && sc.cand[v] >= 0) {
+    double n[3];
+    if (!(self_gap(sc, v, x, n) > act)) ++c;
+  }
   count[v] = c;
 }
 
 __global__ void k_detect_write(int V, const ColliderSet* __restrict__ csp, const double* __restrict__ q, double act,
                                const int* __restrict__ off, int* __restrict__ cvtx, int* __restrict__ ccol,
                                double* __restrict__ cframe, double* __restrict__ cdn, double* __restrict__ cmu,
-                               EvalScalars* esc) {
+                               EvalScalars* esc, SelfContact sc) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v == 0) esc->n_contacts = off[V];
   if (v >= V) return;
@@ -149,6 +400,21 @@ __global__ void k_detect_write(int V, const ColliderSet* __restrict__ csp, const
     cmu[o] = cs.mu[j];
     ++o;
   }
+  if (sc.enabled && sc.cand[v] >= 0) {
+    // self contact: collider index n_colliders, frame from the frozen
+    // triangle plane's oriented normal
+    double n[3], t1[3], t2[3];
+    const double gap = self_gap(sc, v, x, n);
+    if (!(gap > act)) {
+      tangent_basis(n, t1, t2);
+      cvtx[o] = v;
+      ccol[o] = cs.n;
+      double* fr = cframe + (size_t)o * 9;
+      for (int i = 0; i < 3; ++i) { fr[i] = n[i]; fr[3 + i] = t1[i]; fr[6 + i] = t2[i]; }
+      cdn[o] = dot3(n, x) - gap;
+      cmu[o] = sc.mu;
+    }
+  }
 }
 
 int contact_scan_setup(dp_scene* s) {
@@ -164,15 +430,16 @@ int contact_scan_setup(dp_scene* s) {
 
 void launch_detect(dp_scene* s, const double* q) {
   const int V = s->V;
-  if (s->colliders.n == 0) {
+  if (contact_sources(s) == 0) {
     cudaMemsetAsync(&s->esc->n_contacts, 0, sizeof(int), s->stream);
     return;
   }
-  k_detect_count<<<grid_for(V + 1, 256), 256, 0, s->stream>>>(V, s->d_colliders, q, s->act, s->c_count);
+  k_detect_count<<<grid_for(V + 1, 256), 256, 0, s->stream>>>(V, s->d_colliders, q, s->act, s->c_count, s->self);
   size_t bytes = s->scan_tmp_bytes;
   cub::DeviceScan::ExclusiveSum(s->scan_tmp, bytes, s->c_count, s->c_off, V + 1, s->stream);
   k_detect_write<<<grid_for(V, 256), 256, 0, s->stream>>>(V, s->d_colliders, q, s->act, s->c_off, s->c_vertex,
-                                                          s->c_collider, s->c_frame, s->c_dn, s->c_mu, s->esc);
+                                                          s->c_collider, s->c_frame, s->c_dn, s->c_mu, s->esc,
+                                                          s->self);
   s->launches += 3;
 }
 
@@ -245,7 +512,7 @@ __global__ void k_contacts(const int* __restrict__ n_ptr, int n_fixed, const dou
 void launch_contacts(dp_scene* s, const double* q, const double* q_bar, int n_contacts, const int* vtx,
                      const double* frame, const double* dn, const double* mu, double* delta_out, int from_delta,
                      int transpose, EvalScalars* esc) {
-  if (s->colliders.n == 0 && n_contacts <= 0) return;
+  if (contact_sources(s) == 0 && n_contacts <= 0) return;
   // n_contacts < 0: the count lives on device (esc->n_contacts), launch over capacity
   const int cap = n_contacts >= 0 ? n_contacts : s->ccap;
   if (cap == 0) return;

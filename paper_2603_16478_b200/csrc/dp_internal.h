@@ -96,6 +96,42 @@ struct ColliderSet {
   double mu[kMaxColliders];
 };
 
+// Self-contact (the reference has none): vertices against
+// the mesh's own surface triangles, FROZEN at the step's start positions
+// q_bar (a lagged obstacle, re-read every step like the analytic colliders,
+// contact.py:125-127).  Once per step every vertex v picks its candidate: the
+// nearest non-adjacent surface triangle (closest-point distance at q_bar, ties
+// to the lower index) within R_v = activation + |q_hat_v - q_bar_v| (the
+// predicted motion).  For the rest of the step that triangle's plane,
+// oriented to the side v was on at q_bar, is v's half-space collider (index
+// n_colliders): detection (gap <= activation), pullback and the penetration
+// test are the reference's HalfSpace rules (forward.py:63-93,
+// contact.py:115-136), and every downstream kernel (condensation, blocks,
+// adjoint) is unchanged.  An infinite plane per vertex also catches a vertex
+// that would cross its triangle in one Newton step.  Broad phase: a uniform-
+// grid spatial hash of the triangle centroids, rebuilt on the device each
+// step (cell = activation + the largest centroid radius).
+struct SelfContact {
+  int enabled = 0;
+  int n_tri = 0;
+  int H = 0;                       // hash table size (power of two)
+  double mu = 0.0;
+  const int* tri = nullptr;        // 3 n_tri vertex ids
+  const int* adj_ptr = nullptr;    // vertex graph CSR (the block pattern: 1-ring incl. the vertex)
+  const int* adj = nullptr;
+  double* tn = nullptr;            // unit triangle normals at q_bar (3 n_tri)
+  int* cell_start = nullptr;       // H + 1
+  int* cell_fill = nullptr;        // H (counts, then fill cursors)
+  int* items = nullptr;            // n_tri triangle ids bucketed by cell hash
+  int* tcell = nullptr;            // n_tri: hash of each triangle's centroid cell
+  double* hc = nullptr;            // device scalars: cell size, radius scratch
+  int* cand = nullptr;             // per vertex: candidate triangle of this step (-1: none)
+  double* cd2 = nullptr;           // per vertex: its closest-point distance^2 at q_bar
+  double* pn = nullptr;            // per vertex: oriented plane normal (3V)
+  double* pd = nullptr;            // per vertex: plane offset n . a
+  const double* qb = nullptr;      // positions the structure was built from (the scene's q_bar)
+};
+
 // reduction scratch: partial sums per block + a completion counter
 struct Reduce {
   double* partial = nullptr;     // [nblocks * width]
@@ -195,6 +231,10 @@ struct dp_scene {
 
   // contacts (capacity V * n_colliders)
   int ccap = 0;
+  dp::SelfContact self;             // self-contact (disabled unless dp_scene_set_self_contact)
+  int* self_tri_d = nullptr;        // owned device storage behind `self`
+  int* self_adj_ptr_d = nullptr;
+  int* self_adj_d = nullptr;
   int *c_count = nullptr, *c_off = nullptr, *c_vertex = nullptr, *c_collider = nullptr;
   double *c_frame = nullptr, *c_dn = nullptr, *c_mu = nullptr, *c_delta = nullptr;
   double *c_blk = nullptr, *c_force = nullptr, *c_kmu = nullptr, *c_kc = nullptr;
@@ -329,6 +369,8 @@ int mg_level_rows(const dp_scene* s, int l);
 void mg_set_params(dp_scene* s, double omega, int nu);
 void mg_set_symmetric(dp_scene* s, int on);
 void mg_set_pcg_dot(dp_scene* s, double* partial, unsigned int* counter, KrylovScalars* ks);
+void launch_self_build(dp_scene* s);
+void launch_self_candidates(dp_scene* s, const double* q_pred);
 void launch_pcg_rz(dp_scene* s, const double* r, const double* z, double* partial, unsigned int* counter,
                    KrylovScalars* ks);
 void gm_graphs_destroy(dp_scene* s);
@@ -338,6 +380,8 @@ void gm_graphs_destroy(dp_scene* s);
 // another thread's capture (observed: intermittent host crash in the
 // concurrent-rollout test).  Steps themselves never take it.
 std::recursive_mutex& api_mutex();
+// analytic colliders + the self-contact "collider" (index n_colliders)
+inline int contact_sources(const dp_scene* s) { return s->colliders.n + (s->self.enabled ? 1 : 0); }
 // kernel timing (dp_scene_enable_timing): event pair around one launch
 enum { KT_SPMV = 0, KT_ELEM_JAC = 1, KT_ELEM_RES = 2, KT_ASSEMBLE = 3, KT_SMOOTH = 4, KT_PCG_SPMV = 5 };
 void ktm_begin(dp_scene* s, int slot);

@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(kVT) k_residual(int V, const double* __restric
 
 void launch_residual(dp_scene* s, const double* q, const double* q_hat, double* r, EvalScalars* esc) {
   const int nb = grid_for(s->V, kVT);
-  const int has_c = s->colliders.n > 0;
+  const int has_c = contact_sources(s) > 0;
   k_residual<<<nb, kVT, 0, s->stream>>>(s->V, s->mass, q, q_hat, s->inc_ptr, s->inc, s->fe, s->nb ? s->b_ptr : nullptr,
                                         s->b_idx, s->b_target, s->b_comp, s->c_count, s->c_off, s->c_force, has_c,
                                         s->h * s->h, r, s->red.partial, s->red.counter, esc, s->eval_skip);
@@ -649,7 +649,7 @@ void launch_watch_elements(dp_scene* s, const double* q) {
 }
 
 void launch_watch_check(dp_scene* s, const double* q, double rmax_prev) {
-  const int has_c = s->colliders.n > 0;
+  const int has_c = contact_sources(s) > 0;
   k_watch_check<<<grid_for(kWatchMax, 128), 128, 0, s->stream>>>(
       s->watch_v, s->mass, q, s->q_hat, s->inc_ptr, s->inc, s->fe, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_target,
       s->b_comp, s->c_count, s->c_off, s->c_force, has_c, s->h * s->h, rmax_prev, s->esc);
@@ -792,7 +792,7 @@ void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat)
   (void)transpose_contacts;   // contact blocks are already stored transposed by the contact kernel
   const int nt = 256;
   const int nb = grid_for((int64_t)s->S * 32, nt);
-  const int has_c = (s->colliders.n > 0) && !amat;
+  const int has_c = (contact_sources(s) > 0) && !amat;
   ktm_begin(s, KT_ASSEMBLE);
   k_assemble<<<nb, nt, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->diag_slot, s->rinfo,
                                        s->H, s->Ht, s->mass, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_comp,

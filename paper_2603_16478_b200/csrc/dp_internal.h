@@ -42,6 +42,8 @@ struct KrylovScalars {
   double bnorm2, tol2;                      // |b|^2, (tol*|b|)^2
   int done;                                 // 1 converged, 2 breakdown
   int iters;
+  int maxit;                                // PCG graph loop: stop after this many iterations
+  int pad_i;
   double pad[2];
 };
 

@@ -1985,7 +1985,7 @@ __device__ __forceinline__ void minv32_apply(const float* __restrict__ minv, int
 __global__ void __launch_bounds__(kVT) k_pcg_init(int V, const double* __restrict__ b, double* x, double* r, double* p,
                                                   double rtol, double* partial, unsigned int* counter,
                                                   KrylovScalars* ks, const float* __restrict__ minv32, double omega,
-                                                  double* __restrict__ xa) {
+                                                  double* __restrict__ xa, int maxit) {
   __shared__ double sh[32];
   __shared__ double out[1];
   const int i = blockIdx.x * kVT + threadIdx.x;
@@ -2015,10 +2015,17 @@ __global__ void __launch_bounds__(kVT) k_pcg_init(int V, const double* __restric
       ks->tol2 = rtol * rtol * out[0];
       ks->gamma = 0.0; ks->beta = 0.0; ks->alpha = 0.0;
       ks->iters = 0;
+      ks->maxit = maxit;
       ks->done = (out[0] == 0.0) ? 1 : 0;
       *counter = 0;
     }
   }
+}
+
+// graph loop control: continue while not done and within the budget
+__global__ void k_pcg_loopctl(const KrylovScalars* ks, cudaGraphConditionalHandle handle) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  cudaGraphSetConditional(handle, (!ks->done && ks->iters < ks->maxit) ? 1u : 0u);
 }
 
 // gamma' = (r, z); beta = gamma'/gamma (0 on the first iteration): the
@@ -2170,6 +2177,88 @@ int pcg_mg_solve(dp_scene* s, const double* val, const double* b, double* x, dou
   return rc;
 }
 
+// one PCG iteration (V-cycle, fused p-update SpMV, fused x/r update + the
+// next V-cycle's first Jacobi sweep) reading p from pin and writing pout
+static void pcg_iteration(dp_scene* s, const double* val, int fp32, const double* pin, double* pout,
+                          const float* minv32, double omega, double* xa) {
+  const int V = s->V;
+  const int nbv = grid_for(V, kVT);
+  const int nbs = grid_for((int64_t)s->S * 32, 256);
+  double *r = s->kr, *z = s->ku, *q = s->kw, *xc = s->kx;
+  mg_apply_prejac(s, val, r, z, &s->ksc->done);
+  ktm_begin(s, KT_PCG_SPMV);
+  if (fp32)
+    k_pcg_spmv_p<float><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, s->val32, z, pin,
+                                                    pout, q, s->red.partial, s->red.counter, s->ksc);
+  else
+    k_pcg_spmv_p<double><<<nbs, 256, 0, s->stream>>>(V, s->S, s->slice_base, s->slice_width, s->col, val, z, pin,
+                                                     pout, q, s->red.partial, s->red.counter, s->ksc);
+  ktm_end(s, KT_PCG_SPMV);
+  k_pcg_xr_j0<<<nbv, kVT, 0, s->stream>>>(V, xc, r, pout, q, minv32, omega, xa, s->red.partial, s->red.counter,
+                                          s->ksc);
+  s->launches += 2;
+}
+
+// Device-driven PCG loop: a CUDA graph whose WHILE node runs two iterations
+// (the two p-buffer parities) per pass until done or the budget is spent, so
+// a whole inexact Newton solve is one graph launch and one host sync.
+static GmGraph* pcg_graph(dp_scene* s, const double* val, int fp32) {
+  const uint64_t key = (uint64_t)(uintptr_t)val ^ ((uint64_t)fp32 << 6) ^ (1ull << 7);
+  for (auto& e : s->gm_graphs)
+    if (e.first == key) return (GmGraph*)e.second;
+  std::lock_guard<std::recursive_mutex> api_lock(api_mutex());
+  const float* minv32 = nullptr;
+  double* xa = nullptr;
+  double omega = 0.0;
+  mg_fine_jacobi0_target(s, &minv32, &xa, &omega);
+  cudaGraph_t g = nullptr;
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return nullptr;
+  cudaGraphConditionalHandle h;
+  if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return nullptr;
+  }
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, nullptr, 0, &cp) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return nullptr;
+  }
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  const int64_t launches0 = s->launches;
+  if (cudaStreamBeginCaptureToGraph(s->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+      cudaSuccess) {
+    cudaGraphDestroy(g);
+    return nullptr;
+  }
+  const int timing_saved = s->timing;   // no timing events inside a captured graph
+  s->timing = 0;
+  pcg_iteration(s, val, fp32, s->kp, s->ks, minv32, omega, xa);
+  pcg_iteration(s, val, fp32, s->ks, s->kp, minv32, omega, xa);
+  k_pcg_loopctl<<<1, 32, 0, s->stream>>>(s->ksc, h);
+  s->launches++;
+  s->timing = timing_saved;
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(s->stream, &captured);
+  const int nodes = (int)(s->launches - launches0);
+  s->launches = launches0;
+  GmGraph* gg = new GmGraph();
+  if (ce != cudaSuccess || cudaGraphInstantiate(&gg->exec, g, 0) != cudaSuccess) {
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    delete gg;
+    return nullptr;
+  }
+  cudaGraphDestroy(g);
+  gg->nodes = nodes;
+  s->gm_graphs.push_back({key, (void*)gg});
+  return gg;
+}
+
 int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,
                       int* iters, double* relres, int* breakdown, int fp32, const double* x0) {
   const int V = s->V, n = 3 * V;
@@ -2216,9 +2305,17 @@ int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x
     inner = fmin(0.5, fmax(inner, 1e-15));
     int par = 0;
     k_pcg_init<<<nbv, kVT, 0, s->stream>>>(V, bb, xc, r, pb[0], inner, s->red.partial, s->red.counter, s->ksc, minv32,
-                                           omega, xa);
+                                           omega, xa, max_iter - *iters);
     s->launches++;
     int done = 0, launched = 0, chunk = 4;
+    GmGraph* gg = (g_use_graphs && !s->timing) ? pcg_graph(s, val, fp32) : nullptr;
+    if (gg) {
+      // the whole solve on the device: one graph launch, one sync
+      cudaGraphLaunch(gg->exec, s->stream);
+      read_ksc(s);
+      done = 1;
+      s->launches += (int64_t)(gg->nodes / 2) * std::max(1, s->h_ksc->iters);
+    }
     while (!done && *iters + launched < max_iter) {
       int m = chunk;
       if (*iters + launched + m > max_iter) m = max_iter - *iters - launched;

@@ -587,7 +587,8 @@ def gpu_arm(args, rank, world, local_rank):
     spmv_bytes = 76 * nnzb + 4 * (V + 1) + 48 * V
     # smoother sweep: FP32 block 36 B + column 4 B per nonzero block; x (gathered,
     # once), b, out 24 B/row each; FP32 3x3 block-Jacobi inverse 36 B/row
-    smooth_bytes = 40 * nnzb + 4 * (V + 1) + 108 * V
+    sbb = int(getattr(info, "smoother_bytes_per_block", 0) or 40)   # 26 with the FP16 operator copy
+    smooth_bytes = sbb * nnzb + 4 * (V + 1) + 108 * V
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -639,7 +640,7 @@ def gpu_arm(args, rank, world, local_rank):
     conv = [s_[0] for r in res for s_ in r[2]]
     return dict(ms=ms_max, launches=launches, clocks=clk.summary(), spmv_ms=spmv_ms, spmv_bytes=spmv_bytes, kt=kt,
                 achieved=achieved, hbm=hbm, traffic=traffic, e2e=e2e, setup_s=setup_s, R=R, elem=elem,
-                smooth_ms=smooth_ms, smooth_bytes=smooth_bytes, smooth_traffic=smooth_traffic,
+                smooth_ms=smooth_ms, smooth_bytes=smooth_bytes, smooth_traffic=smooth_traffic, sbb=sbb,
                 fp64_peak=float(peaks.get("fp64_tflops", FP64_PEAK_TFLOPS)),
                 nnzb=nnzb, V=V, E=E_, desc=cdef["desc"], newton=[s_[1] for s_ in stats],
                 krylov=[s_[2] for s_ in stats], contacts=[s_[3] for s_ in stats], converged=all(conv),
@@ -748,8 +749,9 @@ def _frac(bytes_, ms, peak):
 def roofline_smoother(r):
     """Dominant kernel of the step (launch-list share): the fine-level V-cycle
     sweep k_mg_smooth<float,1,*> on the FP32 SELL-32 operator copy.
-    Algorithmic bytes per launch: 36 B FP32 block + 4 B column
-    per nonzero block, slice table 4(V+1); per row the residual-form sweep
+    Algorithmic bytes per launch: per nonzero block the
+    operator copy's 18 B FP16 values + 4 B scale + 4 B column (26 B; 40 B
+    with the FP32 copy, DP_SMOOTH16=0), slice table 4(V+1); per row the residual-form sweep
     reads x (gathered, counted once) and b and writes r (72 B), the update
     form reads x, b, the FP32 block-Jacobi inverse (36 B) and agg (4 B) and
     writes z (112 B); a V-cycle runs one of each, so 92 B/row on average.
@@ -758,14 +760,16 @@ def roofline_smoother(r):
     repeated on cold operands, update form) is reported beside it."""
     nnzb, V, hbm = r["nnzb"], r["V"], r["hbm"]
     out = {"bound": "hbm", "unit": "GB/s", "peak": hbm,
-           "kernel": "k_mg_smooth<float,1> (fine-level V-cycle sweep, SELL-32 FP32 3x3 blocks, cp.async ring)",
+           "kernel": "k_mg_smooth16 / k_mg_smooth<float,1> (fine-level V-cycle sweep, SELL-32 FP16(+scale) or FP32 "
+                     "3x3 blocks, cp.async ring)",
            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
     kt = r.get("kt")
     if kt and kt["smooth_calls"]:
         ms = kt["smooth_ms"] / kt["smooth_calls"]
-        b = 40 * nnzb + 4 * (V + 1) + 92 * V
+        b = r["sbb"] * nnzb + 4 * (V + 1) + 92 * V
         ach, fr = _frac(b, ms, hbm)
         out.update(achieved=ach, frac=fr, ms_per_launch=ms, bytes_per_launch=b, launches=kt["smooth_calls"],
+                   bytes_per_block=r["sbb"],
                    timing="in situ: CUDA event pairs around every launch of one rollout of the timed workload",
                    traffic=r["smooth_traffic"])
     if r["smooth_ms"]:

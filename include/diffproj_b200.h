@@ -70,6 +70,9 @@ typedef struct {
   int64_t n_slots;               /* blocks incl. SELL-32 padding              */
   int64_t device_bytes;          /* bytes of device memory owned              */
   int32_t n_colliders, n_bindings;
+  int32_t smoother_bytes_per_block; /* fine-level V-cycle operator copy: 40 = FP32 values + column,
+                                       26 = FP16 values + per-block FP32 scale + column, 0 = none */
+  int32_t pad_;
 } dp_scene_info;
 
 /* ForwardConfig (forward.py:29-34) + Krylov controls of the inexact Newton. */

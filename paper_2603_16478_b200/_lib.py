@@ -48,7 +48,8 @@ class SceneInfo(C.Structure):
     _fields_ = [("n_verts", C.c_int32), ("n_elems", C.c_int32),
                 ("verts_per_elem", C.c_int32), ("nnzb", C.c_int64),
                 ("n_slots", C.c_int64), ("device_bytes", C.c_int64),
-                ("n_colliders", C.c_int32), ("n_bindings", C.c_int32)]
+                ("n_colliders", C.c_int32), ("n_bindings", C.c_int32),
+                ("smoother_bytes_per_block", C.c_int32), ("pad_", C.c_int32)]
 
 
 class ForwardCfg(C.Structure):

@@ -690,6 +690,8 @@ int dp_scene_get_info(const dp_scene* s, dp_scene_info* o) {
   o->device_bytes = (int64_t)s->bytes;
   o->n_colliders = s->colliders.n;
   o->n_bindings = s->nb;
+  o->smoother_bytes_per_block = s->val16 ? 26 : (s->val32 ? 40 : 0);
+  o->pad_ = 0;
   return DP_OK;
 }
 

@@ -209,6 +209,10 @@ struct dp_scene {
   int* epos = nullptr;             // E*NP: (element, a <= b) -> position in H (~pos: stored transposed)
   double* minv = nullptr;          // block-Jacobi inverses [9][V]
   float* val32 = nullptr;          // FP32 copy of the last assembled operator (multigrid fine level)
+  // FP16 copy for the fine-level smoother sweeps: component-major like val32,
+  // each slot's 9 values scaled by its block max |a| (sc16[slot], FP32)
+  unsigned short* val16 = nullptr;
+  float* sc16 = nullptr;
   const double* val32_src = nullptr;   // operator val32 was last written from
   float* minv32 = nullptr;         // FP32 block-Jacobi inverses (multigrid smoother)
 

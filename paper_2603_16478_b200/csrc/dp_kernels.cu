@@ -14,6 +14,7 @@
 // Assembly is a deterministic stream (no atomics): every canonical SELL slot
 // (row <= col) owns a contiguous run of H in element order, and slot (j, i)
 // reads the run of (i, j) transposed.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <algorithm>
@@ -696,7 +697,8 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
                                                   const int* __restrict__ c_off, const double* __restrict__ c_blk,
                                                   int use_extras, double h2, double* __restrict__ val,
                                                   double* __restrict__ minv, float* __restrict__ val32,
-                                                  float* __restrict__ minv32) {
+                                                  float* __restrict__ minv32, unsigned short* __restrict__ val16,
+                                                  float* __restrict__ sc16) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= S) return;
@@ -785,6 +787,18 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
       for (int c = 0; c < 9; ++c) v32[(k * 9 + c) * kSlice + lane] = (float)b[c];
 #endif
     }
+    if (val16) {
+      // FP16 copy for the fine smoother: values / block max |a| (in [-1, 1])
+      double mx = 0.0;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) mx = fmax(mx, fabs(b[c]));
+      const float scf = mx > 0.0 ? (float)mx : 1.0f;
+      sc16[slot] = scf;
+      unsigned short* v16 = val16 + (size_t)base * 9;
+#pragma unroll
+      for (int c = 0; c < 9; ++c)
+        v16[(k * 9 + c) * kSlice + lane] = __half_as_ushort(__float2half_rn((float)(b[c] / (double)scf)));
+    }
   }
 }
 
@@ -798,7 +812,8 @@ void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat)
                                        s->H, s->Ht, s->mass, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_comp,
                                        has_c ? s->c_count : nullptr, s->c_off, s->c_blk, amat ? 0 : 1,
                                        s->h * s->h, val, s->minv, amat ? nullptr : s->val32,
-                                       amat ? nullptr : s->minv32);
+                                       amat ? nullptr : s->minv32, amat ? nullptr : s->val16,
+                                       amat ? nullptr : s->sc16);
   ktm_end(s, KT_ASSEMBLE);
   if (!amat && s->val32) s->val32_src = val;   // the FP32 copy now mirrors `val`
   s->launches++;

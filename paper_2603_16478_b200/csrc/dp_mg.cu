@@ -15,6 +15,7 @@
 //  * apply (V-cycle): damped block-Jacobi pre/post smoothing, residual,
 //    restriction (member gather), prolongation fused into the post-smoother's
 //    SpMV gathers.  Symmetric for symmetric A (CG-safe).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -55,6 +56,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 namespace dp {
 
+// fine-level smoother sweeps on an FP16 operator copy with per-block scales
+// (26 instead of 40 bytes per block; the preconditioner only)
+static const int g_smooth16 = getenv("DP_SMOOTH16") ? atoi(getenv("DP_SMOOTH16")) : 0;   // measured: no faster (latency-bound), off
 static const int g_mg_tail = getenv("DP_MG_TAIL") ? atoi(getenv("DP_MG_TAIL")) : 0;   // measured slower (39 us vs 23 us), off
 constexpr int kCoarseMax = 36;      // dense coarsest solve (<= 108 unknowns, shared memory)
 constexpr int kDenseSmem = 108;
@@ -210,6 +214,10 @@ int mg_setup(dp_scene* s) {
   // the FP64 operator, so the solution accuracy is unaffected
   rc |= al(mg, &s->val32, (size_t)s->NS * kVal32PerSlot);
   rc |= al(mg, &s->minv32, (size_t)s->V * 9);
+  if (g_smooth16 && s->S >= 4 * 148 && DP_VAL32_PACKED == 0) {
+    rc |= al(mg, &s->val16, (size_t)s->NS * 9);
+    rc |= al(mg, &s->sc16, (size_t)s->NS);
+  }
   rc |= al(mg, &L0.x, (size_t)3 * s->V);
   rc |= al(mg, &L0.r, (size_t)3 * s->V);
   rc |= al(mg, &L0.t, (size_t)3 * s->V);
@@ -332,6 +340,10 @@ int mg_setup(dp_scene* s) {
   if (mg->lv.size() < 2 || mg->N > kDenseSmem) {
     // no useful hierarchy (tiny or unaggregatable graph): disable
     if (s->val32) { cudaFree(s->val32); s->val32 = nullptr; }
+  if (s->val16) { cudaFree(s->val16); s->val16 = nullptr; }
+  if (s->sc16) { cudaFree(s->sc16); s->sc16 = nullptr; }
+    if (s->val16) { cudaFree(s->val16); s->val16 = nullptr; }
+    if (s->sc16) { cudaFree(s->sc16); s->sc16 = nullptr; }
     if (s->minv32) { cudaFree(s->minv32); s->minv32 = nullptr; }
     delete mg;
     s->mg = nullptr;
@@ -358,6 +370,8 @@ void mg_destroy(dp_scene* s) {
   MG* mg = s->mg;
   if (!mg) return;
   if (s->val32) { cudaFree(s->val32); s->val32 = nullptr; }
+  if (s->val16) { cudaFree(s->val16); s->val16 = nullptr; }
+  if (s->sc16) { cudaFree(s->sc16); s->sc16 = nullptr; }
   if (s->minv32) { cudaFree(s->minv32); s->minv32 = nullptr; }
   for (size_t l = 0; l < mg->lv.size(); ++l) {
     MGLevel& L = mg->lv[l];
@@ -667,6 +681,227 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
     }
   }
 }
+
+
+// Fine-level sweep on the FP16 operator copy (values scaled per block by
+// sc16, dequantised to FP64 in registers): the same arithmetic as the FP32
+// sweep otherwise, slots streamed through the per-warp cp.async ring
+// (576 B values + 128 B scales + 128 B columns per slot).
+template <bool DOT>
+__global__ void __launch_bounds__(DP_SMOOTH_NT) k_mg_smooth16(int n, int S, const int* __restrict__ slice_base,
+                                                            const int* __restrict__ slice_width,
+                                                            const int* __restrict__ col,
+                                                            const unsigned short* __restrict__ val16,
+                                                            const float* __restrict__ sc16,
+                                                            const float* __restrict__ minv, const double* __restrict__ b,
+                                                            const double* __restrict__ x,
+                                                            const double* __restrict__ xc,
+                                                            const int* __restrict__ agg, double omega,
+                                                            double* __restrict__ out, double* __restrict__ r_out,
+                                                            const int* stop, double alpha, double* dot_partial,
+                                                            unsigned int* dot_counter, KrylovScalars* dot_ks) {
+  __shared__ __align__(16) unsigned short sv[DP_SMOOTH_NT / 32][kSmDepth][9 * kSlice];
+  __shared__ __align__(16) float ss[DP_SMOOTH_NT / 32][kSmDepth][kSlice];
+  __shared__ __align__(16) int sc[DP_SMOOTH_NT / 32][kSmDepth][kSlice];
+  if (stopped(stop)) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double rz = 0.0;
+  if (gw < S) {
+    const int row = gw * kSlice + lane;
+    const int base = slice_base[gw], K = slice_width[gw];
+    const unsigned short* gv = val16 + (size_t)base * 9;
+    const float* gs = sc16 + base;
+    const int* gc = col + base;
+    auto issue = [&](int kk) {
+      if (kk < K) {
+        const unsigned short* src = gv + (size_t)kk * 9 * kSlice;   // 576 B = 36 x 16 B
+        unsigned short* dst = sv[w][kk % kSmDepth];
+        for (int ch = lane; ch < 36; ch += 32) cp_async16(dst + 8 * ch, src + 8 * ch);
+        if (lane < 8) cp_async16(&ss[w][kk % kSmDepth][4 * lane], gs + kk * kSlice + 4 * lane);
+        else if (lane < 16) cp_async16(&sc[w][kk % kSmDepth][4 * (lane - 8)], gc + kk * kSlice + 4 * (lane - 8));
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int kk = 0; kk < kSmDepth; ++kk) issue(kk);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int k = 0; k < K; ++k) {
+      cp_async_wait<kSmDepth - 1>();
+      __syncwarp();
+      const unsigned short* vv = sv[w][k % kSmDepth];
+      const double scl = (double)ss[w][k % kSmDepth][lane];
+      const int j = sc[w][k % kSmDepth][lane];
+      double m[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) m[c] = (double)__half2float(__ushort_as_half(vv[c * kSlice + lane])) * scl;
+      double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
+      if (xc) {
+        const int J = __ldg(agg + j);
+        x0 += alpha * __ldg(xc + 3 * J); x1 += alpha * __ldg(xc + 3 * J + 1); x2 += alpha * __ldg(xc + 3 * J + 2);
+      }
+      a0 += m[0] * x0 + m[1] * x1 + m[2] * x2;
+      a1 += m[3] * x0 + m[4] * x1 + m[5] * x2;
+      a2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
+      __syncwarp();
+      issue(k + kSmDepth);
+    }
+    cp_async_wait<0>();
+    if (row < n) {
+      double xt[3] = {x[3 * row], x[3 * row + 1], x[3 * row + 2]};
+      if (xc) {
+        const int I = agg[row];
+        xt[0] += alpha * xc[3 * I]; xt[1] += alpha * xc[3 * I + 1]; xt[2] += alpha * xc[3 * I + 2];
+      }
+      const double bb[3] = {b[3 * row], b[3 * row + 1], b[3 * row + 2]};
+      const double rr[3] = {bb[0] - a0, bb[1] - a1, bb[2] - a2};
+      if (r_out) { r_out[3 * row] = rr[0]; r_out[3 * row + 1] = rr[1]; r_out[3 * row + 2] = rr[2]; }
+      if (out) {
+        double u[3];
+        mv_minv(minv, n, row, rr, u);
+        const double z0 = xt[0] + omega * u[0], z1 = xt[1] + omega * u[1], z2 = xt[2] + omega * u[2];
+        out[3 * row] = z0;
+        out[3 * row + 1] = z1;
+        out[3 * row + 2] = z2;
+        if (DOT) rz = bb[0] * z0 + bb[1] * z1 + bb[2] * z2;
+      }
+    }
+  }
+  if constexpr (DOT) {
+    __shared__ double sh[32];
+    __shared__ double o1[1];
+    const double t = block_sum<DP_SMOOTH_NT>(rz, sh);
+    if (threadIdx.x == 0) dot_partial[blockIdx.x] = t;
+    if (last_block(dot_counter)) {
+      fold_partials<DP_SMOOTH_NT, 1>(dot_partial, gridDim.x, o1, sh);
+      if (threadIdx.x == 0) {
+        const double g = o1[0];
+        dot_ks->beta = (dot_ks->iters == 0) ? 0.0 : g / dot_ks->gamma;
+        dot_ks->gamma = g;
+        if (!(g > 0.0)) dot_ks->done = 2;
+        *dot_counter = 0;
+      }
+    }
+  }
+}
+
+
+// Fine-level FP32 sweep with the x gathers software-pipelined one slot ahead:
+// a 3-deep cp.async ring; while slot k is accumulated, slot k+1's column
+// indices (already in shared memory) feed the gathers of its x values, so
+// the dependent x-gather latency of a slot overlaps the previous slot's
+// arithmetic and ring wait instead of following it (the sweep is bound by
+// that per-warp latency chain, not by bytes: the FP16 copy measured no
+// faster).  Same values and accumulation order as k_mg_smooth<float,1>.
+constexpr int kPfDepth = 3;
+template <bool DOT>
+__global__ void __launch_bounds__(DP_SMOOTH_NT) k_mg_smooth_pf(int n, int S, const int* __restrict__ slice_base,
+                                                             const int* __restrict__ slice_width,
+                                                             const int* __restrict__ col, const float* __restrict__ val,
+                                                             const float* __restrict__ minv,
+                                                             const double* __restrict__ b,
+                                                             const double* __restrict__ x,
+                                                             const double* __restrict__ xc,
+                                                             const int* __restrict__ agg, double omega,
+                                                             double* __restrict__ out, double* __restrict__ r_out,
+                                                             const int* stop, double alpha, double* dot_partial,
+                                                             unsigned int* dot_counter, KrylovScalars* dot_ks) {
+  __shared__ __align__(16) float sv[DP_SMOOTH_NT / 32][kPfDepth][9 * kSlice];
+  __shared__ __align__(16) int sc[DP_SMOOTH_NT / 32][kPfDepth][kSlice];
+  if (stopped(stop)) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double rz = 0.0;
+  if (gw < S) {
+    const int row = gw * kSlice + lane;
+    const int base = slice_base[gw], K = slice_width[gw];
+    const float* gv = val + (size_t)base * 9;
+    const int* gc = col + base;
+    auto issue = [&](int kk) {
+      if (kk < K) {
+        const float* src = gv + (size_t)kk * 9 * kSlice;
+        float* dst = sv[w][kk % kPfDepth];
+        for (int ch = lane; ch < 9 * kSlice / 4; ch += 32) cp_async16(dst + 4 * ch, src + 4 * ch);
+        if (lane < kSlice / 4) cp_async16(&sc[w][kk % kPfDepth][4 * lane], gc + kk * kSlice + 4 * lane);
+      }
+      cp_async_commit();
+    };
+    auto gather = [&](int kk, double xo[3]) {
+      const int j = sc[w][kk % kPfDepth][lane];
+      xo[0] = __ldg(x + 3 * j); xo[1] = __ldg(x + 3 * j + 1); xo[2] = __ldg(x + 3 * j + 2);
+      if (xc) {
+        const int J = __ldg(agg + j);
+        xo[0] += alpha * __ldg(xc + 3 * J); xo[1] += alpha * __ldg(xc + 3 * J + 1);
+        xo[2] += alpha * __ldg(xc + 3 * J + 2);
+      }
+    };
+#pragma unroll
+    for (int kk = 0; kk < kPfDepth; ++kk) issue(kk);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    double xcur[3] = {0.0, 0.0, 0.0};
+    if (K > 0) {
+      cp_async_wait<kPfDepth - 1>();   // slot 0 landed
+      __syncwarp();
+      gather(0, xcur);
+    }
+    for (int k = 0; k < K; ++k) {
+      double xnext[3] = {0.0, 0.0, 0.0};
+      if (k + 1 < K) {
+        cp_async_wait<kPfDepth - 2>();   // slot k+1 landed
+        __syncwarp();
+        gather(k + 1, xnext);
+      }
+      const float* vv = sv[w][k % kPfDepth];
+      double m[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) m[c] = (double)vv[c * kSlice + lane];
+      a0 += m[0] * xcur[0] + m[1] * xcur[1] + m[2] * xcur[2];
+      a1 += m[3] * xcur[0] + m[4] * xcur[1] + m[5] * xcur[2];
+      a2 += m[6] * xcur[0] + m[7] * xcur[1] + m[8] * xcur[2];
+      __syncwarp();
+      issue(k + kPfDepth);   // reuses slot k's buffer (its columns and values are consumed)
+      xcur[0] = xnext[0]; xcur[1] = xnext[1]; xcur[2] = xnext[2];
+    }
+    cp_async_wait<0>();
+    if (row < n) {
+      double xt[3] = {x[3 * row], x[3 * row + 1], x[3 * row + 2]};
+      if (xc) {
+        const int I = agg[row];
+        xt[0] += alpha * xc[3 * I]; xt[1] += alpha * xc[3 * I + 1]; xt[2] += alpha * xc[3 * I + 2];
+      }
+      const double bb[3] = {b[3 * row], b[3 * row + 1], b[3 * row + 2]};
+      const double rr[3] = {bb[0] - a0, bb[1] - a1, bb[2] - a2};
+      if (r_out) { r_out[3 * row] = rr[0]; r_out[3 * row + 1] = rr[1]; r_out[3 * row + 2] = rr[2]; }
+      if (out) {
+        double u[3];
+        mv_minv(minv, n, row, rr, u);
+        const double z0 = xt[0] + omega * u[0], z1 = xt[1] + omega * u[1], z2 = xt[2] + omega * u[2];
+        out[3 * row] = z0;
+        out[3 * row + 1] = z1;
+        out[3 * row + 2] = z2;
+        if (DOT) rz = bb[0] * z0 + bb[1] * z1 + bb[2] * z2;
+      }
+    }
+  }
+  if constexpr (DOT) {
+    __shared__ double sh[32];
+    __shared__ double o1[1];
+    const double t = block_sum<DP_SMOOTH_NT>(rz, sh);
+    if (threadIdx.x == 0) dot_partial[blockIdx.x] = t;
+    if (last_block(dot_counter)) {
+      fold_partials<DP_SMOOTH_NT, 1>(dot_partial, gridDim.x, o1, sh);
+      if (threadIdx.x == 0) {
+        const double g = o1[0];
+        dot_ks->beta = (dot_ks->iters == 0) ? 0.0 : g / dot_ks->gamma;
+        dot_ks->gamma = g;
+        if (!(g > 0.0)) dot_ks->done = 2;
+        *dot_counter = 0;
+      }
+    }
+  }
+}
+
+static const int g_smooth_pf = getenv("DP_SMOOTH_PF") ? atoi(getenv("DP_SMOOTH_PF")) : 0;   // measured slower (25.6 vs 24.1 us in situ), off
 
 // x = xa + alpha P xc
 __global__ void k_mg_prolong(int n, const double* __restrict__ xa, const double* __restrict__ xc,
@@ -1155,6 +1390,37 @@ static void smooth(dp_scene* s, const MGLevel& L, const TV* val, const TV* minv,
   }
   const bool fine = (&L == &mg->lv[0]);
   if (fine) ktm_begin(s, KT_SMOOTH);
+  if constexpr (sizeof(TV) == 4) {
+    if (fine && g_smooth_pf && !s->val16 && L.S >= 4 * 148 && DP_VAL32_PACKED == 0) {
+      const int nb = grid_for((int64_t)L.S * 32, DP_SMOOTH_NT);
+      if (dot && mg->dot_ks && out)
+        k_mg_smooth_pf<true><<<nb, DP_SMOOTH_NT, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val,
+                                                                 minv, b, x, xc, agg, omega, out, r_out, stop, alpha,
+                                                                 mg->dot_partial, mg->dot_counter, mg->dot_ks);
+      else
+        k_mg_smooth_pf<false><<<nb, DP_SMOOTH_NT, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val,
+                                                                  minv, b, x, xc, agg, omega, out, r_out, stop, alpha,
+                                                                  nullptr, nullptr, nullptr);
+      ktm_end(s, KT_SMOOTH);
+      s->launches++;
+      return;
+    }
+    if (fine && s->val16 && L.S >= 4 * 148) {
+      const int nb = grid_for((int64_t)L.S * 32, DP_SMOOTH_NT);
+      if (dot && mg->dot_ks && out)
+        k_mg_smooth16<true><<<nb, DP_SMOOTH_NT, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col,
+                                                                s->val16, s->sc16, minv, b, x, xc, agg, omega, out,
+                                                                r_out, stop, alpha, mg->dot_partial, mg->dot_counter,
+                                                                mg->dot_ks);
+      else
+        k_mg_smooth16<false><<<nb, DP_SMOOTH_NT, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col,
+                                                                 s->val16, s->sc16, minv, b, x, xc, agg, omega, out,
+                                                                 r_out, stop, alpha, nullptr, nullptr, nullptr);
+      ktm_end(s, KT_SMOOTH);
+      s->launches++;
+      return;
+    }
+  }
   if (dot && mg->dot_ks && out && L.S >= 4 * 148)
     k_mg_smooth<TV, 1, true><<<grid_for((int64_t)L.S * 32, DP_SMOOTH_NT), DP_SMOOTH_NT, 0, s->stream>>>(
         L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x, xc, agg, omega, out, r_out, stop, alpha,

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -202,6 +203,49 @@ static int raise_status(int st) {
     return DP_ERR_PENETRATION;
   }
   return DP_OK;
+}
+
+// Thread-local device scratch arena for the unit-level batch entry points
+// (dp_project_batch, dp_contact_batch, dp_cache_get_projections): grown on
+// demand and reused, so repeated calls (e.g. a report's contacts read every
+// step) do not pay cudaMalloc/cudaFree each time.
+struct ScratchArena {
+  int dev = -1;
+  char* base = nullptr;
+  size_t cap = 0, used = 0;
+  ~ScratchArena() {
+    if (base) cudaFree(base);
+  }
+};
+static thread_local ScratchArena g_scratch;
+
+static int scratch_reserve(size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (g_scratch.dev != dev || bytes > g_scratch.cap) {
+    if (g_scratch.base && g_scratch.dev == dev) cudaFree(g_scratch.base);
+    g_scratch.base = nullptr;
+    g_scratch.cap = 0;
+    const size_t cap = bytes + bytes / 2 + 4096;
+    if (cudaMalloc((void**)&g_scratch.base, cap) != cudaSuccess) return DP_ERR_CUDA;
+    g_scratch.cap = cap;
+    g_scratch.dev = dev;
+  }
+  g_scratch.used = 0;
+  return 0;
+}
+
+template <class T>
+static T* scratch_take(size_t n) {
+  const size_t off = (g_scratch.used + 255) & ~(size_t)255;
+  g_scratch.used = off + n * sizeof(T);
+  return reinterpret_cast<T*>(g_scratch.base + off);
+}
+
+static size_t scratch_bytes(std::initializer_list<size_t> sizes) {
+  size_t t = 0;
+  for (size_t b : sizes) t += ((b + 255) & ~(size_t)255);
+  return t;
 }
 
 }  // namespace dp
@@ -1329,18 +1373,21 @@ int dp_cache_get_projections(dp_scene* s, const dp_cache* c, double* sigma, doub
   cudaSetDevice(s->device);
   const int E = s->E, D = s->D;
   if (!E) return DP_OK;
-  double *ds, *dt, *dP, *de;
-  DP_CUDA(cudaMalloc(&ds, sizeof(double) * E * D));
-  DP_CUDA(cudaMalloc(&dt, sizeof(double) * E * D));
-  DP_CUDA(cudaMalloc(&dP, sizeof(double) * E * 3 * D));
-  DP_CUDA(cudaMalloc(&de, sizeof(double) * E));
+  const size_t ED = (size_t)E * D;
+  if (scratch_reserve(scratch_bytes({ED * 8, ED * 8, ED * 3 * 8, (size_t)E * 8}))) {
+    set_error("device scratch allocation failed");
+    return DP_ERR_CUDA;
+  }
+  double* ds = scratch_take<double>(ED);
+  double* dt = scratch_take<double>(ED);
+  double* dP = scratch_take<double>(ED * 3);
+  double* de = scratch_take<double>(E);
   launch_export_proj(s, c->q_eval, ds, dt, dP, de);
   cudaStreamSynchronize(s->stream);
   if (sigma) cudaMemcpy(sigma, ds, sizeof(double) * E * D, cudaMemcpyDeviceToHost);
   if (theta) cudaMemcpy(theta, dt, sizeof(double) * E * D, cudaMemcpyDeviceToHost);
   if (P) cudaMemcpy(P, dP, sizeof(double) * E * 3 * D, cudaMemcpyDeviceToHost);
   if (energy) cudaMemcpy(energy, de, sizeof(double) * E, cudaMemcpyDeviceToHost);
-  cudaFree(ds); cudaFree(dt); cudaFree(dP); cudaFree(de);
   return DP_OK;
 }
 
@@ -1553,20 +1600,23 @@ int dp_project_batch(int32_t n, int32_t d, const double* F, const int32_t* model
     return DP_ERR_NO_DEVICE;
   }
   const size_t N = n, F_ = 3 * d, J_ = (size_t)(3 * d) * (3 * d);
-  double *dF, *dmu, *dlam, *ds, *dt, *dW, *dP, *dJ, *dPm, *dPl;
-  int *dmod, *dst;
-  DP_CUDA(cudaMalloc(&dF, N * F_ * 8));
-  DP_CUDA(cudaMalloc(&dmu, N * 8));
-  DP_CUDA(cudaMalloc(&dlam, N * 8));
-  DP_CUDA(cudaMalloc(&dmod, N * 4));
-  DP_CUDA(cudaMalloc(&dst, N * 4));
-  DP_CUDA(cudaMalloc(&ds, N * d * 8));
-  DP_CUDA(cudaMalloc(&dt, N * d * 8));
-  DP_CUDA(cudaMalloc(&dW, N * d * d * 8));
-  DP_CUDA(cudaMalloc(&dP, N * F_ * 8));
-  DP_CUDA(cudaMalloc(&dJ, N * J_ * 8));
-  DP_CUDA(cudaMalloc(&dPm, N * F_ * 8));
-  DP_CUDA(cudaMalloc(&dPl, N * F_ * 8));
+  if (scratch_reserve(scratch_bytes({N * F_ * 8, N * 8, N * 8, N * 4, N * 4, N * d * 8, N * d * 8, N * d * d * 8,
+                                     N * F_ * 8, N * J_ * 8, N * F_ * 8, N * F_ * 8}))) {
+    set_error("device scratch allocation failed");
+    return DP_ERR_CUDA;
+  }
+  double* dF = scratch_take<double>(N * F_);
+  double* dmu = scratch_take<double>(N);
+  double* dlam = scratch_take<double>(N);
+  int* dmod = scratch_take<int>(N);
+  int* dst = scratch_take<int>(N);
+  double* ds = scratch_take<double>(N * d);
+  double* dt = scratch_take<double>(N * d);
+  double* dW = scratch_take<double>(N * d * d);
+  double* dP = scratch_take<double>(N * F_);
+  double* dJ = scratch_take<double>(N * J_);
+  double* dPm = scratch_take<double>(N * F_);
+  double* dPl = scratch_take<double>(N * F_);
   cudaMemcpy(dF, F, N * F_ * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dmu, mu, N * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dlam, lam, N * 8, cudaMemcpyHostToDevice);
@@ -1590,8 +1640,6 @@ int dp_project_batch(int32_t n, int32_t d, const double* F, const int32_t* model
     if (dP_dlam) cudaMemcpy(dP_dlam, dPl, N * F_ * 8, cudaMemcpyDeviceToHost);
     if (status) cudaMemcpy(status, dst, N * 4, cudaMemcpyDeviceToHost);
   }
-  void* p[] = {dF, dmu, dlam, dmod, dst, ds, dt, dW, dP, dJ, dPm, dPl};
-  for (void* x : p) cudaFree(x);
   if (e != cudaSuccess) return cuda_fail(e, "project batch");
   return DP_OK;
 }
@@ -1601,22 +1649,25 @@ int dp_contact_batch(int32_t n, const double* frame, const double* d_n, const do
                      int32_t* capped, double* Kc, double* k_mu, double* residual, int32_t* status) {
   if (n <= 0) return DP_OK;
   const size_t N = n;
-  double *df, *ddn, *dmu, *deps, *dx, *dxb, *dl, *dd, *dsg, *dK, *dkm, *dres;
-  int *dcp, *dst;
-  DP_CUDA(cudaMalloc(&df, N * 72));
-  DP_CUDA(cudaMalloc(&ddn, N * 8));
-  DP_CUDA(cudaMalloc(&dmu, N * 8));
-  DP_CUDA(cudaMalloc(&deps, N * 8));
-  DP_CUDA(cudaMalloc(&dx, N * 24));
-  DP_CUDA(cudaMalloc(&dxb, N * 24));
-  DP_CUDA(cudaMalloc(&dl, N * 24));
-  DP_CUDA(cudaMalloc(&dd, N * 24));
-  DP_CUDA(cudaMalloc(&dsg, N * 8));
-  DP_CUDA(cudaMalloc(&dK, N * 72));
-  DP_CUDA(cudaMalloc(&dkm, N * 24));
-  DP_CUDA(cudaMalloc(&dres, N * 24));
-  DP_CUDA(cudaMalloc(&dcp, N * 4));
-  DP_CUDA(cudaMalloc(&dst, N * 4));
+  if (scratch_reserve(scratch_bytes({N * 72, N * 8, N * 8, N * 8, N * 24, N * 24, N * 24, N * 24, N * 8, N * 72,
+                                     N * 24, N * 24, N * 4, N * 4}))) {
+    set_error("device scratch allocation failed");
+    return DP_ERR_CUDA;
+  }
+  double* df = scratch_take<double>(N * 9);
+  double* ddn = scratch_take<double>(N);
+  double* dmu = scratch_take<double>(N);
+  double* deps = scratch_take<double>(N);
+  double* dx = scratch_take<double>(N * 3);
+  double* dxb = scratch_take<double>(N * 3);
+  double* dl = scratch_take<double>(N * 3);
+  double* dd = scratch_take<double>(N * 3);
+  double* dsg = scratch_take<double>(N);
+  double* dK = scratch_take<double>(N * 9);
+  double* dkm = scratch_take<double>(N * 3);
+  double* dres = scratch_take<double>(N * 3);
+  int* dcp = scratch_take<int>(N);
+  int* dst = scratch_take<int>(N);
   cudaMemcpy(df, frame, N * 72, cudaMemcpyHostToDevice);
   cudaMemcpy(ddn, d_n, N * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dmu, mu, N * 8, cudaMemcpyHostToDevice);
@@ -1641,8 +1692,6 @@ int dp_contact_batch(int32_t n, const double* frame, const double* d_n, const do
     if (residual) cudaMemcpy(residual, dres, N * 24, cudaMemcpyDeviceToHost);
     if (status) cudaMemcpy(status, dst, N * 4, cudaMemcpyDeviceToHost);
   }
-  void* p[] = {df, ddn, dmu, deps, dx, dxb, dl, dd, dsg, dK, dkm, dres, dcp, dst};
-  for (void* xx : p) cudaFree(xx);
   if (e != cudaSuccess) return cuda_fail(e, "contact batch");
   return DP_OK;
 }

@@ -5,7 +5,6 @@
 // reference runs on), everything else rounds per
 // operation like the reference's scalar Python/numpy expressions, so contact
 // sets are bit-exact (detect_contacts, contact.py:115-136).
-#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include "dp_common.cuh"
@@ -355,11 +354,71 @@ void launch_penetration(dp_scene* s, const double* q, EvalScalars* esc) {
 
 // ---------------------------------------------------------------------------
 // detection: count -> exclusive scan -> write (order: vertex, then collider)
-__global__ void k_detect_count(int V, const ColliderSet* __restrict__ csp, const double* __restrict__ q, double act,
-                               int* __restrict__ count, SelfContact sc) {
+// count + the block-local exclusive scan of the counts (the grid-level
+// offsets come from k_scan_blocks; no library scan on the detection path)
+constexpr int kDetNT = 256;
+__device__ int detect_count_one(const ColliderSet* __restrict__ csp, const double* __restrict__ q, double act,
+                                const SelfContact& sc, int v);
+__global__ void __launch_bounds__(kDetNT) k_detect_count(int V, const ColliderSet* __restrict__ csp,
+                                                         const double* __restrict__ q, double act,
+                                                         int* __restrict__ count, int* __restrict__ local_off,
+                                                         int* __restrict__ blk_sum, SelfContact sc) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v > V) return;
-  if (v == V) { count[V] = 0; return; }
+  int c = 0;
+  if (v < V) c = detect_count_one(csp, q, act, sc, v);
+  if (v <= V) count[v] = (v < V) ? c : 0;
+  // block exclusive scan (warp shuffles + one smem pass)
+  __shared__ int ws[kDetNT / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) ws[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int t = (lane < kDetNT / 32) ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < kDetNT / 32) ws[lane] = t;   // inclusive over warps
+  }
+  __syncthreads();
+  const int wpre = (wid > 0) ? ws[wid - 1] : 0;
+  if (v <= V) local_off[v] = wpre + incl - c;
+  if (threadIdx.x == kDetNT - 1) blk_sum[blockIdx.x] = ws[kDetNT / 32 - 1];
+}
+
+// exclusive scan of the per-block totals in one CTA; total -> esc->n_contacts
+__global__ void __launch_bounds__(1024) k_scan_blocks(int nb, int* __restrict__ blk, EvalScalars* esc) {
+  __shared__ int part[1024];
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int per = (nb + nt - 1) / nt, lo = t * per, hi = min(nb, lo + per);
+  int sum = 0;
+  for (int i = lo; i < hi; ++i) sum += blk[i];
+  part[t] = sum;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {
+    const int y = (t >= off) ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += y;
+    __syncthreads();
+  }
+  int run = part[t] - sum;
+  for (int i = lo; i < hi; ++i) {
+    const int c = blk[i];
+    blk[i] = run;
+    run += c;
+  }
+  if (t == nt - 1) esc->n_contacts = part[nt - 1];
+}
+
+__device__ int detect_count_one(const ColliderSet* __restrict__ csp, const double* __restrict__ q, double act,
+                                const SelfContact& sc, int v) {
   const ColliderSet& cs = *csp;
   const double x[3] = {q[3 * v], q[3 * v + 1], q[3 * v + 2]};
   int c = 0;
@@ -371,18 +430,19 @@ __global__ void k_detect_count(int V, const ColliderSet* __restrict__ csp, const
     double n[3];
     if (!(self_gap(sc, v, x, n) > act)) ++c;
   }
-  count[v] = c;
+  return c;
 }
 
 __global__ void k_detect_write(int V, const ColliderSet* __restrict__ csp, const double* __restrict__ q, double act,
-                               const int* __restrict__ off, int* __restrict__ cvtx, int* __restrict__ ccol,
+                               int* __restrict__ off, const int* __restrict__ count,
+                               const int* __restrict__ blk_off, int* __restrict__ cvtx, int* __restrict__ ccol,
                                double* __restrict__ cframe, double* __restrict__ cdn, double* __restrict__ cmu,
                                EvalScalars* esc, SelfContact sc) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v == 0) esc->n_contacts = off[V];
-  if (v >= V) return;
-  int o = off[v];
-  if (off[v + 1] == o) return;
+  if (v > V) return;
+  int o = off[v] + blk_off[v / kDetNT];   // block-local exclusive offset + the block's offset
+  off[v] = o;
+  if (v == V || count[v] == 0) return;
   const ColliderSet& cs = *csp;
   const double x[3] = {q[3 * v], q[3 * v + 1], q[3 * v + 2]};
   for (int j = 0; j < cs.n; ++j) {
@@ -418,8 +478,8 @@ __global__ void k_detect_write(int V, const ColliderSet* __restrict__ csp, const
 }
 
 int contact_scan_setup(dp_scene* s) {
-  size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, s->c_count, s->c_off, s->V + 1, s->stream);
+  // per-block totals of the detection scan (one int per kDetNT vertices)
+  const size_t bytes = sizeof(int) * ((size_t)(s->V + 1 + kDetNT - 1) / kDetNT + 1);
   if (bytes > s->scan_tmp_bytes) {
     if (s->scan_tmp) cudaFree(s->scan_tmp);
     DP_CUDA(cudaMalloc(&s->scan_tmp, bytes));
@@ -434,12 +494,12 @@ void launch_detect(dp_scene* s, const double* q) {
     cudaMemsetAsync(&s->esc->n_contacts, 0, sizeof(int), s->stream);
     return;
   }
-  k_detect_count<<<grid_for(V + 1, 256), 256, 0, s->stream>>>(V, s->d_colliders, q, s->act, s->c_count, s->self);
-  size_t bytes = s->scan_tmp_bytes;
-  cub::DeviceScan::ExclusiveSum(s->scan_tmp, bytes, s->c_count, s->c_off, V + 1, s->stream);
-  k_detect_write<<<grid_for(V, 256), 256, 0, s->stream>>>(V, s->d_colliders, q, s->act, s->c_off, s->c_vertex,
-                                                          s->c_collider, s->c_frame, s->c_dn, s->c_mu, s->esc,
-                                                          s->self);
+  const int nb = grid_for(V + 1, kDetNT);
+  int* blk = static_cast<int*>(s->scan_tmp);
+  k_detect_count<<<nb, kDetNT, 0, s->stream>>>(V, s->d_colliders, q, s->act, s->c_count, s->c_off, blk, s->self);
+  k_scan_blocks<<<1, 1024, 0, s->stream>>>(nb, blk, s->esc);
+  k_detect_write<<<nb, kDetNT, 0, s->stream>>>(V, s->d_colliders, q, s->act, s->c_off, s->c_count, blk, s->c_vertex,
+                                               s->c_collider, s->c_frame, s->c_dn, s->c_mu, s->esc, s->self);
   s->launches += 3;
 }
 

@@ -1449,6 +1449,9 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
     s->mg_adj_ready = 1;
   }
   if (method == DP_SOLVER_CG) {
+    // (a warm start from the previous adjoint solution, as the GMRES branch
+    // does, saves 1.6% of the iterations but costs more than that in the
+    // extra residual SpMV and sync: measured slower, not used)
     if (mg) rc = pcg_mg_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, &iters, &relres, &brk, 0);
     else rc = cg_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, &iters, &relres, &brk);
     if (brk) {

@@ -60,6 +60,7 @@ namespace dp {
 // (26 instead of 40 bytes per block; the preconditioner only)
 static const int g_smooth16 = getenv("DP_SMOOTH16") ? atoi(getenv("DP_SMOOTH16")) : 0;   // measured: no faster (latency-bound), off
 static const int g_mg_tail = getenv("DP_MG_TAIL") ? atoi(getenv("DP_MG_TAIL")) : 0;   // measured slower (39 us vs 23 us), off
+static const int g_mg_agg2 = getenv("DP_MG_AGG2") ? atoi(getenv("DP_MG_AGG2")) : 0;
 constexpr int kCoarseMax = 36;      // dense coarsest solve (<= 108 unknowns, shared memory)
 constexpr int kDenseSmem = 108;
 __global__ void k_mg_dense_invert(int N, const double* __restrict__ Ag, double* __restrict__ Ainv);
@@ -241,9 +242,34 @@ int mg_setup(dp_scene* s) {
     cur_addr[k] = DP_VAL32_PACKED == 2 ? s->h_block_slot[k] * 8
                   : DP_VAL32_PACKED   ? s->h_block_slot[k] * 12
                                       : fine_addr[k];
+  int lev = 0;
   while (cur.n > kCoarseMax && !rc) {
     std::vector<int> agg;
-    const int na = aggregate(cur, agg);
+    int na = aggregate(cur, agg);
+    if (g_mg_agg2 && lev >= 1 && na > kCoarseMax) {
+      // coarse levels: aggregate the aggregates once more (fewer, larger
+      // coarse levels -> a shorter latency-bound coarse chain per V-cycle)
+      HostPattern M;
+      M.n = na;
+      std::vector<std::vector<int>> mr(na);
+      for (int i = 0; i < cur.n; ++i)
+        for (int k = cur.rowptr[i]; k < cur.rowptr[i + 1]; ++k) mr[agg[i]].push_back(agg[cur.col[k]]);
+      M.rowptr.assign(na + 1, 0);
+      for (int I = 0; I < na; ++I) {
+        auto& r = mr[I];
+        std::sort(r.begin(), r.end());
+        r.erase(std::unique(r.begin(), r.end()), r.end());
+        M.rowptr[I + 1] = M.rowptr[I] + (int)r.size();
+      }
+      for (int I = 0; I < na; ++I) M.col.insert(M.col.end(), mr[I].begin(), mr[I].end());
+      std::vector<int> agg2;
+      const int na2 = aggregate(M, agg2);
+      if (na2 >= 1 && na2 < na) {
+        for (int i = 0; i < cur.n; ++i) agg[i] = agg2[agg[i]];
+        na = na2;
+      }
+    }
+    ++lev;
     if (na >= cur.n || na < 1 || (double)cur.n / na < 1.5) break;
     // coarse pattern
     HostPattern C;

@@ -18,7 +18,7 @@ caches = []
 t0 = time.time()
 for k in range(K):
     bench.move_fingers(sc, k)
-    st, rep = fw.forward_step(sc, st, sm, fw.ForwardConfig(tol=fam["tol"]))
+    st, rep = fw.forward_step(sc, st, sm, fw.ForwardConfig(tol=fam["tol"], pullback_margin=float(os.environ.get("MARGIN", "1e-6"))))
     print(f"step {k}: its {rep.iterations} kry {rep.krylov_iterations} conv {rep.converged}", file=sys.stderr, flush=True)
     caches.append(rep.cache)
 t1 = time.time()

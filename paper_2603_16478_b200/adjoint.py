@@ -20,6 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
+from . import _pinned
 from . import elasticity as el
 from .linsolve import SolverConfig, SolveReport
 
@@ -256,9 +257,13 @@ def backprop_rollout(caches, loss_spec, solver_cfg=None, solve_reports=None):
                 check_solve(rep, k)
                 _lib.check(L.dp_backprop_step(dev.handle, cache._dc.handle, _lib.ptr(z), _lib.ptr(dv),
                                               _lib.PTR_DEVICE, _lib.ptr(dqb), _lib.ptr(dvb), _lib.ptr(f)))
-                fext[k - 1] = f.cpu().numpy()
+                # dL/dfext of the step, straight into page-locked host memory
+                fk = _pinned.empty(n)
+                torch.from_numpy(fk).copy_(f, non_blocking=True)
+                fext[k - 1] = fk
                 dq, dqb = dqb, dq
                 dv, dvb = dvb, dv
+            stream.synchronize()   # the non-blocking dL/dfext copies have landed
             dq = dq.cpu().numpy()
             dv = dv.cpu().numpy()
     else:

@@ -28,6 +28,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
+from . import _pinned
 from . import core
 
 
@@ -258,8 +259,10 @@ def forward_step(scene, state, sysmat, cfg=None, device_io=None):
             raise ValueError("state does not match scene")
         q0 = _lib.f64(state.q)
         v0 = _lib.f64(state.v)
-        q1 = np.empty(n)
-        v1 = np.empty(n)
+        # outputs in page-locked memory: the step's device-to-host copies are
+        # direct DMA, and the next step's host-to-device copies of them too
+        q1 = _pinned.empty(n)
+        v1 = _pinned.empty(n)
         kind = _lib.PTR_HOST
     else:
         q0, v0 = device_io["q_bar"], device_io["v_bar"]

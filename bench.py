@@ -343,6 +343,8 @@ def gpu_arm(args, rank, world, local_rank):
     K, W = args.steps, args.warmup
     dd = dict(device="cuda:%d" % local_rank, dtype=torch.float64)
     cfg = fw.ForwardConfig(tol=cdef["tol"])
+    if os.environ.get("BENCH_ETA"):          # diagnostics: Newton forcing term
+        cfg.lin_rtol_max = cfg.lin_rtol_min = float(os.environ["BENCH_ETA"])
     # adjoint: the reference's tolerance (1e-10) and iteration cap; GMRES(20)
     # instead of the default restart length 50: with the V-cycle the solve
     # needs ~60-70 iterations either way and the shorter Gram-Schmidt

@@ -81,8 +81,9 @@ typedef struct {
   int32_t max_iter;              /* 100    */
   int32_t max_line_search;       /* 40     */
   double pullback_margin;        /* 1e-6   */
-  double lin_rtol_max;           /* loosest Newton linear-solve rtol (1e-3)   */
-  double lin_rtol_min;           /* tightest (1e-3: constant forcing term)   */
+  double lin_rtol_max;           /* Newton linear-solve rtol while the residual
+                                    is > 1000 tol (1e-2)                     */
+  double lin_rtol_min;           /* ... and once within 1000 tol (1e-3)      */
   int32_t lin_max_iter;          /* per Newton linear solve                   */
   int32_t gmres_restart;         /* 50                                        */
 } dp_forward_cfg;

@@ -263,6 +263,7 @@ static const double g_watch_frac = getenv("DP_LS_WATCH_FRAC") ? atof(getenv("DP_
 static const int g_spec_jac = getenv("DP_LS_SPECJAC") ? atoi(getenv("DP_LS_SPECJAC")) : 1;
 static const int g_ls_norm = getenv("DP_LS_NORM") ? atoi(getenv("DP_LS_NORM")) : 0;
 static const int g_newton_x0 = getenv("DP_NEWTON_X0") ? atoi(getenv("DP_NEWTON_X0")) : 1;
+static const double g_eta_near = getenv("DP_ETA_NEAR") ? atof(getenv("DP_ETA_NEAR")) : 1000.0;
 static const double g_eta_plateau = getenv("DP_ETA_PLATEAU") ? atof(getenv("DP_ETA_PLATEAU")) : 0.0;
 static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -316,8 +317,8 @@ void dp_forward_cfg_default(dp_forward_cfg* c) {
   c->max_iter = 100;
   c->max_line_search = 40;
   c->pullback_margin = 1e-6;
-  c->lin_rtol_max = 1e-3;
-  c->lin_rtol_min = 1e-3;
+  c->lin_rtol_max = 1e-2;   // while max|r| > 1000 tol
+  c->lin_rtol_min = 1e-3;   // once max|r| <= 1000 tol
   c->lin_max_iter = 5000;
   c->gmres_restart = 50;
 }
@@ -1182,12 +1183,19 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     launch_assemble(s, s->val_fwd, 0, 0);
     k_neg<<<grid_for(n3, 256), 256, 0, s->stream>>>(n3, s->r, s->rhs);
     s->launches++;
-    // forcing term: aim the linear residual at 0.1 * tol * scale in 2-norm
+    // forcing term (relative 2-norm of the linear residual): lin_rtol_max
+    // while the Newton residual is far from the stop threshold, lin_rtol_min
+    // once it is within 1000x of it (DP_ETA_NEAR), so the last steps are
+    // accurate solves and the root lands as close to the exact-solve root as
+    // before (measured: C5 19.1 -> 23.8 steps/s with fewer Newton iterations;
+    // a constant 1e-2 moved the converged state of the soft, stiffly bound
+    // trunk parity scene by 1.4e-9 m, over its 1e-8 relative bound; 100x
+    // did too, 1000x keeps every parity test green)
     const double rn = std::sqrt(E.rnorm2);
-    double eta = (rn > 0) ? 0.1 * cfg.tol * scale / rn : cfg.lin_rtol_max;
+    double eta = (res <= g_eta_near * cfg.tol) ? cfg.lin_rtol_min : cfg.lin_rtol_max;
+    if (eta > cfg.lin_rtol_max) eta = cfg.lin_rtol_max;
     // after a line search that had to cut the step below 1/16 the Newton
     // model is poor (friction cone / activation kinks): a cheap direction is enough
-    eta = std::min(cfg.lin_rtol_max, std::max(cfg.lin_rtol_min, eta));
     if (last_t < 1.0 / 16) eta = std::max(eta, g_eta_plateau);
     int iters = 0, brk = 0;
     double relres = 0;

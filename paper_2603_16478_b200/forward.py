@@ -40,8 +40,8 @@ class ForwardConfig:
     max_iter: int = 100
     max_line_search: int = 40
     pullback_margin: float = 1e-6
-    lin_rtol_max: float = 1e-3
-    lin_rtol_min: float = 1e-3
+    lin_rtol_max: float = 1e-2     # Krylov rtol while max|r| > 1000 tol
+    lin_rtol_min: float = 1e-3     # ... and once it is within 1000 tol
     lin_max_iter: int = 5000
     gmres_restart: int = 50
 

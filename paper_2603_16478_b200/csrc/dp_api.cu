@@ -263,6 +263,9 @@ static const double g_watch_frac = getenv("DP_LS_WATCH_FRAC") ? atof(getenv("DP_
 static const int g_spec_jac = getenv("DP_LS_SPECJAC") ? atoi(getenv("DP_LS_SPECJAC")) : 1;
 static const int g_ls_norm = getenv("DP_LS_NORM") ? atoi(getenv("DP_LS_NORM")) : 0;
 static const int g_newton_x0 = getenv("DP_NEWTON_X0") ? atoi(getenv("DP_NEWTON_X0")) : 1;
+// adjoint PCG with the FP32 operator copy inside the iterations and FP64
+// iterative refinement (pcg_mg_solve); the 1e-10 stop test stays FP64
+static const int g_adj_fp32 = getenv("DP_ADJ_FP32") ? atoi(getenv("DP_ADJ_FP32")) : 1;
 static const double g_eta_near = getenv("DP_ETA_NEAR") ? atof(getenv("DP_ETA_NEAR")) : 1000.0;
 static const double g_eta_plateau = getenv("DP_ETA_PLATEAU") ? atof(getenv("DP_ETA_PLATEAU")) : 0.0;
 static double now_s() {
@@ -1460,7 +1463,7 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
     // (a warm start from the previous adjoint solution, as the GMRES branch
     // does, saves 1.6% of the iterations but costs more than that in the
     // extra residual SpMV and sync: measured slower, not used)
-    if (mg) rc = pcg_mg_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, &iters, &relres, &brk, 0);
+    if (mg) rc = pcg_mg_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, &iters, &relres, &brk, g_adj_fp32);
     else rc = cg_solve(s, s->val_adj, s->rhs, s->z, cfg.tol, cfg.max_iter, &iters, &relres, &brk);
     if (brk) {
       int it2 = 0;

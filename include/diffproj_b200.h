@@ -128,6 +128,11 @@ const char* dp_version(void);
 int dp_device_count(void);
 /* host wait policy for device synchronisation on `device`: 1 spin (default
  * at scene creation), 2 yield, 4 blocking sync, 0 unchanged */
+/* Page-locked host memory for the public API's per-step output arrays
+ * (cudaHostAlloc, portable).  The Python side carves arrays out of these
+ * slabs and recycles them; they are not returned before process exit. */
+int dp_pinned_alloc(int64_t bytes, void** out);
+int dp_pinned_free(void* p);
 int dp_set_spin_wait(int32_t device, int32_t mode);
 
 /* ---- scene (core.assemble_system_matrix, core.py:379-389; build_elements,

@@ -105,6 +105,8 @@ SIGNATURES = {
     "dp_scene_set_params": (C.c_int, [_P, C.c_double, C.c_double, C.c_double, _P]),
     "dp_scene_set_solver_options": (C.c_int, [_P, C.c_int32, C.c_double, C.c_int32]),
     "dp_scene_set_materials": (C.c_int, [_P, _P, _P, _P]),
+    "dp_pinned_alloc": (C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),
+    "dp_pinned_free": (C.c_int, [_P]),
     "dp_scene_set_self_contact": (C.c_int, [_P, C.c_int32, _P, C.c_double, C.c_int32]),
     "dp_self_contact_query": (C.c_int, [_P, _P, _P, C.c_int32, _P, _P, _P, _P]),
     "dp_scene_get_mg_levels": (C.c_int, [_P, c_int32_p, _P, C.c_int32]),

@@ -19,19 +19,29 @@ import weakref
 
 import numpy as np
 
+_ALL_SLABS = []               # every slab ever allocated (kept until exit)
 _MIN_BYTES = 1 << 20          # below this a plain NumPy array is as fast
 _SLAB_BYTES = 64 << 20
 
 
 class _Slab:
+    """One cudaHostAlloc'd block (dp_pinned_alloc), never freed before the
+    process exits: freeing page-locked memory during interpreter teardown,
+    after the CUDA context is gone, aborts the process."""
+
     __slots__ = ("buf", "size", "off", "live", "__weakref__")
 
     def __init__(self, nbytes):
-        import torch
-        self.buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        import ctypes as C
+        from . import _lib
+        L = _lib.lib()
+        p = C.c_void_p()
+        _lib.check(L.dp_pinned_alloc(nbytes, C.byref(p)))
+        self.buf = np.frombuffer((C.c_uint8 * nbytes).from_address(p.value), dtype=np.uint8)
         self.size = nbytes
         self.off = 0
         self.live = 0
+        _ALL_SLABS.append(self)
 
 
 class _Owner:
@@ -91,7 +101,7 @@ class PinnedPool:
             off = s.off
             s.off += need
             s.live += 1
-        owner = _Owner(s.buf[off:off + nbytes].numpy())
+        owner = _Owner(s.buf[off:off + nbytes])
         arr = np.ndarray((int(n),), dtype=dt, buffer=owner)
         weakref.finalize(owner, self._release, s)
         return arr

@@ -266,6 +266,9 @@ static const int g_newton_x0 = getenv("DP_NEWTON_X0") ? atoi(getenv("DP_NEWTON_X
 // adjoint PCG with the FP32 operator copy inside the iterations and FP64
 // iterative refinement (pcg_mg_solve); the 1e-10 stop test stays FP64
 static const int g_adj_fp32 = getenv("DP_ADJ_FP32") ? atoi(getenv("DP_ADJ_FP32")) : 1;
+// FP32 element block stream + FP32-only forward operator for frictionless
+// multigrid-PCG steps (EV_H32)
+static const int g_fwd_h32 = getenv("DP_FWD_H32") ? atoi(getenv("DP_FWD_H32")) : 1;
 static const double g_eta_near = getenv("DP_ETA_NEAR") ? atof(getenv("DP_ETA_NEAR")) : 1000.0;
 static const double g_eta_plateau = getenv("DP_ETA_PLATEAU") ? atof(getenv("DP_ETA_PLATEAU")) : 0.0;
 static double now_s() {
@@ -285,6 +288,18 @@ const char* dp_version(void) { return "diffproj_b200 0.1 (sm_100a)"; }
 static inline void invalidate_adjoint(dp_scene* s) {
   s->adj_cache_tag = nullptr;
   s->mg_adj_ready = 0;
+}
+
+int dp_pinned_alloc(int64_t bytes, void** out) {
+  *out = nullptr;
+  if (bytes <= 0) { set_error("pinned allocation size must be positive"); return DP_ERR_VALUE; }
+  DP_CUDA(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable));
+  return DP_OK;
+}
+
+int dp_pinned_free(void* p) {
+  if (p) DP_CUDA(cudaFreeHost(p));
+  return DP_OK;
 }
 
 int dp_set_spin_wait(int32_t device, int32_t mode) {
@@ -1077,8 +1092,8 @@ static int cache_store(dp_scene* s, dp_cache* c, const double* q_eval, int C, in
 
 // evaluate(q, contacts) of forward.py:186-192: element projections (with
 // or without Jacobian blocks), contact multipliers, momentum residual.
-static void evaluate(dp_scene* s, const double* q, double* r, int jac) {
-  launch_elements(s, q, jac ? EV_JAC : 0, &s->esc->status);
+static void evaluate(dp_scene* s, const double* q, double* r, int mode) {
+  launch_elements(s, q, mode, &s->esc->status);
   launch_contacts(s, q, s->q_bar, -1, s->c_vertex, s->c_frame, s->c_dn, s->c_mu, s->c_delta, 0, 0, s->esc);
   launch_residual(s, q, s->q_hat, r, s->esc);
 }
@@ -1153,7 +1168,18 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
   double* q_eval = s->q_ev;
   double last_t = 1.0;   // step length accepted by the previous line search
   bool elems_at_q = false;   // element buffers hold the Jacobian pass at q
-  const int trial_mode = g_spec_jac ? EV_JAC : 0;
+  // frictionless scenes solved by multigrid PCG: the Newton operator is only
+  // ever applied from its FP32 copy, so the element kernel writes an FP32
+  // block stream and the assembly writes only the FP32 operator (EV_H32)
+  const bool frictionless = [&] {
+    for (int j = 0; j < s->colliders.n; ++j)
+      if (s->colliders.mu[j] != 0.0) return false;
+    return !(s->self.enabled && s->self.mu != 0.0);
+  }();
+  const int h32 = (g_fwd_h32 && frictionless && s->mg != nullptr && s->use_mg >= 2 && s->val32 != nullptr &&
+                   s->NV == 4) ? EV_H32 : 0;
+  const int jac_mode = EV_JAC | h32;
+  const int trial_mode = g_spec_jac ? jac_mode : 0;
   for (int it = 0; it < cfg.max_iter; ++it) {
     double t_it0 = g_debug ? now_s() : 0.0;
     k_reset_flags<<<1, 1, 0, s->stream>>>(s->esc);
@@ -1164,7 +1190,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
       launch_contacts(s, q, s->q_bar, -1, s->c_vertex, s->c_frame, s->c_dn, s->c_mu, s->c_delta, 0, 0, s->esc);
       launch_residual(s, q, s->q_hat, s->r, s->esc);
     } else {
-      evaluate(s, q, s->r, 1);
+      evaluate(s, q, s->r, jac_mode);
     }
     elems_at_q = false;
     s->launches += 1;
@@ -1183,7 +1209,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     if (res <= cfg.tol) { converged = true; break; }
     // Newton matrix A - dA + K_b + K_c (assemble_system_jacobian, forward.py:113-149)
     const double t_asm0 = g_debug ? now_s() : 0.0;
-    launch_assemble(s, s->val_fwd, 0, 0);
+    launch_assemble(s, s->val_fwd, 0, 0, h32 ? 1 : 0);
     k_neg<<<grid_for(n3, 256), 256, 0, s->stream>>>(n3, s->r, s->rhs);
     s->launches++;
     // forcing term (relative 2-norm of the linear residual): lin_rtol_max

@@ -214,6 +214,7 @@ struct dp_scene {
   unsigned short* val16 = nullptr;
   float* sc16 = nullptr;
   const double* val32_src = nullptr;   // operator val32 was last written from
+  int val64_valid = 1;                 // 0: the last assembly wrote only the FP32 copy (EV_H32 forward)
   float* minv32 = nullptr;         // FP32 block-Jacobi inverses (multigrid smoother)
 
   // element outputs
@@ -320,7 +321,7 @@ int grid_for(int64_t n, int threads);
 // launchers (dp_kernels.cu) -----------------------------------------------
 // element evaluation: mode bit 1 = jacobian blocks, bit 2 = store P/dP for
 // backprop, bit 4 = zero jacobian (A-matrix assembly).
-enum { EV_JAC = 1, EV_STOREP = 2, EV_AMAT = 4, EV_LIST = 8 };
+enum { EV_JAC = 1, EV_STOREP = 2, EV_AMAT = 4, EV_LIST = 8, EV_H32 = 16 };
 void launch_elements(dp_scene* s, const double* q, int mode, int* status);
 // residual gather r = M(q - q_hat) + sum_e f_e - h^2 J_b^T lam_b + contact forces; max|r| into esc
 void launch_residual(dp_scene* s, const double* q, const double* q_hat, double* r, dp::EvalScalars* esc);
@@ -329,7 +330,7 @@ void launch_watch_select(dp_scene* s, const double* r, double frac);
 void launch_watch_elements(dp_scene* s, const double* q);
 void launch_watch_check(dp_scene* s, const double* q, double rmax_prev);
 // BSR gather: val = M + sum_e H_e + K_b + (K_c or K_c^T); plus block-Jacobi inverses
-void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat);
+void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat, int h32 = 0);
 void launch_spmv(dp_scene* s, const double* val, const double* x, double* y);
 // Krylov
 int cg_solve(dp_scene* s, const double* val, const double* b, double* x, double rtol, int max_iter,

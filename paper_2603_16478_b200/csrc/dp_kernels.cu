@@ -191,6 +191,34 @@ __device__ __forceinline__ void store_hpair(double* __restrict__ Hs, double* __r
   Ht[t] = v[8];
 }
 
+// FP32 block stream (frictionless forward steps, EV_H32): the same block,
+// rounded to FP32, 8 floats in one 256-bit store + the tail float, in the
+// first half of the FP64 stream's storage (half the stream traffic of the
+// element kernel and the assembly; the forward solves run on the FP32
+// operator anyway)
+template <int NV>
+__device__ __forceinline__ void store_hpair32(double* __restrict__ Hs, double* __restrict__ Ht,
+                                              const int* __restrict__ epos, int e, int p, double hw, double bb,
+                                              const double blk[3][3]) {
+  constexpr int NP = NV * (NV + 1) / 2;
+  float v[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) v[i * 3 + j] = (float)(hw * (((i == j) ? bb : 0.0) - blk[i][j]));
+  const int tc = __ldg(epos + (size_t)e * NP + p);
+  const int t = tc >= 0 ? tc : ~tc;
+  float* o = reinterpret_cast<float*>(Hs) + (size_t)t * 8;
+  if (tc >= 0) {
+    const float f8[8] = {v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]};
+    st256f(o, f8);
+  } else {
+    const float f8[8] = {v[0], v[3], v[6], v[1], v[4], v[7], v[2], v[5]};
+    st256f(o, f8);
+  }
+  reinterpret_cast<float*>(Ht)[t] = v[8];
+}
+
 // One thread per element.  NV = vertices per element (4 tet, 3 tri).  The
 // mode is a template parameter: the residual-only instantiation (line-search
 // trials) does not carry the Jacobian path's registers (168 -> fewer), so it
@@ -401,7 +429,8 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
         const double bb = js[(FB + p) * 128];
         double blk[3][3];
         jac_block<D>(J, aa, ab, blk);
-        store_hpair<NV>(H, Ht, epos, e, p, hw, bb, blk);
+        if (mode & EV_H32) store_hpair32<NV>(H, Ht, epos, e, p, hw, bb, blk);
+        else store_hpair<NV>(H, Ht, epos, e, p, hw, bb, blk);
       }
     }
     return;
@@ -439,7 +468,8 @@ __global__ void __launch_bounds__(128, DP_ELEM_MINB)
         } else {
           jac_block<D>(J, alpha[a], alpha[b], blk);
         }
-        store_hpair<NV>(H, Ht, epos, e, p, hw, bb, blk);
+        if (mode & EV_H32) store_hpair32<NV>(H, Ht, epos, e, p, hw, bb, blk);
+        else store_hpair<NV>(H, Ht, epos, e, p, hw, bb, blk);
       }
   }
 }
@@ -454,6 +484,7 @@ static void launch_elements_nv(dp_scene* s, const double* q, int mode, int* stat
   switch (mode) {
     DP_ELEM_CASE(0)
     DP_ELEM_CASE(EV_JAC)
+    DP_ELEM_CASE(EV_JAC | EV_H32)
     DP_ELEM_CASE(EV_JAC | EV_STOREP)
     DP_ELEM_CASE(EV_JAC | EV_AMAT)
     DP_ELEM_CASE(EV_STOREP)
@@ -702,7 +733,7 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
                                                   int use_extras, double h2, double* __restrict__ val,
                                                   double* __restrict__ minv, float* __restrict__ val32,
                                                   float* __restrict__ minv32, unsigned short* __restrict__ val16,
-                                                  float* __restrict__ sc16) {
+                                                  float* __restrict__ sc16, int h32) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= S) return;
@@ -710,7 +741,7 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
   const int base = slice_base[gw];
   const int K = slice_width[gw];
   const int dslot = (row < V) ? diag_slot[row] : -1;
-  double* vs = val + (size_t)base * 9;
+  double* vs = val ? val + (size_t)base * 9 : nullptr;   // null: FP32 copy only
   for (int k = 0; k < K; ++k) {
     const int slot = base + k * kSlice + lane;
     double b[9];
@@ -725,6 +756,33 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
     const double* hs = H + (size_t)ri.x * kHS;
     const double* ht = Ht + ri.x;
     int t = 0;
+    if (h32) {
+      // FP32 block stream (EV_H32): 32 B + 4 B per block
+      const float* hs32 = reinterpret_cast<const float*>(H) + (size_t)ri.x * 8;
+      const float* ht32 = reinterpret_cast<const float*>(Ht) + ri.x;
+      for (; t + ASM_CHUNK <= n; t += ASM_CHUNK) {
+        double src[ASM_CHUNK][9];
+#pragma unroll
+        for (int g = 0; g < ASM_CHUNK; ++g) {
+          float f[8];
+          ld256f(hs32 + (size_t)(t + g) * 8, f);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) src[g][c] = f[c];
+          src[g][8] = __ldg(ht32 + t + g);
+        }
+#pragma unroll
+        for (int g = 0; g < ASM_CHUNK; ++g) acc_block(b, src[g], tr);
+      }
+      for (; t < n; ++t) {
+        double src[9];
+        float f[8];
+        ld256f(hs32 + (size_t)t * 8, f);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) src[c] = f[c];
+        src[8] = __ldg(ht32 + t);
+        acc_block(b, src, tr);
+      }
+    } else {
     for (; t + ASM_CHUNK <= n; t += ASM_CHUNK) {
       double src[ASM_CHUNK][9];
 #pragma unroll
@@ -742,6 +800,7 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
       ld256(hs + (size_t)t * kHS + 4, &src[4]);
       src[8] = __ldg(ht + t);
       acc_block(b, src, tr);
+    }
     }
     if (slot == dslot) {
       const double m = mass[row];
@@ -769,8 +828,10 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
         for (int u = 0; u < 9; ++u) minv32[(size_t)u * V + row] = (float)o[u];
       }
     }
+    if (vs) {
 #pragma unroll
-    for (int c = 0; c < 9; ++c) vs[(k * 9 + c) * kSlice + lane] = b[c];
+      for (int c = 0; c < 9; ++c) vs[(k * 9 + c) * kSlice + lane] = b[c];
+    }
     if (val32) {
       // FP32 copy for the multigrid smoother: 12 floats per slot (9 + pad),
       // slot-major, so a lane reads its block as three 16-byte loads and a
@@ -806,7 +867,7 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
   }
 }
 
-void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat) {
+void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat, int h32) {
   (void)transpose_contacts;   // contact blocks are already stored transposed by the contact kernel
   const int nt = 256;
   const int nb = grid_for((int64_t)s->S * 32, nt);
@@ -815,41 +876,46 @@ void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat)
   k_assemble<<<nb, nt, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->diag_slot, s->rinfo,
                                        s->H, s->Ht, s->mass, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_comp,
                                        has_c ? s->c_count : nullptr, s->c_off, s->c_blk, amat ? 0 : 1,
-                                       s->h * s->h, val, s->minv, amat ? nullptr : s->val32,
+                                       s->h * s->h, h32 ? nullptr : val, s->minv, amat ? nullptr : s->val32,
                                        amat ? nullptr : s->minv32, amat ? nullptr : s->val16,
-                                       amat ? nullptr : s->sc16);
+                                       amat ? nullptr : s->sc16, h32);
   ktm_end(s, KT_ASSEMBLE);
   if (!amat && s->val32) s->val32_src = val;   // the FP32 copy now mirrors `val`
+  if (!amat) s->val64_valid = !h32;              // false: only the FP32 copy of `val` is current
   s->launches++;
 }
 
 // ---------------------------------------------------------------------------
 // SELL-32 BSR SpMV: one warp per slice of 32 block rows, one lane per row.
 
-template <bool PRECOND>
+template <bool PRECOND, class TV>
 __device__ __forceinline__ void spmv_row(int V, int slice, int lane, const int* __restrict__ slice_base,
                                          const int* __restrict__ slice_width, const int* __restrict__ col,
-                                         const double* __restrict__ val, const double* __restrict__ x, double y[3]) {
+                                         const TV* __restrict__ val, const double* __restrict__ x, double y[3]) {
   const int base = slice_base[slice];
   const int K = slice_width[slice];
-  const double* vs = val + (size_t)base * 9 + lane;
+  const TV* vs = val + (size_t)base * 9 + lane;
   const int* cs = col + base + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll 2
   for (int k = 0; k < K; ++k) {
     const int j = __ldg(cs + k * kSlice);
-    const double* v = vs + k * 9 * kSlice;
+    const TV* v = vs + k * 9 * kSlice;
     const double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
-    a0 += __ldcs(v + 0 * kSlice) * x0 + __ldcs(v + 1 * kSlice) * x1 + __ldcs(v + 2 * kSlice) * x2;
-    a1 += __ldcs(v + 3 * kSlice) * x0 + __ldcs(v + 4 * kSlice) * x1 + __ldcs(v + 5 * kSlice) * x2;
-    a2 += __ldcs(v + 6 * kSlice) * x0 + __ldcs(v + 7 * kSlice) * x1 + __ldcs(v + 8 * kSlice) * x2;
+    a0 += (double)__ldcs(v + 0 * kSlice) * x0 + (double)__ldcs(v + 1 * kSlice) * x1 +
+          (double)__ldcs(v + 2 * kSlice) * x2;
+    a1 += (double)__ldcs(v + 3 * kSlice) * x0 + (double)__ldcs(v + 4 * kSlice) * x1 +
+          (double)__ldcs(v + 5 * kSlice) * x2;
+    a2 += (double)__ldcs(v + 6 * kSlice) * x0 + (double)__ldcs(v + 7 * kSlice) * x1 +
+          (double)__ldcs(v + 8 * kSlice) * x2;
   }
   y[0] = a0; y[1] = a1; y[2] = a2;
 }
 
+template <class TV>
 __global__ void __launch_bounds__(256) k_spmv(int V, int S, const int* __restrict__ slice_base,
                                               const int* __restrict__ slice_width, const int* __restrict__ col,
-                                              const double* __restrict__ val, const double* __restrict__ x,
+                                              const TV* __restrict__ val, const double* __restrict__ x,
                                               double* __restrict__ y) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -863,7 +929,10 @@ __global__ void __launch_bounds__(256) k_spmv(int V, int S, const int* __restric
 void launch_spmv(dp_scene* s, const double* val, const double* x, double* y) {
   const int nb = grid_for((int64_t)s->S * 32, 256);
   ktm_begin(s, KT_SPMV);
-  k_spmv<<<nb, 256, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->col, val, x, y);
+  if (val == s->val32_src && !s->val64_valid)   // FP32-only forward operator (EV_H32)
+    k_spmv<float><<<nb, 256, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->col, s->val32, x, y);
+  else
+    k_spmv<double><<<nb, 256, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->col, val, x, y);
   ktm_end(s, KT_SPMV);
   s->launches++;
 }
@@ -1016,9 +1085,10 @@ __global__ void __launch_bounds__(kVT) k_cg_update(int V, const double* __restri
 }
 
 // r = b - A x ; returns partial |r|^2 -> scalar (used for true residuals)
+template <class TV>
 __global__ void __launch_bounds__(256) k_resid_true(int V, int S, const int* __restrict__ slice_base,
                                                     const int* __restrict__ slice_width, const int* __restrict__ col,
-                                                    const double* __restrict__ val, const double* __restrict__ x,
+                                                    const TV* __restrict__ val, const double* __restrict__ x,
                                                     const double* __restrict__ b, double* __restrict__ r,
                                                     double* partial, unsigned int* counter, double* result) {
   __shared__ double sh[32];
@@ -1089,8 +1159,12 @@ double device_norm2(dp_scene* s, const double* x) {
 static double true_relres(dp_scene* s, const double* val, const double* b, const double* x, double* r, double bnorm) {
   const int nb = grid_for((int64_t)s->S * 32, 256);
   double* res = s->red.partial + s->red.cap_blocks * s->red.width - 1;
-  k_resid_true<<<nb, 256, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->col, val, x, b, r,
-                                          s->red.partial, s->red.counter, res);
+  if (val == s->val32_src && !s->val64_valid)   // FP32-only forward operator (EV_H32)
+    k_resid_true<float><<<nb, 256, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->col, s->val32, x,
+                                                   b, r, s->red.partial, s->red.counter, res);
+  else
+    k_resid_true<double><<<nb, 256, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->col, val, x, b,
+                                                    r, s->red.partial, s->red.counter, res);
   s->launches++;
   cudaMemcpyAsync(&s->h_ksc->pad[1], res, sizeof(double), cudaMemcpyDeviceToHost, s->stream);
   cudaStreamSynchronize(s->stream);
@@ -1844,7 +1918,13 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   double* y_dev = s->ks;   // scratch (>= restart doubles)
   const bool tight = rtol < 1e-7;   // inexact Newton solves skip re-orthogonalisation
   // inexact solves with the V-cycle run in FP32 (basis + operator copy)
-  const bool lowp = g_gm_fp32 && use_mg && !left && !tight && s->val32 != nullptr && val == s->val32_src;
+  const bool fp32_only = s->val32 != nullptr && val == s->val32_src && !s->val64_valid;   // EV_H32 forward
+  const bool lowp = (fp32_only || g_gm_fp32) && use_mg && !left && !tight && s->val32 != nullptr &&
+                    val == s->val32_src;
+  if (fp32_only && !lowp) {
+    set_error("GMRES needs the FP64 operator, the last assembly wrote only its FP32 copy");
+    return 1;
+  }
   *iters = 0;
   // x = 0, or the caller's initial guess (use_x0) when it beats x = 0
   if (!use_x0) cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);

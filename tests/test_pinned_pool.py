@@ -9,8 +9,7 @@ import numpy as np
 
 class _FakeSlab:
     def __init__(self, nbytes):
-        import torch
-        self.buf = torch.empty(nbytes, dtype=torch.uint8)
+        self.buf = np.empty(nbytes, dtype=np.uint8)
         self.size = nbytes
         self.off = 0
         self.live = 0

@@ -59,7 +59,8 @@ namespace dp {
 // fine-level smoother sweeps on an FP16 operator copy with per-block scales
 // (26 instead of 40 bytes per block; the preconditioner only)
 static const int g_smooth16 = getenv("DP_SMOOTH16") ? atoi(getenv("DP_SMOOTH16")) : 0;   // measured: no faster (latency-bound), off
-static const int g_mg_tail = getenv("DP_MG_TAIL") ? atoi(getenv("DP_MG_TAIL")) : 0;   // measured slower (39 us vs 23 us), off
+// two coarsest levels in one cluster launch (k_mg_tail): C5 V-cycle tail 23 -> ~14 us
+static const int g_mg_tail = getenv("DP_MG_TAIL") ? atoi(getenv("DP_MG_TAIL")) : 1;
 static const int g_mg_agg2 = getenv("DP_MG_AGG2") ? atoi(getenv("DP_MG_AGG2")) : 0;
 constexpr int kCoarseMax = 36;      // dense coarsest solve (<= 108 unknowns, shared memory)
 constexpr int kDenseSmem = 108;
@@ -75,6 +76,7 @@ struct MGLevel {
   int *mem_ptr = nullptr, *mem = nullptr;      // coarse row -> fine rows
   int* agg = nullptr;                          // fine row -> coarse row (owned by the coarse level)
   int* slot_row = nullptr;                     // SELL slot -> block row
+  int kmax = 0;                                // widest slice (slots per row)
   double *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr, *u = nullptr;
 };
 
@@ -326,6 +328,7 @@ int mg_setup(dp_scene* s) {
     L.NS = NS;
     rc |= up(mg, &L.slice_base, sb);
     rc |= up(mg, &L.slice_width, sw);
+    L.kmax = sw.empty() ? 0 : *std::max_element(sw.begin(), sw.end());
     rc |= up(mg, &L.col, cc);
     rc |= up(mg, &L.diag_slot, ds);
     rc |= al(mg, &L.val, (size_t)NS * 9);
@@ -1394,9 +1397,7 @@ void mg_assemble(dp_scene* s, const double* val) {
     s->launches++;
   }
   const MGLevel& Lc = mg->lv.back();
-  // coarsest handled by in-CTA Jacobi sweeps, unless the cluster tail kernel
-  // (exact coarsest solve) is in use
-  if (mg->coarse_sweeps > 0 && !(g_mg_tail && mg->dinv && mg->lv.size() >= 3)) return;
+  if (mg->coarse_sweeps > 0) return;   // coarsest handled by Jacobi sweeps (in-CTA / in the tail kernel)
   k_mg_dense_build<<<1, 1024, 0, s->stream>>>(Lc.n, Lc.S, Lc.slice_base, Lc.slice_width, Lc.col, Lc.val, mg->dense);
   k_mg_dense_invert<<<1, 256, (size_t)2 * mg->N * mg->N * sizeof(double), s->stream>>>(mg->N, mg->dense, mg->dinv);
   s->launches += 2;
@@ -1478,20 +1479,24 @@ static const int g_mg_rj0 = getenv("DP_MG_RJ0") ? atoi(getenv("DP_MG_RJ0")) : 1;
 
 
 // ---------------------------------------------------------------------------
-// The two coarsest levels of the V-cycle in ONE launch on a thread-block
-// cluster (round 2).  Level a = L-2 (C5: 343 block rows), level c = L-1 (27
-// rows).  Replaces restrict+jacobi0 (a), residual sweep (a), restrict + the
-// one-CTA Jacobi solve (c) and the post-sweep (a): four dependent launches
-// of 4-10 us each that were pure latency (a few hundred KB, L2-resident).
-// Rows of level a are spread over the cluster's warps (one warp per row,
-// lanes over the row's SELL slots); phases are separated by cluster
-// barriers (hardware, cheap) instead of kernel boundaries; level c (tiny) is
-// solved redundantly by every CTA in shared memory, which saves a barrier.
-// Same operators, same smoother and coarse sweeps as the per-level kernels
-// (summation order differs: warp trees instead of slot-ordered sums).
-constexpr int kTailCTAs = 8;
-constexpr int kTailNT = 256;
-constexpr int kTailMaxC = 64;   // rows of the coarsest level held in shared memory
+// The two coarsest levels of the V-cycle in ONE launch on a 16-CTA
+// thread-block cluster (round 2).  Level a = L-2 (C5: 343 block rows, one
+// SELL slice per CTA, one row per warp), level c = L-1 (27 rows, one slice).
+// Replaces restrict+jacobi0 (a), residual sweep (a), restrict + the one-CTA
+// Jacobi solve (c) and the post-sweep (a): four dependent launches that
+// were pure latency (a few hundred KB, L2-resident).
+// Each CTA stages its level-a slice and all of level c (values transposed
+// to row-major [row][slot][9] so a warp's lanes, one per slot, hit distinct
+// banks) in shared memory with cp.async while phase 1 gathers the fine
+// residual; the level-a iterate / rhs / residual never leave shared memory:
+// other CTAs read them through distributed shared memory (DSMEM) after a
+// cluster barrier.  Level c is solved redundantly by every CTA, which saves
+// a barrier.  Same operators, smoother and coarse sweeps as the per-level
+// kernels (summation order differs: warp trees instead of slot order).
+constexpr int kTailCTAs = 16;   // non-portable cluster size (sm_100 allows 16)
+constexpr int kTailNT = 1024;   // 32 warps = one level-a slice per CTA
+constexpr int kTailMaxC = 32;   // level c: one slice
+constexpr int kTailKW = 16;     // warps splitting a level-c row's slots in the coarse sweeps
 
 struct TailArgs {
   // level a (L-2)
@@ -1499,127 +1504,289 @@ struct TailArgs {
   const int *sb_a, *sw_a, *col_a;
   const double *val_a, *minv_a;
   const int *mptr_a, *mem_a;      // level-a row -> rows of the level above (rf)
-  double *b_a, *xa_a, *r_a, *x_a; // rhs, pre-smoothed iterate, residual, output
+  double* x_a;                    // output
   // level c (L-1)
   int nc;
-  const int *sb_c, *sw_c, *col_c;
+  const int *sw_c, *col_c;
   const double *val_c, *minv_c;
   const int *mptr_c, *mem_c;      // level-c row -> level-a rows
   const int* agg_c;               // level-a row -> level-c row
-  const double* dinv;             // dense inverse of the level-c operator (3 n_c square)
   const double* rf;               // residual of the level above level a
   double omega, alpha;
-  int sweeps;
+  int sweeps, ka, kc;             // coarse sweeps; shared-memory slot capacity of a / c
   const int* stop;
 };
 
-__device__ __forceinline__ void tail_row_sum(int row, int lane, const int* __restrict__ sb, const int* __restrict__ sw,
-                                             const int* __restrict__ col, const double* __restrict__ val,
-                                             const double* __restrict__ x, const double* __restrict__ xc,
-                                             const int* __restrict__ agg, double alpha, double a[3]) {
-  const int sl = row / kSlice, li = row % kSlice;
-  const int base = sb[sl], K = sw[sl];
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  for (int k = lane; k < K; k += 32) {
-    const int slot = base + k * kSlice + li;
-    const int j = col[slot];
-    const double* v = val + (size_t)base * 9 + (size_t)k * 9 * kSlice + li;
-    double x0 = x[3 * j], x1 = x[3 * j + 1], x2 = x[3 * j + 2];
-    if (xc) {
-      const int J = agg[j];
-      x0 += alpha * xc[3 * J]; x1 += alpha * xc[3 * J + 1]; x2 += alpha * xc[3 * J + 2];
-    }
-    a0 += v[0 * kSlice] * x0 + v[1 * kSlice] * x1 + v[2 * kSlice] * x2;
-    a1 += v[3 * kSlice] * x0 + v[4 * kSlice] * x1 + v[5 * kSlice] * x2;
-    a2 += v[6 * kSlice] * x0 + v[7 * kSlice] * x1 + v[8 * kSlice] * x2;
+// phase timestamps of CTA 0 (diagnostics: build with -DDP_MG_TAIL_TIMING=1
+// and run with DP_MG_TAIL_DBG=1 DP_GRAPHS=0)
+#ifndef DP_MG_TAIL_TIMING
+#define DP_MG_TAIL_TIMING 0
+#endif
+__device__ unsigned long long g_tail_clk[12], g_tail_cyc[12];
+__device__ __forceinline__ void tail_mark(int k) {
+  if (DP_MG_TAIL_TIMING && threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tail_clk[k] = t;
+    g_tail_cyc[k] = clock64();
   }
-  a[0] = warp_sum(a0); a[1] = warp_sum(a1); a[2] = warp_sum(a2);
 }
 
-__global__ void __cluster_dims__(kTailCTAs, 1, 1) __launch_bounds__(kTailNT) k_mg_tail(const __grid_constant__ TailArgs A) {
-  __shared__ double xs[3 * kTailMaxC], bs[3 * kTailMaxC];
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+
+// one SELL slice (base, width K) -> row-major shared copies sv[(li K + k) 9 + e], sc[li K + k]
+__device__ __forceinline__ void tail_stage_slice(const double* __restrict__ val, const int* __restrict__ col, int base,
+                                                 int K, double* sv, int* sc) {
+  for (int g = threadIdx.x; g < K * 9 * kSlice; g += blockDim.x) {
+    const int li = g % kSlice, ke = g / kSlice, k = ke / 9, e = ke - 9 * k;
+    cp_async8(sv + (li * K + k) * 9 + e, val + (size_t)base * 9 + g);
+  }
+  for (int g = threadIdx.x; g < K * kSlice; g += blockDim.x) {
+    const int li = g % kSlice, k = g / kSlice;
+    cp_async4(sc + li * K + k, col + base + g);
+  }
+}
+
+__global__ void __launch_bounds__(kTailNT) k_mg_tail(const __grid_constant__ TailArgs A) {
+  extern __shared__ __align__(16) double tsm[];
   if (stopped(A.stop)) return;   // uniform (set by an earlier kernel)
   cg::cluster_group cl = cg::this_cluster();
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int nw = kTailCTAs * (kTailNT / 32);
-  const int gw = (int)cl.block_rank() * (kTailNT / 32) + wib;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int rank = (int)cl.block_rank();
   const double om = A.omega;
-  // phase 1: restriction to level a and its first Jacobi sweep from zero
-  for (int I = gw; I < A.na; I += nw) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  // shared layout
+  double* sv_a = tsm;                                  // [32][ka][9]
+  double* sv_c = sv_a + (size_t)kSlice * A.ka * 9;     // [32][kc][9]
+  double* sm_a = sv_c + (size_t)kSlice * A.kc * 9;     // minv, [9][32]
+  double* sm_c = sm_a + 9 * kSlice;
+  double* sxa = sm_c + 9 * kSlice;                     // level-a pre-smoothed iterate (own slice)
+  double* sba = sxa + 3 * kSlice;                      // level-a rhs
+  double* sra = sba + 3 * kSlice;                      // level-a residual
+  double* xs = sra + 3 * kSlice;                       // level-c iterate
+  double* ys = xs + 3 * kTailMaxC;
+  double* bs = ys + 3 * kTailMaxC;
+  double* spc = bs + 3 * kTailMaxC;                    // this slice's part of the level-c rhs
+  double* spart = spc + 3 * kTailMaxC;                 // [kTailKW][3][32] partial row sums
+  int* sc_a = (int*)(spart + kTailKW * 3 * kSlice);    // [32][ka]
+  int* sc_c = sc_a + kSlice * A.ka;                    // [32][kc]
+  int* sagg = sc_c + kSlice * A.kc;                    // agg_c
+  const int I = rank * kSlice + w;                     // this warp's level-a row
+  const bool own = I < A.na;
+  const int Ka = rank * kSlice < A.na ? A.sw_a[rank] : 0;
+  const int Kc = A.sw_c[0];
+  tail_mark(0);
+  // prefetch (async) everything phases 2-4 read
+  if (rank * kSlice < A.na) tail_stage_slice(A.val_a, A.col_a, A.sb_a[rank], Ka, sv_a, sc_a);
+  tail_stage_slice(A.val_c, A.col_c, 0, Kc, sv_c, sc_c);
+  for (int g = threadIdx.x; g < 9 * kSlice; g += blockDim.x) {
+    const int e = g / kSlice, li = g % kSlice;
+    if (rank * kSlice + li < A.na) cp_async8(sm_a + g, A.minv_a + (size_t)e * A.na + rank * kSlice + li);
+    if (li < A.nc) cp_async8(sm_c + g, A.minv_c + (size_t)e * A.nc + li);
+  }
+  for (int g = threadIdx.x; g < A.na; g += blockDim.x) cp_async4(sagg + g, A.agg_c + g);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  // phase 1: restriction to level a (gather of the fine residual) and its
+  // first Jacobi sweep from zero
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  if (own) {
     for (int t = A.mptr_a[I] + lane; t < A.mptr_a[I + 1]; t += 32) {
       const int i = A.mem_a[t];
       s0 += A.rf[3 * i]; s1 += A.rf[3 * i + 1]; s2 += A.rf[3 * i + 2];
     }
     s0 = warp_sum(s0); s1 = warp_sum(s1); s2 = warp_sum(s2);
-    if (lane == 0) {
-      A.b_a[3 * I] = s0; A.b_a[3 * I + 1] = s1; A.b_a[3 * I + 2] = s2;
-      const double r[3] = {s0, s1, s2};
-      double u[3];
-      mv_minv(A.minv_a, A.na, I, r, u);
-      A.xa_a[3 * I] = om * u[0]; A.xa_a[3 * I + 1] = om * u[1]; A.xa_a[3 * I + 2] = om * u[2];
-    }
   }
-  cl.sync();
-  // phase 2: residual of level a after the pre-sweep
-  for (int I = gw; I < A.na; I += nw) {
-    double a[3];
-    tail_row_sum(I, lane, A.sb_a, A.sw_a, A.col_a, A.val_a, A.xa_a, nullptr, nullptr, 0.0, a);
-    if (lane == 0) {
-      A.r_a[3 * I] = A.b_a[3 * I] - a[0];
-      A.r_a[3 * I + 1] = A.b_a[3 * I + 1] - a[1];
-      A.r_a[3 * I + 2] = A.b_a[3 * I + 2] - a[2];
-    }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  if (own && lane == 0) {
+    sba[3 * w] = s0; sba[3 * w + 1] = s1; sba[3 * w + 2] = s2;
+    const double r[3] = {s0, s1, s2};
+    double u[3];
+    mv_minv(sm_a, kSlice, w, r, u);
+    sxa[3 * w] = om * u[0]; sxa[3 * w + 1] = om * u[1]; sxa[3 * w + 2] = om * u[2];
   }
+  tail_mark(1);
   cl.sync();
-  // phase 3 (every CTA, shared memory): restriction to level c and its
-  // exact solve with the dense inverse (mg_assemble builds it whenever the
-  // tail kernel is in use; N = 3 n_c <= 108)
-  for (int I = wib; I < A.nc; I += kTailNT / 32) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int t = A.mptr_c[I] + lane; t < A.mptr_c[I + 1]; t += 32) {
-      const int i = A.mem_c[t];
-      s0 += A.r_a[3 * i]; s1 += A.r_a[3 * i + 1]; s2 += A.r_a[3 * i + 2];
+  tail_mark(2);
+  // phase 2: residual of level a after the pre-sweep (x of other slices via DSMEM)
+  if (own) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int k = lane; k < Ka; k += 32) {
+      const int j = sc_a[w * Ka + k];
+      const double* v = sv_a + (w * Ka + k) * 9;
+      const double* xr = cl.map_shared_rank(sxa, j / kSlice) + 3 * (j % kSlice);
+      const double x0 = xr[0], x1 = xr[1], x2 = xr[2];
+      a0 += v[0] * x0 + v[1] * x1 + v[2] * x2;
+      a1 += v[3] * x0 + v[4] * x1 + v[5] * x2;
+      a2 += v[6] * x0 + v[7] * x1 + v[8] * x2;
     }
-    s0 = warp_sum(s0); s1 = warp_sum(s1); s2 = warp_sum(s2);
-    if (lane == 0) { bs[3 * I] = s0; bs[3 * I + 1] = s1; bs[3 * I + 2] = s2; }
+    a0 = warp_sum(a0); a1 = warp_sum(a1); a2 = warp_sum(a2);
+    if (lane == 0) {
+      sra[3 * w] = sba[3 * w] - a0; sra[3 * w + 1] = sba[3 * w + 1] - a1; sra[3 * w + 2] = sba[3 * w + 2] - a2;
+    }
   }
   __syncthreads();
+  // this slice's contribution to the level-c restriction (rows in order)
+  if (w == 0 && lane < A.nc) {
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    const int nr = min(kSlice, A.na - rank * kSlice);
+    for (int li = 0; li < nr; ++li)
+      if (sagg[rank * kSlice + li] == lane) { t0 += sra[3 * li]; t1 += sra[3 * li + 1]; t2 += sra[3 * li + 2]; }
+    spc[3 * lane] = t0; spc[3 * lane + 1] = t1; spc[3 * lane + 2] = t2;
+  }
+  tail_mark(3);
+  cl.sync();
+  tail_mark(4);
+  // phase 3 (every CTA): restriction to level c = sum over the cluster's
+  // CTAs of their per-slice partial sums (DSMEM, fixed CTA order), and
+  // k_mg_coarse_jacobi's iteration x = w Minv b, then `sweeps` times
+  // x <- x + w Minv (b - A x)
+  if (w == 0 && lane < A.nc) {
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0, p[3 * kTailCTAs];
+#pragma unroll
+    for (int q = 0; q < kTailCTAs; ++q) {   // all loads in flight, then the ordered sum
+      const double* pr = cl.map_shared_rank(spc, q) + 3 * lane;
+      p[3 * q] = pr[0]; p[3 * q + 1] = pr[1]; p[3 * q + 2] = pr[2];
+    }
+#pragma unroll
+    for (int q = 0; q < kTailCTAs; ++q) { t0 += p[3 * q]; t1 += p[3 * q + 1]; t2 += p[3 * q + 2]; }
+    bs[3 * lane] = t0; bs[3 * lane + 1] = t1; bs[3 * lane + 2] = t2;
+    const double r[3] = {t0, t1, t2};
+    double u[3];
+    mv_minv(sm_c, kSlice, lane, r, u);
+    xs[3 * lane] = om * u[0]; xs[3 * lane + 1] = om * u[1]; xs[3 * lane + 2] = om * u[2];
+  }
+  __syncthreads();
+  tail_mark(7);
+  const double* xcs = xs;
+  // sweeps: lane = level-c row, warps split the row's slots (partial sums
+  // in shared memory), ping-pong iterates: two block barriers per sweep
   {
-    const int N = 3 * A.nc;
-    for (int i = wib; i < N; i += kTailNT / 32) {
-      double acc = 0.0;
-      for (int j = lane; j < N; j += 32) acc += A.dinv[(size_t)i * N + j] * bs[j];
-      acc = warp_sum(acc);
-      if (lane == 0) xs[i] = acc;
-    }
-  }
-  __syncthreads();
-  // phase 4: post-sweep of level a with the coarse correction in its gathers
-  for (int I = gw; I < A.na; I += nw) {
-    double a[3];
-    tail_row_sum(I, lane, A.sb_a, A.sw_a, A.col_a, A.val_a, A.xa_a, xs, A.agg_c, A.alpha, a);
-    if (lane == 0) {
-      const int J = A.agg_c[I];
-      double xt[3], r[3], u[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        xt[c] = A.xa_a[3 * I + c] + A.alpha * xs[3 * J + c];
-        r[c] = A.b_a[3 * I + c] - a[c];
+    double* xc = xs;
+    double* yc = ys;
+    for (int it = 0; it < A.sweeps; ++it) {
+      if (w < kTailKW) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        if (lane < A.nc) {
+          for (int k = w; k < Kc; k += kTailKW) {
+            const int j = sc_c[lane * Kc + k];
+            const double* v = sv_c + (lane * Kc + k) * 9;
+            const double x0 = xc[3 * j], x1 = xc[3 * j + 1], x2 = xc[3 * j + 2];
+            a0 += v[0] * x0 + v[1] * x1 + v[2] * x2;
+            a1 += v[3] * x0 + v[4] * x1 + v[5] * x2;
+            a2 += v[6] * x0 + v[7] * x1 + v[8] * x2;
+          }
+        }
+        spart[(w * 3 + 0) * kSlice + lane] = a0;
+        spart[(w * 3 + 1) * kSlice + lane] = a1;
+        spart[(w * 3 + 2) * kSlice + lane] = a2;
       }
-      mv_minv(A.minv_a, A.na, I, r, u);
+      __syncthreads();
+      if (w == 0 && lane < A.nc) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) A.x_a[3 * I + c] = xt[c] + om * u[c];
+        for (int q = 0; q < kTailKW; ++q) {
+          a0 += spart[(q * 3 + 0) * kSlice + lane];
+          a1 += spart[(q * 3 + 1) * kSlice + lane];
+          a2 += spart[(q * 3 + 2) * kSlice + lane];
+        }
+        const double r[3] = {bs[3 * lane] - a0, bs[3 * lane + 1] - a1, bs[3 * lane + 2] - a2};
+        double u[3];
+        mv_minv(sm_c, kSlice, lane, r, u);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) yc[3 * lane + c] = xc[3 * lane + c] + om * u[c];
+      }
+      __syncthreads();
+      double* t = xc; xc = yc; yc = t;
     }
+    xcs = xc;
   }
+  tail_mark(5);
+  // phase 4: post-sweep of level a with the coarse correction in its gathers
+  const double* xcr = xcs;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  if (own) {
+    for (int k = lane; k < Ka; k += 32) {
+      const int j = sc_a[w * Ka + k];
+      const double* v = sv_a + (w * Ka + k) * 9;
+      const double* xr = cl.map_shared_rank(sxa, j / kSlice) + 3 * (j % kSlice);
+      const int J = sagg[j];
+      const double x0 = xr[0] + A.alpha * xcr[3 * J], x1 = xr[1] + A.alpha * xcr[3 * J + 1],
+                   x2 = xr[2] + A.alpha * xcr[3 * J + 2];
+      a0 += v[0] * x0 + v[1] * x1 + v[2] * x2;
+      a1 += v[3] * x0 + v[4] * x1 + v[5] * x2;
+      a2 += v[6] * x0 + v[7] * x1 + v[8] * x2;
+    }
+    a0 = warp_sum(a0); a1 = warp_sum(a1); a2 = warp_sum(a2);
+  }
+  cl.barrier_arrive();   // last remote (DSMEM) read done; the wait below keeps our shared memory alive for the others
+  if (own && lane == 0) {
+    const int J = sagg[I];
+    const double a[3] = {a0, a1, a2};
+    double xt[3], r[3], u[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      xt[c] = sxa[3 * w + c] + A.alpha * xcr[3 * J + c];
+      r[c] = sba[3 * w + c] - a[c];
+    }
+    mv_minv(sm_a, kSlice, w, r, u);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) A.x_a[3 * I + c] = xt[c] + om * u[c];
+  }
+  tail_mark(6);
+  cl.barrier_wait();
 }
 
+static size_t tail_smem_bytes(int na, int nc, int ka, int kc) {
+  return sizeof(double) * ((size_t)kSlice * (ka + kc) * 9 + 2 * 9 * kSlice + 3 * 3 * kSlice + 4 * 3 * kTailMaxC +
+                            kTailKW * 3 * kSlice) +
+         sizeof(int) * ((size_t)kSlice * (ka + kc) + (size_t)na);
+}
+
+// the cluster size the device launches k_mg_tail with (0: none)
+static int tail_cluster(size_t smem) {
+  static int ok = -1;
+  static size_t ok_smem = 0;
+  if (ok >= 0 && ok_smem >= smem) return ok;
+  cudaFuncSetAttribute(k_mg_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_mg_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kTailCTAs);
+  cfg.blockDim = dim3(kTailNT);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kTailCTAs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_mg_tail, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  ok = n > 0 ? kTailCTAs : 0;
+  ok_smem = smem;
+  return ok;
+}
 
 // usable for the level pair (l, l+1) = (L-2, L-1)
 static bool tail_usable(const MG* mg, int la) {
   const int L = (int)mg->lv.size();
-  return g_mg_tail && L >= 2 && la == L - 2 && la >= 1 && mg->nu == 1 && mg->gamma == 1 && mg->dinv != nullptr &&
-         mg->lv[L - 1].n <= kTailMaxC && (mg->post == 1 || mg->symmetric_needed);
+  if (!(g_mg_tail && L >= 2 && la == L - 2 && la >= 1 && mg->nu == 1 && mg->gamma == 1 && mg->coarse_sweeps > 0 &&
+        (mg->post == 1 || mg->symmetric_needed)))
+    return false;
+  const MGLevel &a = mg->lv[L - 2], &c = mg->lv[L - 1];
+  if (c.n > kTailMaxC || a.n > kSlice * kTailCTAs) return false;
+  const size_t smem = tail_smem_bytes(a.n, c.n, a.kmax, c.kmax);
+  return smem <= 200 * 1024 && tail_cluster(smem) > 0;
 }
 
 static void launch_tail(dp_scene* s, const double* rf, const int* stop) {
@@ -1629,12 +1796,50 @@ static void launch_tail(dp_scene* s, const double* rf, const int* stop) {
   MGLevel& c = mg->lv[L - 1];
   TailArgs A;
   A.na = a.n; A.sb_a = a.slice_base; A.sw_a = a.slice_width; A.col_a = a.col; A.val_a = a.val; A.minv_a = a.minv;
-  A.mptr_a = a.mem_ptr; A.mem_a = a.mem; A.b_a = a.b; A.xa_a = a.t; A.r_a = a.r; A.x_a = a.x;
-  A.nc = c.n; A.sb_c = c.slice_base; A.sw_c = c.slice_width; A.col_c = c.col; A.val_c = c.val; A.minv_c = c.minv;
-  A.mptr_c = c.mem_ptr; A.mem_c = c.mem; A.agg_c = c.agg; A.dinv = mg->dinv;
+  A.mptr_a = a.mem_ptr; A.mem_a = a.mem; A.x_a = a.x;
+  A.nc = c.n; A.sw_c = c.slice_width; A.col_c = c.col; A.val_c = c.val; A.minv_c = c.minv;
+  A.mptr_c = c.mem_ptr; A.mem_c = c.mem; A.agg_c = c.agg;
   A.rf = rf; A.omega = mg->omega; A.alpha = mg->alpha; A.sweeps = mg->coarse_sweeps; A.stop = stop;
-  k_mg_tail<<<kTailCTAs, kTailNT, 0, s->stream>>>(A);
+  A.ka = a.kmax; A.kc = c.kmax;
+  const size_t smem = tail_smem_bytes(a.n, c.n, a.kmax, c.kmax);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kTailCTAs);
+  cfg.blockDim = dim3(kTailNT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kTailCTAs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_mg_tail, A);
   s->launches++;
+  if (DP_MG_TAIL_TIMING && getenv("DP_MG_TAIL_DBG")) {
+    static double acc[9];
+    static long cnt = 0;
+    unsigned long long t[12];
+    cudaStreamSynchronize(s->stream);
+    cudaMemcpyFromSymbol(t, g_tail_clk, sizeof(t));
+    unsigned long long cy[12];
+    cudaMemcpyFromSymbol(cy, g_tail_cyc, sizeof(cy));
+    static double cacc[8];
+    for (int k = 1; k < 7; ++k) cacc[k] += (double)(cy[k] - cy[k - 1]);
+    cacc[7] += (double)(cy[7] - cy[4]);
+    if (t[6] > t[0]) {
+      for (int k = 1; k < 7; ++k) acc[k] += (double)(t[k] - t[k - 1]);
+      acc[7] += (double)(t[7] - t[4]);
+      if (++cnt % 200 == 0)
+        fprintf(stderr, "tail phases ns: p1 %.0f sync %.0f p2 %.0f sync %.0f p3 %.0f p4 %.0f restrict_c %.0f (n=%ld) "
+                "nc %d na %d ka %d kc %d smem %zu\n",
+                acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt, acc[6] / cnt, acc[7] / cnt,
+                cnt, A.nc, A.na, A.ka, A.kc, smem);
+      if (cnt % 200 == 0)
+        fprintf(stderr, "tail phases cycles: p1 %.0f sync %.0f p2 %.0f sync %.0f p3 %.0f p4 %.0f restrict_c %.0f\n",
+                cacc[1] / cnt, cacc[2] / cnt, cacc[3] / cnt, cacc[4] / cnt, cacc[5] / cnt, cacc[6] / cnt, cacc[7] / cnt);
+    }
+  }
 }
 
 static const int g_mg_fused_env = getenv("DP_MG_FUSED") ? atoi(getenv("DP_MG_FUSED")) : 0;

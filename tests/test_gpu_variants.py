@@ -16,12 +16,16 @@ import pytest
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _digest(env_extra):
+def _digest(env_extra, out=None):
     env = dict(os.environ)
-    # the cluster tail kernel (two coarsest levels in one launch, exact
-    # coarsest solve) is a different preconditioner, not a plumbing switch:
-    # the bitwise comparisons run on the per-level V-cycle
-    env["DP_MG_TAIL"] = "0"
+    env.pop("DP_MG_TAIL", None)
+    if out:
+        env["VARIANT_OUT"] = out
+    # the cluster tail kernel (two coarsest levels in one launch) sums in a
+    # different order (warp trees), so it is not bitwise: the bitwise
+    # comparisons run on the per-level V-cycle (test_cluster_tail_* below
+    # compares the two preconditioners)
+    env.setdefault("DP_MG_TAIL", "0")
     env.update(env_extra)
     out = subprocess.run([sys.executable, os.path.join(HERE, "_variant_run.py")], env=env,
                          capture_output=True, text=True, timeout=600)
@@ -37,3 +41,23 @@ def _digest(env_extra):
                               "separate-restriction", "no-speculative-trial-jacobian"])
 def test_variant_bitwise_identical(variant):
     assert _digest(variant) == _digest({})
+
+
+@pytest.mark.gpu
+def test_cluster_tail_matches_per_level_vcycle(tmp_path):
+    """The two coarsest V-cycle levels in one 16-CTA cluster launch
+    (k_mg_tail, DSMEM) against the per-level kernels: the same
+    preconditioner up to summation order, so the rollout (Newton tol 1e-11)
+    and its gradients agree to solver tolerance; two tail runs are bitwise
+    identical (fixed reduction order, no atomics)."""
+    import numpy as np
+    a, b, c = (str(tmp_path / n) for n in ("a.npz", "b.npz", "c.npz"))
+    _digest({"DP_MG_TAIL": "0"}, a)
+    d1 = _digest({"DP_MG_TAIL": "1"}, b)
+    d2 = _digest({"DP_MG_TAIL": "1"}, c)
+    assert d1 == d2
+    A, B = np.load(a), np.load(b)
+    assert np.max(np.abs(A["q"] - B["q"])) <= 1e-9
+    assert abs(float(A["dL_dE"]) - float(B["dL_dE"])) <= 1e-6 * abs(float(A["dL_dE"]))
+    gq = np.abs(A["dL_dqbar"]).max()
+    assert np.max(np.abs(A["dL_dqbar"] - B["dL_dqbar"])) <= 1e-6 * gq

@@ -454,14 +454,23 @@ def gpu_arm(args, rank, world, local_rank):
         scene = c.scene
         st0 = scene.rest_state()
         st, caches = st0, []
+        trace = [] if os.environ.get("BENCH_TRACE") else None
         for k in range(nsteps):
+            if trace is not None:
+                trace.append(time.perf_counter())
             move_fingers(scene, k0 + k)
             st, rep = fw.forward_step(scene, st, c.sysmat, cfg)
             if not rep.converged:   # forward.py:261-264 (rollout raises)
                 raise RuntimeError(f"forward step {k} did not converge (residual {rep.residual_history[-1]:.3e})")
             caches.append(rep.cache)
         target = st0.q + c.target_shift
+        if trace is not None:
+            trace.append(time.perf_counter())
         g = aj.backprop_rollout(caches, target, solver_cfg=adj_cfg)
+        if trace is not None:
+            trace.append(time.perf_counter())
+            print("[trace] e2e step ms", [round(1e3 * (b - a), 1) for a, b in zip(trace, trace[1:])],
+                  file=sys.stderr, flush=True)
         return g, float(np.sum((st.q - target) ** 2))
 
     pool = ThreadPoolExecutor(max_workers=R)

@@ -29,6 +29,16 @@ from . import _lib
 # state / parameters
 
 
+def _all_finite(a):
+    """np.isfinite(a).all(), fast path: a finite a.a implies finite entries
+    (inf/nan propagate through the BLAS dot, 10x faster than the elementwise
+    test at 0.5M entries); only a non-finite dot (a non-finite entry or an
+    overflow) takes the elementwise test."""
+    with np.errstate(all="ignore"):
+        s = a.dot(a)
+    return bool(np.isfinite(s)) or bool(np.isfinite(a).all())
+
+
 @dataclass
 class SimState:
     """Positions and velocities, flat xyz-interleaved (length 3n)."""
@@ -38,11 +48,13 @@ class SimState:
     step_index: int = 0
 
     def __post_init__(self):
-        self.q = np.array(self.q, dtype=np.float64).reshape(-1)
-        self.v = np.array(self.v, dtype=np.float64).reshape(-1)
+        # no copy (core.py:31-33 np.asarray): a step's page-locked output
+        # arrays stay page-locked as the next step's inputs
+        self.q = np.asarray(self.q, dtype=np.float64).ravel()
+        self.v = np.asarray(self.v, dtype=np.float64).ravel()
         if self.q.size != self.v.size:
             raise ValueError("q and v must have the same length")
-        if not np.isfinite(self.q).all() or not np.isfinite(self.v).all():
+        if not (_all_finite(self.q) and _all_finite(self.v)):
             raise ValueError("non-finite state")
 
     def copy(self):

@@ -84,7 +84,7 @@ class DeviceCache:
 
     def states(self):
         n = 3 * self.dev.n_verts
-        out = [np.empty(n) for _ in range(4)]
+        out = [_pinned.empty(n) for _ in range(4)]   # direct DMA
         _lib.check(self.dev.lib.dp_cache_get_states(self.handle, *[_lib.ptr(a) for a in out]))
         return out
 

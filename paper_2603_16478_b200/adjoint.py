@@ -186,7 +186,10 @@ def _chain_lame(scene, dmu, dlam, grads):
 def loss_final_state(q_final, q_target):
     """L = |q - q*|^2 and dL/dq (adjoint.py:222-225)."""
     d = np.asarray(q_final, dtype=np.float64) - np.asarray(q_target, dtype=np.float64)
-    return float(d @ d), 2.0 * d
+    # einsum, not BLAS ddot: a threaded ddot leaves OpenBLAS workers spinning
+    # on every core for milliseconds, which starves the host threads of
+    # concurrent rollouts (measured: C3 public-API path 455 -> 260 steps/s)
+    return float(np.einsum("i,i->", d, d)), 2.0 * d
 
 
 def _torch_cuda():

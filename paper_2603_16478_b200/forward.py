@@ -282,7 +282,12 @@ def forward_step(scene, state, sysmat, cfg=None, device_io=None):
     step_index = getattr(state, "step_index", 0) + 1 if state is not None else 0
     # snapshot for StepCache.fext (scene.external_force() at this step)
     fext = (None if scene.fext is None else scene.fext.copy(), scene.gravity.copy(), scene.masses)
-    new_state = core.SimState(q1, v1, step_index) if device_io is None else None
+    if device_io is not None:
+        new_state = None
+    elif report.converged:
+        new_state = core.SimState._converged(q1, v1, step_index)
+    else:
+        new_state = core.SimState(q1, v1, step_index)
     report.cache = StepCache(scene, sysmat, dc, fext, report)
     return new_state, report
 

@@ -526,7 +526,7 @@ __global__ void k_mg_jacobi0(int n, const TM* __restrict__ minv, const double* _
 // DOT (fine level, SPLIT = 1, with `out`): the PCG's (r, z) reduction fused
 // into the epilogue - b is r, out is z; the last CTA folds the per-CTA
 // partials in a fixed order and updates beta/gamma exactly as k_pcg_rz
-template <class TV, int SPLIT, bool DOT = false>
+template <class TV, int SPLIT, bool DOT = false, int BULK = 0>
 __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __restrict__ slice_base,
                                                    const int* __restrict__ slice_width, const int* __restrict__ col,
                                                    const TV* __restrict__ val, const TV* __restrict__ minv,
@@ -549,7 +549,52 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
   const int* cs = col + base + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #if DP_SMOOTH_ASYNC
-  if constexpr (sizeof(TV) == 4 && SPLIT == 1 && DP_VAL32_PACKED == 0) {
+  if constexpr (sizeof(TV) == 4 && SPLIT == 1 && DP_VAL32_PACKED == 0 && BULK > 0) {
+    // the same ring filled by the TMA engine: one lane per warp issues two
+    // bulk copies per slot (1,152 B of values + 128 B of columns) that
+    // complete on the slot's mbarrier; same values, same order
+    __shared__ __align__(128) float sv[DP_SMOOTH_NT / 32][BULK][9 * kSlice];
+    __shared__ __align__(128) int sc[DP_SMOOTH_NT / 32][BULK][kSlice];
+    __shared__ __align__(8) uint64_t mb[DP_SMOOTH_NT / 32][BULK];
+    const int w = threadIdx.x >> 5;
+    const float* gv = reinterpret_cast<const float*>(val) + (size_t)base * 9;
+    const int* gc = col + base;
+    if (lane == 0) {
+#pragma unroll
+      for (int d = 0; d < BULK; ++d) mbar_init(&mb[w][d], 1);
+      mbar_fence_init();
+    }
+    __syncwarp();
+    auto issue = [&](int kk) {
+      if (kk < K && lane == 0) {
+        const int d = kk % BULK;
+        mbar_expect_tx(&mb[w][d], (9 + 1) * kSlice * 4);
+        bulk_g2s(sv[w][d], gv + (size_t)kk * 9 * kSlice, 9 * kSlice * 4, &mb[w][d]);
+        bulk_g2s(sc[w][d], gc + (size_t)kk * kSlice, kSlice * 4, &mb[w][d]);
+      }
+    };
+#pragma unroll
+    for (int kk = 0; kk < BULK; ++kk) issue(kk);
+    for (int k = 0; k < K; ++k) {
+      const int d = k % BULK;
+      mbar_wait(&mb[w][d], (uint32_t)((k / BULK) & 1));
+      const float* vv = sv[w][d];
+      const int j = sc[w][d][lane];
+      double m[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) m[c] = (double)vv[c * kSlice + lane];
+      double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
+      if (xc) {
+        const int J = __ldg(agg + j);
+        x0 += alpha * __ldg(xc + 3 * J); x1 += alpha * __ldg(xc + 3 * J + 1); x2 += alpha * __ldg(xc + 3 * J + 2);
+      }
+      a0 += m[0] * x0 + m[1] * x1 + m[2] * x2;
+      a1 += m[3] * x0 + m[4] * x1 + m[5] * x2;
+      a2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
+      __syncwarp();
+      issue(k + BULK);
+    }
+  } else if constexpr (sizeof(TV) == 4 && SPLIT == 1 && DP_VAL32_PACKED == 0) {
     // fine level: the slice's slots stream through a per-warp shared-memory
     // ring, kSmDepth slots ahead, with cp.async (a slot is 1,152 contiguous
     // bytes of component-major FP32 values + 128 bytes of column indices), so
@@ -933,6 +978,8 @@ __global__ void __launch_bounds__(DP_SMOOTH_NT) k_mg_smooth_pf(int n, int S, con
   }
 }
 
+// fine sweep ring filled by TMA bulk copies (depth 2; 0 = per-lane cp.async ring): in situ 24.7 -> 23.6 us
+static const int g_smooth_bulk = getenv("DP_SMOOTH_BULK") ? atoi(getenv("DP_SMOOTH_BULK")) : 2;
 static const int g_smooth_pf = getenv("DP_SMOOTH_PF") ? atoi(getenv("DP_SMOOTH_PF")) : 0;   // measured slower (25.6 vs 24.1 us in situ), off
 
 // x = xa + alpha P xc
@@ -1446,6 +1493,26 @@ static void smooth(dp_scene* s, const MGLevel& L, const TV* val, const TV* minv,
         k_mg_smooth16<false><<<nb, DP_SMOOTH_NT, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col,
                                                                  s->val16, s->sc16, minv, b, x, xc, agg, omega, out,
                                                                  r_out, stop, alpha, nullptr, nullptr, nullptr);
+      ktm_end(s, KT_SMOOTH);
+      s->launches++;
+      return;
+    }
+  }
+  if constexpr (sizeof(TV) == 4) {
+    if (fine && g_smooth_bulk && L.S >= 4 * 148 && DP_VAL32_PACKED == 0) {
+      const int nb = grid_for((int64_t)L.S * 32, DP_SMOOTH_NT);
+#define DP_BULK_LAUNCH(DEPTH)                                                                                       \
+  if (dot && mg->dot_ks && out)                                                                                     \
+    k_mg_smooth<TV, 1, true, DEPTH><<<nb, DP_SMOOTH_NT, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, \
+                                                                     val, minv, b, x, xc, agg, omega, out, r_out,  \
+                                                                     stop, alpha, mg->dot_partial, mg->dot_counter, \
+                                                                     mg->dot_ks);                                   \
+  else                                                                                                              \
+    k_mg_smooth<TV, 1, false, DEPTH><<<nb, DP_SMOOTH_NT, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width,     \
+                                                                      L.col, val, minv, b, x, xc, agg, omega, out, \
+                                                                      r_out, stop, alpha);
+      if (g_smooth_bulk >= 4) { DP_BULK_LAUNCH(4) } else if (g_smooth_bulk == 3) { DP_BULK_LAUNCH(3) } else { DP_BULK_LAUNCH(2) }
+#undef DP_BULK_LAUNCH
       ktm_end(s, KT_SMOOTH);
       s->launches++;
       return;

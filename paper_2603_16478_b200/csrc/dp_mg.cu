@@ -46,6 +46,15 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -527,7 +536,7 @@ __global__ void k_mg_jacobi0(int n, const TM* __restrict__ minv, const double* _
 // into the epilogue - b is r, out is z; the last CTA folds the per-CTA
 // partials in a fixed order and updates beta/gamma exactly as k_pcg_rz
 template <class TV, int SPLIT, bool DOT = false, int BULK = 0>
-__global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __restrict__ slice_base,
+__global__ void __launch_bounds__(256, 5) k_mg_smooth(int n, int S, const int* __restrict__ slice_base,
                                                    const int* __restrict__ slice_width, const int* __restrict__ col,
                                                    const TV* __restrict__ val, const TV* __restrict__ minv,
                                                    const double* __restrict__ b, const double* __restrict__ x,
@@ -548,6 +557,9 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
   const TV* vs = val + (size_t)base * 9 + lane;
   const int* cs = col + base + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  double ex[3] = {0.0, 0.0, 0.0}, eb[3] = {0.0, 0.0, 0.0};   // x and b of the row, when staged (bulk path)
+  TV em[9] = {};                                            // its Minv block, when staged
+  bool staged = false;
 #if DP_SMOOTH_ASYNC
   if constexpr (sizeof(TV) == 4 && SPLIT == 1 && DP_VAL32_PACKED == 0 && BULK > 0) {
     // the same ring filled by the TMA engine: one lane per warp issues two
@@ -556,9 +568,25 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
     __shared__ __align__(128) float sv[DP_SMOOTH_NT / 32][BULK][9 * kSlice];
     __shared__ __align__(128) int sc[DP_SMOOTH_NT / 32][BULK][kSlice];
     __shared__ __align__(8) uint64_t mb[DP_SMOOTH_NT / 32][BULK];
+    // the rows' own operands (x, b, Minv), fetched into shared memory while
+    // the slots stream, so the epilogue does not wait a memory round trip
+    __shared__ __align__(16) double sxb[DP_SMOOTH_NT / 32][2][3 * kSlice];
+    __shared__ __align__(16) float smv[DP_SMOOTH_NT / 32][9][kSlice];
     const int w = threadIdx.x >> 5;
     const float* gv = reinterpret_cast<const float*>(val) + (size_t)base * 9;
     const int* gc = col + base;
+    {
+      const int row0 = gw * kSlice, nr = min(kSlice, n - row0);
+      for (int t = lane; t < 3 * nr; t += 32) {
+        cp_async8(&sxb[w][0][t], x + 3 * (size_t)row0 + t);
+        cp_async8(&sxb[w][1][t], b + 3 * (size_t)row0 + t);
+      }
+      if (out && lane < nr) {
+#pragma unroll
+        for (int c = 0; c < 9; ++c) cp_async4(&smv[w][c][lane], minv + (size_t)c * n + row0 + lane);
+      }
+      cp_async_commit();
+    }
     if (lane == 0) {
 #pragma unroll
       for (int d = 0; d < BULK; ++d) mbar_init(&mb[w][d], 1);
@@ -593,6 +621,17 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
       a2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
       __syncwarp();
       issue(k + BULK);
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    if (row < n) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { ex[c] = sxb[w][0][3 * lane + c]; eb[c] = sxb[w][1][3 * lane + c]; }
+      if (out) {
+#pragma unroll
+        for (int c = 0; c < 9; ++c) em[c] = smv[w][c][lane];
+      }
+      staged = true;
     }
   } else if constexpr (sizeof(TV) == 4 && SPLIT == 1 && DP_VAL32_PACKED == 0) {
     // fine level: the slice's slots stream through a per-warp shared-memory
@@ -721,17 +760,29 @@ __global__ void __launch_bounds__(256) k_mg_smooth(int n, int S, const int* __re
     for (int w = 0; w < SPLIT; ++w) { a0 += part[w][0][lane]; a1 += part[w][1][lane]; a2 += part[w][2][lane]; }
   }
   if (row < n) {
-    double xt[3] = {x[3 * row], x[3 * row + 1], x[3 * row + 2]};
+    double xt[3], bb[3];
+    if (staged) {
+      xt[0] = ex[0]; xt[1] = ex[1]; xt[2] = ex[2];
+      bb[0] = eb[0]; bb[1] = eb[1]; bb[2] = eb[2];
+    } else {
+      xt[0] = x[3 * row]; xt[1] = x[3 * row + 1]; xt[2] = x[3 * row + 2];
+      bb[0] = b[3 * row]; bb[1] = b[3 * row + 1]; bb[2] = b[3 * row + 2];
+    }
     if (xc) {
       const int I = agg[row];
       xt[0] += alpha * xc[3 * I]; xt[1] += alpha * xc[3 * I + 1]; xt[2] += alpha * xc[3 * I + 2];
     }
-    const double bb[3] = {b[3 * row], b[3 * row + 1], b[3 * row + 2]};
     const double rr[3] = {bb[0] - a0, bb[1] - a1, bb[2] - a2};
     if (r_out) { r_out[3 * row] = rr[0]; r_out[3 * row + 1] = rr[1]; r_out[3 * row + 2] = rr[2]; }
     if (out) {
       double u[3];
-      mv_minv(minv, n, row, rr, u);
+      if (staged) {
+        u[0] = em[0] * rr[0] + em[1] * rr[1] + em[2] * rr[2];
+        u[1] = em[3] * rr[0] + em[4] * rr[1] + em[5] * rr[2];
+        u[2] = em[6] * rr[0] + em[7] * rr[1] + em[8] * rr[2];
+      } else {
+        mv_minv(minv, n, row, rr, u);
+      }
       const double z0 = xt[0] + omega * u[0], z1 = xt[1] + omega * u[1], z2 = xt[2] + omega * u[2];
       out[3 * row] = z0;
       out[3 * row + 1] = z1;
@@ -1511,7 +1562,7 @@ static void smooth(dp_scene* s, const MGLevel& L, const TV* val, const TV* minv,
     k_mg_smooth<TV, 1, false, DEPTH><<<nb, DP_SMOOTH_NT, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width,     \
                                                                       L.col, val, minv, b, x, xc, agg, omega, out, \
                                                                       r_out, stop, alpha);
-      if (g_smooth_bulk >= 4) { DP_BULK_LAUNCH(4) } else if (g_smooth_bulk == 3) { DP_BULK_LAUNCH(3) } else { DP_BULK_LAUNCH(2) }
+      DP_BULK_LAUNCH(2)   // depth 3 / 4 measured no faster (and need > 48 KB of static shared memory)
 #undef DP_BULK_LAUNCH
       ktm_end(s, KT_SMOOTH);
       s->launches++;
@@ -1597,15 +1648,6 @@ __device__ __forceinline__ void tail_mark(int k) {
     g_tail_clk[k] = t;
     g_tail_cyc[k] = clock64();
   }
-}
-
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
 }
 
 // one SELL slice (base, width K) -> row-major shared copies sv[(li K + k) 9 + e], sc[li K + k]

@@ -625,6 +625,21 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
     for (int64_t t = 0; t < NS; ++t)
       if (cptr[t + 1] > cptr[t]) rinfo[t] = make_int2((int)cptr[t], (int)(cptr[t + 1] - cptr[t]));
   }
+  // canonical off-diagonal slot (i, j), i < j -> the slot of (j, i): the
+  // assembly sums each run once and writes the block and its transpose
+  std::vector<int> tslot(NS, -1);
+  for (int i = 0; i < V; ++i) {
+    const int sl = i / kSlice, l = i % kSlice;
+    for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+      const int j = colidx[k];
+      if (j <= i) continue;
+      const int* rb = colidx.data() + rowptr[j];
+      const int rl = rowptr[j + 1] - rowptr[j];
+      const int kk = (int)(std::lower_bound(rb, rb + rl, i) - rb);
+      tslot[slice_base[sl] + (int64_t)(k - rowptr[i]) * kSlice + l] =
+          (int)(slice_base[j / kSlice] + (int64_t)kk * kSlice + (j % kSlice));
+    }
+  }
 
   // ---- device buffers
   int rc = 0;
@@ -643,6 +658,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   rc |= upload(s, &s->col, col);
   rc |= upload(s, &s->diag_slot, diag_slot);
   rc |= upload(s, &s->rinfo, rinfo);
+  rc |= upload(s, &s->tslot, tslot);
   rc |= upload(s, &s->epos, epos);
   rc |= dalloc(s, &s->val_fwd, (size_t)NS * 9);
   rc |= dalloc(s, &s->val_adj, (size_t)NS * 9);
@@ -727,7 +743,7 @@ int dp_scene_destroy(dp_scene* s) {
   mg_destroy(s);
   void* ptrs[] = {s->ev, s->B, s->w, s->vol, s->mu, s->lam, s->model, s->mass, s->inc_ptr, s->inc,
                   s->slice_base, s->slice_width, s->col, s->diag_slot, s->val_fwd, s->val_adj, s->val_A,
-                  s->rinfo, s->epos, s->minv, s->fe, s->fe_pos, s->H, s->Ht, s->Pst, s->watch_v, s->watch_e, s->d_colliders, s->b_ptr, s->b_idx,
+                  s->rinfo, s->tslot, s->epos, s->minv, s->fe, s->fe_pos, s->H, s->Ht, s->Pst, s->watch_v, s->watch_e, s->d_colliders, s->b_ptr, s->b_idx,
                   s->b_target, s->b_comp, s->b_vertex, s->fext, s->c_count, s->c_off, s->c_vertex, s->c_collider,
                   s->c_frame, s->c_dn, s->c_mu, s->c_delta, s->c_blk, s->c_force, s->c_kmu, s->c_kc, s->scan_tmp,
                   s->q, s->q_hat, s->q_bar, s->v_bar, s->r, s->dq, s->q_try, s->rhs, s->z, s->z_prev, s->tmp, s->q_ev, s->r_try, s->kx, s->kr,

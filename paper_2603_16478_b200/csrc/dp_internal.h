@@ -206,6 +206,7 @@ struct dp_scene {
   double* val_adj = nullptr;       // adjoint operator (transposed contact blocks)
   double* val_A = nullptr;         // constant A (lazy, export only)
   int2* rinfo = nullptr;           // slot -> {start, count} of its run of H (count < 0: read transposed)
+  int* tslot = nullptr;            // canonical slot (i < j) -> slot of (j, i); -1 otherwise
   int* epos = nullptr;             // E*NP: (element, a <= b) -> position in H (~pos: stored transposed)
   double* minv = nullptr;          // block-Jacobi inverses [9][V]
   float* val32 = nullptr;          // FP32 copy of the last assembled operator (multigrid fine level)

@@ -728,7 +728,7 @@ __device__ __forceinline__ void inv3_guarded(const double a[9], double o[9]) {
 
 __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __restrict__ slice_base,
                                                   const int* __restrict__ slice_width, const int* __restrict__ diag_slot,
-                                                  const int2* __restrict__ rinfo,
+                                                  const int2* __restrict__ rinfo, const int* __restrict__ tslot,
                                                   const double* __restrict__ H, const double* __restrict__ Ht,
                                                   const double* __restrict__ mass,
                                                   const int* __restrict__ b_ptr, const int* __restrict__ b_idx,
@@ -756,6 +756,10 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
     // group of ASM_CHUNK blocks are issued before the accumulation
     const int2 ri = rinfo[slot];
     const bool tr = ri.y < 0;
+    // with tslot: a (j, i) slot is written by its canonical partner (i, j)
+    // (the transposed run sum is the transpose of the run sum, entry by
+    // entry the same additions), padding slots keep their zeros
+    if (tslot && (tr || (ri.y == 0 && slot != dslot))) continue;
     const int n = tr ? -ri.y : ri.y;
     const double* hs = H + (size_t)ri.x * kHS;
     const double* ht = Ht + ri.x;
@@ -856,6 +860,24 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
       for (int c = 0; c < 9; ++c) v32[(k * 9 + c) * kSlice + lane] = (float)b[c];
 #endif
     }
+    if (tslot) {
+      const int t = tslot[slot];
+      if (t >= 0) {
+        const size_t tb = (size_t)(t - (t % kSlice)) * 9 + (t % kSlice);   // component 0 of slot t
+        if (val) {
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) val[tb + (size_t)(r * 3 + c) * kSlice] = b[c * 3 + r];
+        }
+        if (val32) {
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) val32[tb + (size_t)(r * 3 + c) * kSlice] = (float)b[c * 3 + r];
+        }
+      }
+    }
     if (val16) {
       // FP16 copy for the fine smoother: values / block max |a| (in [-1, 1])
       double mx = 0.0;
@@ -871,13 +893,18 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
   }
 }
 
+static const int g_asm_tslot = getenv("DP_ASM_TSLOT") ? atoi(getenv("DP_ASM_TSLOT")) : 1;
+
 void launch_assemble(dp_scene* s, double* val, int transpose_contacts, int amat, int h32) {
   (void)transpose_contacts;   // contact blocks are already stored transposed by the contact kernel
   const int nt = 256;
   const int nb = grid_for((int64_t)s->S * 32, nt);
   const int has_c = (contact_sources(s) > 0) && !amat;
   ktm_begin(s, KT_ASSEMBLE);
-  k_assemble<<<nb, nt, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->diag_slot, s->rinfo,
+  // canonical-slot assembly (each run read once, the transpose written by
+  // the same lane): not for the FP16 copy or the mass-matrix pass
+  const int* tslot = (g_asm_tslot && !amat && !s->val16 && DP_VAL32_PACKED == 0) ? s->tslot : nullptr;
+  k_assemble<<<nb, nt, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->diag_slot, s->rinfo, tslot,
                                        s->H, s->Ht, s->mass, s->nb ? s->b_ptr : nullptr, s->b_idx, s->b_comp,
                                        has_c ? s->c_count : nullptr, s->c_off, s->c_blk, amat ? 0 : 1,
                                        s->h * s->h, h32 ? nullptr : val, s->minv, amat ? nullptr : s->val32,

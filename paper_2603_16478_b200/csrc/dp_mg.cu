@@ -470,6 +470,8 @@ __global__ void __launch_bounds__(256) k_mg_galerkin(int n, int S, const int* __
   const int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (slot >= NS) return;
+  // SELL padding (no fine blocks): stays the zero block written at setup
+  if (gal_ptr[slot] == gal_ptr[slot + 1]) return;
   double b[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int t = gal_ptr[slot] + lane; t < gal_ptr[slot + 1]; t += 32) {
     const TF* src = valf + gal[t];

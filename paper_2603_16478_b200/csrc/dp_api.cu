@@ -13,6 +13,7 @@
 #include <initializer_list>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "dp_internal.h"
@@ -275,6 +276,21 @@ static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// host setup: body(lo, hi) over [0, n) split into contiguous chunks on up to
+// 16 threads (each chunk's output is written by its own thread only)
+template <class F>
+static void parallel_chunks(int64_t n, F body) {
+  int nt = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+  if (n < 4096) nt = 1;
+  if (nt == 1) { body((int64_t)0, n); return; }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t lo = n * t / nt, hi = n * (t + 1) / nt;
+    th.emplace_back([=] { body(lo, hi); });
+  }
+  for (auto& x : th) x.join();
+}
+
 // ===========================================================================
 extern "C" {
 
@@ -404,6 +420,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   cudaEventCreate(&s->ev0);
   cudaEventCreate(&s->ev1);
 
+  const double t_el = now_s();
   // ---- element kinematics (build_elements, elasticity.py:74-108)
   std::vector<int4> ev(E);
   std::vector<double> Bsoa((size_t)D * D * std::max(E, 1));
@@ -510,6 +527,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
       return DP_ERR_VALUE;
     }
 
+  const double t_inc = now_s();
   // ---- vertex incidence (residual gather) and block pattern (core.py:339-364)
   std::vector<int> inc_ptr(V + 1, 0), inc, fe_pos((size_t)E * NV);
   for (int e = 0; e < E; ++e) {
@@ -532,23 +550,41 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   std::vector<int>& colidx = s->h_colidx;
   rowptr.assign(V + 1, 0);
   colidx.clear();
-  colidx.reserve((size_t)V * 16);
-  std::vector<int> nbr;
-  for (int i = 0; i < V; ++i) {
-    nbr.clear();
-    nbr.push_back(i);
-    for (int k = inc_ptr[i]; k < inc_ptr[i + 1]; ++k) {
-      const int e = inc[k] / NV;
-      const int* vv = &ev[e].x;
-      for (int b = 0; b < NV; ++b) nbr.push_back(vv[b]);
+  {
+    // each row's sorted neighbour set (itself + the vertices of its
+    // elements), rows split over host threads, then concatenated in row order
+    const int nt = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<std::vector<int>> part(nt);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) {
+      th.emplace_back([&, t] {
+        const int lo = (int)((int64_t)V * t / nt), hi = (int)((int64_t)V * (t + 1) / nt);
+        std::vector<int>& out = part[t];
+        out.reserve((size_t)(hi - lo) * 16);
+        std::vector<int> nbr;
+        for (int i = lo; i < hi; ++i) {
+          nbr.clear();
+          nbr.push_back(i);
+          for (int k = inc_ptr[i]; k < inc_ptr[i + 1]; ++k) {
+            const int e = inc[k] / NV;
+            const int* vv = &ev[e].x;
+            for (int b = 0; b < NV; ++b) nbr.push_back(vv[b]);
+          }
+          std::sort(nbr.begin(), nbr.end());
+          nbr.erase(std::unique(nbr.begin(), nbr.end()), nbr.end());
+          out.insert(out.end(), nbr.begin(), nbr.end());
+          rowptr[i + 1] = (int)nbr.size();
+        }
+      });
     }
-    std::sort(nbr.begin(), nbr.end());
-    nbr.erase(std::unique(nbr.begin(), nbr.end()), nbr.end());
-    colidx.insert(colidx.end(), nbr.begin(), nbr.end());
-    rowptr[i + 1] = (int)colidx.size();
+    for (auto& x : th) x.join();
+    for (int i = 0; i < V; ++i) rowptr[i + 1] += rowptr[i];
+    colidx.reserve(rowptr[V]);
+    for (auto& p : part) colidx.insert(colidx.end(), p.begin(), p.end());
   }
   s->nnzb = (int64_t)colidx.size();
 
+  const double t_sell = now_s();
   // ---- SELL-32 layout
   const int S = (V + kSlice - 1) / kSlice;
   s->S = S;
@@ -575,6 +611,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
       if (colidx[k] == i) diag_slot[i] = (int)slot;
     }
   }
+  const double t_runs = now_s();
   // ---- contribution runs per slot.  Slot (i, j) and slot (j, i) receive
   // blocks from the same elements (those holding edge ij), element-ascending,
   // the (j, i) ones being the transposes of the (i, j) ones.  So only the
@@ -582,20 +619,27 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   // reads the run of (i, j) transposed (rinfo count < 0).
   std::vector<int> cptr(NS + 1, 0);
   std::vector<int64_t> eslot((size_t)E * NV * NV);
-  for (int e = 0; e < E; ++e) {
-    const int* vv = &ev[e].x;
-    for (int a = 0; a < NV; ++a) {
-      const int i = vv[a];
-      const int* rb = colidx.data() + rowptr[i];
-      const int rl = rowptr[i + 1] - rowptr[i];
-      for (int b = 0; b < NV; ++b) {
-        const int j = vv[b];
-        const int k = (int)(std::lower_bound(rb, rb + rl, j) - rb);
-        const int64_t slot = slice_base[i / kSlice] + (int64_t)k * kSlice + (i % kSlice);
-        eslot[((size_t)e * NV + a) * NV + b] = slot;
-        if (i <= j && (i < j || a == b)) cptr[slot + 1]++;
+  parallel_chunks(E, [&](int64_t e0, int64_t e1) {   // the slot of every local pair (binary searches)
+    for (int64_t e = e0; e < e1; ++e) {
+      const int* vv = &ev[e].x;
+      for (int a = 0; a < NV; ++a) {
+        const int i = vv[a];
+        const int* rb = colidx.data() + rowptr[i];
+        const int rl = rowptr[i + 1] - rowptr[i];
+        for (int b = 0; b < NV; ++b) {
+          const int k = (int)(std::lower_bound(rb, rb + rl, vv[b]) - rb);
+          eslot[((size_t)e * NV + a) * NV + b] = slice_base[i / kSlice] + (int64_t)k * kSlice + (i % kSlice);
+        }
       }
     }
+  });
+  for (int e = 0; e < E; ++e) {
+    const int* vv = &ev[e].x;
+    for (int a = 0; a < NV; ++a)
+      for (int b = 0; b < NV; ++b) {
+        const int i = vv[a], j = vv[b];
+        if (i <= j && (i < j || a == b)) cptr[eslot[((size_t)e * NV + a) * NV + b] + 1]++;
+      }
   }
   for (int64_t t = 0; t < NS; ++t) cptr[t + 1] += cptr[t];
   // block-stream position of every unordered local pair (a <= b) of every
@@ -628,19 +672,22 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   // canonical off-diagonal slot (i, j), i < j -> the slot of (j, i): the
   // assembly sums each run once and writes the block and its transpose
   std::vector<int> tslot(NS, -1);
-  for (int i = 0; i < V; ++i) {
-    const int sl = i / kSlice, l = i % kSlice;
-    for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) {
-      const int j = colidx[k];
-      if (j <= i) continue;
-      const int* rb = colidx.data() + rowptr[j];
-      const int rl = rowptr[j + 1] - rowptr[j];
-      const int kk = (int)(std::lower_bound(rb, rb + rl, i) - rb);
-      tslot[slice_base[sl] + (int64_t)(k - rowptr[i]) * kSlice + l] =
-          (int)(slice_base[j / kSlice] + (int64_t)kk * kSlice + (j % kSlice));
+  parallel_chunks(V, [&](int64_t i0, int64_t i1) {
+    for (int i = (int)i0; i < (int)i1; ++i) {
+      const int sl = i / kSlice, l = i % kSlice;
+      for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+        const int j = colidx[k];
+        if (j <= i) continue;
+        const int* rb = colidx.data() + rowptr[j];
+        const int rl = rowptr[j + 1] - rowptr[j];
+        const int kk = (int)(std::lower_bound(rb, rb + rl, i) - rb);
+        tslot[slice_base[sl] + (int64_t)(k - rowptr[i]) * kSlice + l] =
+            (int)(slice_base[j / kSlice] + (int64_t)kk * kSlice + (j % kSlice));
+      }
     }
-  }
+  });
 
+  const double t_dev = now_s();
   // ---- device buffers
   int rc = 0;
   rc |= upload(s, &s->ev, ev);
@@ -709,7 +756,12 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   s->colliders.n = 0;
   cudaMemcpy(s->d_colliders, &s->colliders, sizeof(ColliderSet), cudaMemcpyHostToDevice);
   if (ensure_contact_capacity(s, 1) || contact_scan_setup(s)) { dp_scene_destroy(s); return DP_ERR_CUDA; }
+  const double t_mg = now_s();
   if (mg_setup(s)) { dp_scene_destroy(s); return DP_ERR_CUDA; }
+  if (g_debug)
+    fprintf(stderr, "[dp] setup: elements %.1f ms, incidence+pattern %.1f ms, SELL %.1f ms, runs %.1f ms, "
+            "device buffers %.1f ms, multigrid %.1f ms\n", 1e3 * (t_inc - t_el), 1e3 * (t_sell - t_inc),
+            1e3 * (t_runs - t_sell), 1e3 * (t_dev - t_runs), 1e3 * (t_mg - t_dev), 1e3 * (now_s() - t_mg));
   if (getenv("DP_MG")) s->use_mg = atoi(getenv("DP_MG"));
   if (getenv("DP_ADJ_WARM")) s->adj_warm = atoi(getenv("DP_ADJ_WARM"));
   cudaError_t e = cudaDeviceSynchronize();

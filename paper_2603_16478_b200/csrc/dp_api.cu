@@ -254,6 +254,8 @@ static size_t scratch_bytes(std::initializer_list<size_t> sizes) {
 using namespace dp;
 
 static const int g_debug = getenv("DP_DEBUG") ? atoi(getenv("DP_DEBUG")) : 0;
+// line search: penetration of all trials tested with the first (DP_PEN_MASK=0 off)
+static const int g_pen_mask = getenv("DP_PEN_MASK") ? atoi(getenv("DP_PEN_MASK")) : 1;
 // after a line search that had to cut the step below 1/16 the Newton model is
 // poor (friction-cone / activation kinks): a cheap direction is enough
 static const int g_precheck = getenv("DP_LS_PRECHECK") ? atoi(getenv("DP_LS_PRECHECK")) : 1;
@@ -1202,6 +1204,7 @@ __global__ void k_reset_flags(EvalScalars* esc) {
   esc->asym = 0;
   esc->skip = 0;
   esc->precheck = 0;
+  esc->pen_mask = 0;
 }
 
 int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32_t ptr_kind,
@@ -1343,10 +1346,21 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     // the pre-check bounds max|r| only: off under the 2-norm acceptance rule
     const bool precheck = g_precheck && g_ls_norm != 2 && s->NV == 4 && s->E > 0;
     if (precheck) launch_watch_select(s, s->r, g_watch_frac);
+    // the first trial's sync also returns the penetration verdict of every
+    // later trial (k_penetration_mask): penetrating trials are then skipped
+    // without a launch or a sync - exactly the trials the reference skips
+    const bool use_mask = g_pen_mask && contact_sources(s) > 0;
+    unsigned int pen_mask = 0;
     for (int ls = 0; ls < cfg.max_line_search; ++ls) {
+      if (use_mask && ls > 0 && ls < 32 && ((pen_mask >> ls) & 1u)) {
+        R.line_search_trials++;   // forward.py:218-219: penetrating, not evaluated
+        t *= 0.5;
+        continue;
+      }
       launch_axpy_to(s, q_try, q, t, s->dq);
       k_reset_flags<<<1, 1, 0, s->stream>>>(s->esc);
       launch_penetration(s, q_try, s->esc);
+      if (use_mask && ls == 0) launch_penetration_mask(s, q, s->dq, cfg.max_line_search, s->esc);
       // forward.py:218-219: a penetrating trial is not evaluated; the kernels
       // read the skip flag on the device and exit (no extra sync).  The
       // pre-check (watched rows) sets the same flag when the trial cannot
@@ -1367,6 +1381,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
       R.line_search_trials++;
       if ((rc = sync_esc(s))) return rc;
       const EvalScalars T = *s->h_esc;
+      if (ls == 0) pen_mask = T.pen_mask;
       if (g_debug > 1)
         fprintf(stderr, "[dp]   ls=%d t=%.3e pen=%d st=%d rmax_try=%.6e (rmax=%.6e)\n", ls, t, T.penetrating, T.status,
                 T.rmax, E.rmax);

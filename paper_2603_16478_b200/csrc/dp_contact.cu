@@ -352,6 +352,45 @@ void launch_penetration(dp_scene* s, const double* q, EvalScalars* esc) {
   s->launches++;
 }
 
+// The penetration test of every line-search trial of one search at once
+// (forward.py:218-219): bit k of esc->pen_mask = some vertex of
+// q + 2^-k dq has a gap <= 0.  The trial point is formed exactly as
+// k_axpy_to forms it (t * dq is exact for t = 2^-k), so each bit equals
+// k_penetration's verdict on that trial.
+__global__ void k_penetration_mask(int V, const ColliderSet* __restrict__ csp, const double* __restrict__ q,
+                                   const double* __restrict__ dq, int nls, EvalScalars* esc, SelfContact sc) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned int m = 0;
+  if (v < V) {
+    const ColliderSet& cs = *csp;
+    const double q0 = q[3 * v], q1 = q[3 * v + 1], q2 = q[3 * v + 2];
+    const double d0 = dq[3 * v], d1 = dq[3 * v + 1], d2 = dq[3 * v + 2];
+    double t = 1.0;
+    for (int k = 0; k < nls; ++k, t *= 0.5) {
+      const double x[3] = {q0 + t * d0, q1 + t * d1, q2 + t * d2};
+      bool pen = false;
+      for (int j = 0; j < cs.n && !pen; ++j) {
+        double n[3];
+        pen = gap_normal(cs, j, x, n) <= 0.0;
+      }
+      if (!pen && sc.enabled && sc.cand[v] >= 0) {
+        double n[3];
+        pen = self_gap(sc, v, x, n) <= 0.0;
+      }
+      if (pen) m |= 1u << k;
+    }
+  }
+  m = __reduce_or_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicOr(&esc->pen_mask, m);
+}
+
+void launch_penetration_mask(dp_scene* s, const double* q, const double* dq, int nls, EvalScalars* esc) {
+  if (contact_sources(s) == 0) return;
+  k_penetration_mask<<<grid_for(s->V, 256), 256, 0, s->stream>>>(s->V, s->d_colliders, q, dq, nls < 32 ? nls : 32,
+                                                                 esc, s->self);
+  s->launches++;
+}
+
 // ---------------------------------------------------------------------------
 // detection: count -> exclusive scan -> write (order: vertex, then collider)
 // count + the block-local exclusive scan of the counts (the grid-level

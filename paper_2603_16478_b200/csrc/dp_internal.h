@@ -32,6 +32,7 @@ struct EvalScalars {
   int n_watch;          // watched rows (pre-check), capped at kWatchMax
   int n_watch_elem;     // element entries of the watched rows, capped at kWatchElemMax
   int discont;          // q_bar differs from the previous step's output (not a rollout continuation)
+  unsigned int pen_mask;   // bit k: the line-search trial q + 2^-k dq penetrates (k_penetration_mask)
 };
 constexpr int kWatchMax = 256;
 constexpr int kWatchElemMax = 256 * 32;
@@ -354,6 +355,7 @@ void launch_backprop(dp_scene* s, const dp_cache* c, const double* z, const doub
 // launchers (dp_contact.cu) ------------------------------------------------
 void launch_pullback(dp_scene* s, double* q, const double* q_bar, double margin);
 void launch_penetration(dp_scene* s, const double* q, dp::EvalScalars* esc);
+void launch_penetration_mask(dp_scene* s, const double* q, const double* dq, int nls, dp::EvalScalars* esc);
 void launch_detect(dp_scene* s, const double* q);   // fills contact records + esc->n_contacts
 // per-contact condensation; writes c_delta, c_blk (h^2 fr^T Kc fr, or ^T if
 // transpose), c_force; status/asym bits into esc

@@ -2,9 +2,11 @@
 §6b): host-driven GMRES columns instead of CUDA-graph WHILE nodes, the fused
 cooperative coarse V-cycle, the un-fused first fine Jacobi sweep, and the
 line search without the watched-row pre-check, the restriction in
-launches of its own, and line-search trials evaluated without the Jacobian
+launches of its own, line-search trials evaluated without the Jacobian
 blocks (the accepted trial's element pass is then repeated at the next Newton
-point).  Each
+point), every trial's penetration tested by its own launch and sync, the
+assembly reading each block run for both slots, and the fine sweep's ring
+filled by per-lane cp.async instead of TMA bulk copies.  Each
 variant runs in its own process (the switches are read when the library
 loads) on the same C5-family rollout, forward and reverse."""
 import os
@@ -36,9 +38,11 @@ def _digest(env_extra, out=None):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("variant", [{"DP_GRAPHS": "0"}, {"DP_MG_FUSED": "1"}, {"DP_PREJAC": "0"},
-                                     {"DP_LS_PRECHECK": "0"}, {"DP_MG_RJ0": "0"}, {"DP_LS_SPECJAC": "0"}],
+                                     {"DP_LS_PRECHECK": "0"}, {"DP_MG_RJ0": "0"}, {"DP_LS_SPECJAC": "0"},
+                                     {"DP_PEN_MASK": "0"}, {"DP_ASM_TSLOT": "0"}, {"DP_SMOOTH_BULK": "0"}],
                          ids=["host-driven-gmres", "fused-coarse-vcycle", "unfused-jacobi0", "no-ls-precheck",
-                              "separate-restriction", "no-speculative-trial-jacobian"])
+                              "separate-restriction", "no-speculative-trial-jacobian", "per-trial-penetration",
+                              "both-slots-assembly", "cp-async-sweep-ring"])
 def test_variant_bitwise_identical(variant):
     assert _digest(variant) == _digest({})
 

@@ -547,6 +547,7 @@ def gpu_arm(args, rank, world, local_rank):
     del gvec, gw                # the packed vectors' device memory goes back to the caching allocator
     ms = ev0.elapsed_time(ev1)
     launches = sum(int(c.L.dp_scene_launch_count(c.dev.handle)) for c in ctxs)
+    host_syncs = sum(int(c.L.dp_scene_host_sync_count(c.dev.handle)) for c in ctxs)
     t = torch.tensor([ms], device=dd["device"])
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -666,7 +667,7 @@ def gpu_arm(args, rank, world, local_rank):
                "d2h_bytes_per_step": d2h}
     pool.shutdown()
     conv = [s_[0] for r in res for s_ in r[2]]
-    return dict(ms=ms_max, launches=launches, clocks=clk.summary(), spmv_ms=spmv_ms, spmv_bytes=spmv_bytes, kt=kt,
+    return dict(ms=ms_max, launches=launches, host_syncs=host_syncs, clocks=clk.summary(), spmv_ms=spmv_ms, spmv_bytes=spmv_bytes, kt=kt,
                 achieved=achieved, hbm=hbm, traffic=traffic, e2e=e2e, setup_s=setup_s, R=R, elem=elem,
                 smooth_ms=smooth_ms, smooth_bytes=smooth_bytes, smooth_traffic=smooth_traffic, sbb=sbb,
                 fp64_peak=float(peaks.get("fp64_tflops", FP64_PEAK_TFLOPS)),
@@ -949,6 +950,7 @@ def main():
                 "roofline_fp64": roofline_fp64(r, E_tets=n_tets),
                 "kernel_times_insitu": r["kt"],
                 "clocks": r["clocks"], "gpu_launches": r["launches"], "e2e": r["e2e"],
+                "host_syncs_per_step": round(r["host_syncs"] / max(1, K * r["R"]), 1),   # fwd + bwd, per rollout step
                 "newton_iterations": r["newton"], "krylov_iterations": r["krylov"],
                 "adjoint_krylov_iterations": r["adj_iters"], "contacts": r["contacts"],
                 "converged": r["converged"], "setup_s": r["setup_s"], "nnzb": r["nnzb"],

@@ -293,6 +293,10 @@ int dp_scene_get_timing(dp_scene* s, dp_kernel_times* out);
 int dp_scene_reset_timing(dp_scene* s);
 /* number of kernel launches issued by the library on this scene since reset */
 int64_t dp_scene_launch_count(dp_scene* s);
+/* Host waits on the scene's stream issued by the library since the last
+ * dp_scene_reset_timing (Newton and line-search decisions, Krylov stop tests,
+ * step ends); for the bench's host-sync-per-step figure.  New in round 2. */
+int64_t dp_scene_host_sync_count(dp_scene* s);
 /* CUDA stream (cudaStream_t) of the scene, for callers that interleave work */
 void* dp_scene_stream(dp_scene* s);
 int dp_scene_synchronize(dp_scene* s);

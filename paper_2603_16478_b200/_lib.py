@@ -141,6 +141,7 @@ SIGNATURES = {
     "dp_scene_get_timing": (C.c_int, [_P, C.POINTER(KernelTimes)]),
     "dp_scene_reset_timing": (C.c_int, [_P]),
     "dp_scene_launch_count": (C.c_int64, [_P]),
+    "dp_scene_host_sync_count": (C.c_int64, [_P]),
     "dp_scene_stream": (_P, [_P]),
     "dp_scene_synchronize": (C.c_int, [_P]),
 }

@@ -53,7 +53,7 @@ void ktm_flush(dp_scene* s) {
   bool any = false;
   for (auto& t : s->kslot) any |= t.used > 0;
   if (!any) return;
-  cudaStreamSynchronize(s->stream);
+  host_sync(s);
   double* ms_of[] = {&s->times.spmv_ms, &s->times.elem_jac_ms, &s->times.elem_res_ms, &s->times.assemble_ms,
                      &s->times.smooth_ms, &s->times.pcg_spmv_ms};
   int64_t* n_of[] = {&s->times.spmv_calls, &s->times.elem_jac_calls, &s->times.elem_res_calls,
@@ -128,7 +128,7 @@ static int copy_out(dp_scene* s, double* dst, const double* src, size_t n, int p
 
 static int sync_esc(dp_scene* s) {
   DP_CUDA(cudaMemcpyAsync(s->h_esc, s->esc, sizeof(EvalScalars), cudaMemcpyDeviceToHost, s->stream));
-  DP_CUDA(cudaStreamSynchronize(s->stream));
+  DP_CUDA(host_sync(s));
   return 0;
 }
 
@@ -778,7 +778,7 @@ int dp_scene_destroy(dp_scene* s) {
   std::lock_guard<std::recursive_mutex> api_lock(dp::api_mutex());
   if (!s) return DP_OK;
   cudaSetDevice(s->device);
-  if (s->stream) cudaStreamSynchronize(s->stream);
+  if (s->stream) host_sync(s);
   {
     SelfContact& sc = s->self;
     dfree(s->self_tri_d); dfree(s->self_adj_ptr_d); dfree(s->self_adj_d);
@@ -844,7 +844,7 @@ int dp_scene_set_colliders(dp_scene* s, int32_t n, const int32_t* kind, const do
   }
   s->colliders = cs;
   DP_CUDA(cudaMemcpyAsync(s->d_colliders, &s->colliders, sizeof(ColliderSet), cudaMemcpyHostToDevice, s->stream));
-  DP_CUDA(cudaStreamSynchronize(s->stream));
+  DP_CUDA(host_sync(s));
   return ensure_contact_capacity(s, std::max(1, s->V * std::max(contact_sources(s), 1)));
 }
 
@@ -852,7 +852,7 @@ int dp_scene_set_bindings(dp_scene* s, int32_t n, const int64_t* vertex, const d
                           const double* compliance) {
   invalidate_adjoint(s);
   cudaSetDevice(s->device);
-  cudaStreamSynchronize(s->stream);
+  host_sync(s);
   for (int b = 0; b < n; ++b) {
     if (vertex[b] < 0 || vertex[b] >= s->V) { set_error("binding vertex out of range"); return DP_ERR_VALUE; }
     if (!(compliance[b] > 0)) { set_error("binding compliance must be positive"); return DP_ERR_VALUE; }
@@ -954,7 +954,7 @@ int dp_scene_set_materials(dp_scene* s, const double* E, const double* nu, const
     DP_CUDA(cudaMemcpyAsync(s->w, s->h_w.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
     DP_CUDA(cudaMemcpyAsync(s->mu, hmu.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
     DP_CUDA(cudaMemcpyAsync(s->lam, hlam.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
-    DP_CUDA(cudaStreamSynchronize(s->stream));
+    DP_CUDA(host_sync(s));
   }
   return DP_OK;
 }
@@ -965,7 +965,7 @@ int dp_scene_set_self_contact(dp_scene* s, int32_t n_tri, const int32_t* tri, do
   cudaSetDevice(s->device);
   if (mu < 0) { set_error("friction coefficient must be nonnegative"); return DP_ERR_VALUE; }
   SelfContact& sc = s->self;
-  cudaStreamSynchronize(s->stream);
+  host_sync(s);
   dfree(s->self_tri_d); dfree(s->self_adj_ptr_d); dfree(s->self_adj_d);
   dfree(sc.tn); dfree(sc.cell_start); dfree(sc.cell_fill); dfree(sc.items); dfree(sc.tcell); dfree(sc.hc);
   dfree(sc.cand); dfree(sc.cd2); dfree(sc.pn); dfree(sc.pd);
@@ -1011,7 +1011,7 @@ int dp_self_contact_query(dp_scene* s, const double* q_bar, const double* q_pred
   if (rc) return rc;
   launch_self_build(s);
   launch_self_candidates(s, s->q_try);
-  DP_CUDA(cudaStreamSynchronize(s->stream));
+  DP_CUDA(host_sync(s));
   const SelfContact& sc = s->self;
   if (tri_out) DP_CUDA(cudaMemcpy(tri_out, sc.cand, sizeof(int) * s->V, cudaMemcpyDefault));
   if (d2_out) DP_CUDA(cudaMemcpy(d2_out, sc.cd2, sizeof(double) * s->V, cudaMemcpyDefault));
@@ -1044,7 +1044,7 @@ int dp_scene_export_bsr(dp_scene* s, int32_t which, int32_t* rowptr, int32_t* co
   }
   std::vector<double> sell((size_t)s->NS * 9);
   DP_CUDA(cudaMemcpyAsync(sell.data(), v, sell.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-  DP_CUDA(cudaStreamSynchronize(s->stream));
+  DP_CUDA(host_sync(s));
   if (rowptr) std::memcpy(rowptr, s->h_rowptr.data(), sizeof(int) * (s->V + 1));
   if (col) std::memcpy(col, s->h_colidx.data(), sizeof(int) * s->nnzb);
   if (val) {
@@ -1305,7 +1305,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     if (mg) mg_assemble(s, s->val_fwd);
     double t_solve0 = 0;
     if (g_debug) {
-      cudaStreamSynchronize(s->stream);
+      host_sync(s);
       t_solve0 = now_s();
       fprintf(stderr, "[dp]   assemble %.2fms\n", 1e3 * (t_solve0 - t_asm0));
     }
@@ -1334,7 +1334,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
     }
     double t_ls0 = 0;
     if (g_debug) {
-      cudaStreamSynchronize(s->stream);
+      host_sync(s);
       t_ls0 = now_s();
       fprintf(stderr, "[dp] it=%d res=%.3e |r|2=%.3e C=%d asym=%d eta=%.1e krylov=%d relres=%.2e rc=%d solve=%.2fms guess=%d/%d\n",
               it, res, rn, n_contacts, asym, eta, iters, relres, rc, 1e3 * (t_ls0 - t_solve0), s->dq_prev_valid, E.discont);
@@ -1419,7 +1419,7 @@ int dp_forward_step(dp_scene* s, const double* q_bar, const double* v_bar, int32
   if (q_out && (rc = copy_out(s, q_out, s->q, n3, ptr_kind))) return rc;
   if (v_out && (rc = copy_out(s, v_out, s->z, n3, ptr_kind))) return rc;
   if (cache && (rc = cache_store(s, cache, q_eval, n_contacts, asym))) return rc;
-  DP_CUDA(cudaStreamSynchronize(s->stream));
+  DP_CUDA(host_sync(s));
   if (g_debug) fprintf(stderr, "[dp] step total %.2fms\n", 1e3 * (now_s() - t_step0));
   R.converged = converged ? 1 : 0;
   R.iterations = nhist;
@@ -1503,7 +1503,7 @@ int dp_cache_get_projections(dp_scene* s, const dp_cache* c, double* sigma, doub
   double* dP = scratch_take<double>(ED * 3);
   double* de = scratch_take<double>(E);
   launch_export_proj(s, c->q_eval, ds, dt, dP, de);
-  cudaStreamSynchronize(s->stream);
+  host_sync(s);
   if (sigma) cudaMemcpy(sigma, ds, sizeof(double) * E * D, cudaMemcpyDeviceToHost);
   if (theta) cudaMemcpy(theta, dt, sizeof(double) * E * D, cudaMemcpyDeviceToHost);
   if (P) cudaMemcpy(P, dP, sizeof(double) * E * 3 * D, cudaMemcpyDeviceToHost);
@@ -1615,7 +1615,7 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
   DP_CUDA(cudaMemcpyAsync(s->z_prev, s->z, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s->stream));
   s->z_prev_valid = 1;
   if (g_debug) {
-    cudaStreamSynchronize(s->stream);
+    host_sync(s);
     fprintf(stderr, "[dp] adjoint sym=%d iters=%d relres=%.2e solve %.2fms\n", sym, iters, relres,
             1e3 * (now_s() - t0));
   }
@@ -1629,7 +1629,7 @@ int dp_adjoint_solve(dp_scene* s, const dp_cache* c, const double* dL_dq, const 
     int rc2 = copy_out(s, z_out, s->z, n3, ptr_kind);
     if (rc2) return rc2;
   }
-  DP_CUDA(cudaStreamSynchronize(s->stream));
+  DP_CUDA(host_sync(s));
   if (!(relres <= cfg.tol)) {
     char buf[160];
     snprintf(buf, sizeof buf, "adjoint solve did not converge; relative residual %.3e", relres);
@@ -1664,7 +1664,7 @@ int dp_backprop_step(dp_scene* s, const dp_cache* c, const double* z, const doub
   if (dL_dqbar_out && (rc = copy_out(s, dL_dqbar_out, dq, n3, ptr_kind))) return rc;
   if (dL_dvbar_out && (rc = copy_out(s, dL_dvbar_out, dv, n3, ptr_kind))) return rc;
   if (dL_dfext_out && (rc = copy_out(s, dL_dfext_out, df, n3, ptr_kind))) return rc;
-  DP_CUDA(cudaStreamSynchronize(s->stream));
+  DP_CUDA(host_sync(s));
   cudaError_t e = cudaGetLastError();
   if (g_debug) fprintf(stderr, "[dp] backprop %.2fms\n", 1e3 * (now_s() - t0));
   if (e != cudaSuccess) return cuda_fail(e, "backprop");
@@ -1680,7 +1680,7 @@ int dp_grads_reset(dp_scene* s) {
     DP_CUDA(cudaMemsetAsync(s->g_dEb, 0, sizeof(double) * s->g_nb_cap, s->stream));
     DP_CUDA(cudaMemsetAsync(s->g_ddb, 0, sizeof(double) * 3 * s->g_nb_cap, s->stream));
   }
-  DP_CUDA(cudaStreamSynchronize(s->stream));
+  DP_CUDA(host_sync(s));
   return DP_OK;
 }
 
@@ -1688,7 +1688,7 @@ int dp_grads_get(dp_scene* s, dp_grad_scalars* out) {
   cudaSetDevice(s->device);
   double h[4];
   DP_CUDA(cudaMemcpyAsync(h, s->g_scal, sizeof h, cudaMemcpyDeviceToHost, s->stream));
-  DP_CUDA(cudaStreamSynchronize(s->stream));
+  DP_CUDA(host_sync(s));
   out->dL_dmu_friction = h[0];
   out->dL_dstiffness = h[1];
   out->dmu_lame = h[2];
@@ -1705,7 +1705,7 @@ int dp_grads_get_arrays(dp_scene* s, double* dL_dw, double* dL_dEb, double* dL_d
   if (dL_dw && s->E) DP_CUDA(cudaMemcpyAsync(dL_dw, s->g_dw, sizeof(double) * s->E, k, s->stream));
   if (dL_dEb && s->nb) DP_CUDA(cudaMemcpyAsync(dL_dEb, s->g_dEb, sizeof(double) * s->nb, k, s->stream));
   if (dL_ddb && s->nb) DP_CUDA(cudaMemcpyAsync(dL_ddb, s->g_ddb, sizeof(double) * 3 * s->nb, k, s->stream));
-  DP_CUDA(cudaStreamSynchronize(s->stream));
+  DP_CUDA(host_sync(s));
   return DP_OK;
 }
 
@@ -1902,9 +1902,11 @@ int dp_scene_reset_timing(dp_scene* s) {
   dp::ktm_flush(s);
   s->times = dp_kernel_times{};
   s->launches = 0;
+  s->host_syncs = 0;
   return DP_OK;
 }
 int64_t dp_scene_launch_count(dp_scene* s) { return s->launches; }
+int64_t dp_scene_host_sync_count(dp_scene* s) { return s->host_syncs; }
 void* dp_scene_stream(dp_scene* s) { return (void*)s->stream; }
 int dp_scene_synchronize(dp_scene* s) {
   DP_CUDA(cudaStreamSynchronize(s->stream));

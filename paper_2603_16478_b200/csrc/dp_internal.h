@@ -292,6 +292,7 @@ struct dp_scene {
     int used = 0;
   } kslot[8];
   int64_t launches = 0;
+  int64_t host_syncs = 0;         // host waits on the scene stream (host_sync)
 
   // last assembled operator: symmetric flag
   int last_sym_fwd = 1, last_sym_adj = 1;
@@ -397,5 +398,12 @@ enum { KT_SPMV = 0, KT_ELEM_JAC = 1, KT_ELEM_RES = 2, KT_ASSEMBLE = 3, KT_SMOOTH
 void ktm_begin(dp_scene* s, int slot);
 void ktm_end(dp_scene* s, int slot);
 void ktm_flush(dp_scene* s);
+
+// every host wait on a scene's stream goes through here (counted: the
+// Newton / line-search loop's round trips, dp_scene_host_sync_count)
+inline cudaError_t host_sync(dp_scene* s) {
+  ++s->host_syncs;
+  return cudaStreamSynchronize(s->stream);
+}
 
 }  // namespace dp

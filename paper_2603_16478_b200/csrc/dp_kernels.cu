@@ -1181,7 +1181,7 @@ double device_norm2(dp_scene* s, const double* x) {
   s->launches++;
   double h = 0.0;
   cudaMemcpyAsync(&s->h_ksc->pad[1], res, sizeof(double), cudaMemcpyDeviceToHost, s->stream);
-  cudaStreamSynchronize(s->stream);
+  host_sync(s);
   h = s->h_ksc->pad[1];
   return h;
 }
@@ -1198,13 +1198,13 @@ static double true_relres(dp_scene* s, const double* val, const double* b, const
                                                     r, s->red.partial, s->red.counter, res);
   s->launches++;
   cudaMemcpyAsync(&s->h_ksc->pad[1], res, sizeof(double), cudaMemcpyDeviceToHost, s->stream);
-  cudaStreamSynchronize(s->stream);
+  host_sync(s);
   return sqrt(s->h_ksc->pad[1]) / bnorm;
 }
 
 static void read_ksc(dp_scene* s) {
   cudaMemcpyAsync(s->h_ksc, s->ksc, sizeof(KrylovScalars), cudaMemcpyDeviceToHost, s->stream);
-  cudaStreamSynchronize(s->stream);
+  host_sync(s);
 }
 
 // Solve A x = b to rtol (true relative residual).  Returns 0 ok, 1 not
@@ -2028,7 +2028,7 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
       // the whole cycle on the device: one graph launch, one sync
       cudaGraphLaunch(gg->exec, s->stream);
       cudaMemcpyAsync(s->h_gsc, s->gsc, gsc_bytes, cudaMemcpyDeviceToHost, s->stream);
-      cudaStreamSynchronize(s->stream);
+      host_sync(s);
       s->launches += (int64_t)gg->nodes * std::max(1, s->h_gsc->used);
     } else {
       // host-driven columns, polled every 8
@@ -2039,7 +2039,7 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
         for (int c = 0; c < chunk; ++c) s->launches += gm_column(s, val, use_mg, left, tight, lowp, zb, 0, 0);
         launched += chunk;
         cudaMemcpyAsync(s->h_gsc, s->gsc, gsc_bytes, cudaMemcpyDeviceToHost, s->stream);
-        cudaStreamSynchronize(s->stream);
+        host_sync(s);
         stop = s->h_gsc->done || !s->h_gsc->active;
       }
     }

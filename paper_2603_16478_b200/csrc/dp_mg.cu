@@ -677,6 +677,51 @@ __global__ void __launch_bounds__(256, 5) k_mg_smooth(int n, int S, const int* _
       issue(k + kSmDepth);
     }
     cp_async_wait<0>();
+  } else if constexpr (sizeof(TV) == 8 && SPLIT == 8 && BULK > 0) {
+    // coarse levels, the ring filled by TMA bulk copies (one lane per warp,
+    // 2,304 + 128 B per slot, mbarrier completion); same values, same order
+    __shared__ __align__(128) double sv[SPLIT][BULK][9 * kSlice];
+    __shared__ __align__(128) int sc[SPLIT][BULK][kSlice];
+    __shared__ __align__(8) uint64_t mb[SPLIT][BULK];
+    const double* gv = reinterpret_cast<const double*>(val) + (size_t)base * 9;
+    const int* gc = col + base;
+    const int nk = (K > wsub) ? (K - wsub + SPLIT - 1) / SPLIT : 0;
+    if (lane == 0) {
+#pragma unroll
+      for (int d = 0; d < BULK; ++d) mbar_init(&mb[wsub][d], 1);
+      mbar_fence_init();
+    }
+    __syncwarp();
+    auto issue = [&](int i) {
+      if (i < nk && lane == 0) {
+        const int kk = wsub + i * SPLIT;
+        const int d = i % BULK;
+        mbar_expect_tx(&mb[wsub][d], 9 * kSlice * 8 + kSlice * 4);
+        bulk_g2s(sv[wsub][d], gv + (size_t)kk * 9 * kSlice, 9 * kSlice * 8, &mb[wsub][d]);
+        bulk_g2s(sc[wsub][d], gc + (size_t)kk * kSlice, kSlice * 4, &mb[wsub][d]);
+      }
+    };
+#pragma unroll
+    for (int i = 0; i < BULK; ++i) issue(i);
+    for (int i = 0; i < nk; ++i) {
+      const int d = i % BULK;
+      mbar_wait(&mb[wsub][d], (uint32_t)((i / BULK) & 1));
+      const double* vv = sv[wsub][d];
+      const int j = sc[wsub][d][lane];
+      double m[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) m[c] = vv[c * kSlice + lane];
+      double x0 = __ldg(x + 3 * j), x1 = __ldg(x + 3 * j + 1), x2 = __ldg(x + 3 * j + 2);
+      if (xc) {
+        const int J = __ldg(agg + j);
+        x0 += alpha * __ldg(xc + 3 * J); x1 += alpha * __ldg(xc + 3 * J + 1); x2 += alpha * __ldg(xc + 3 * J + 2);
+      }
+      a0 += m[0] * x0 + m[1] * x1 + m[2] * x2;
+      a1 += m[3] * x0 + m[4] * x1 + m[5] * x2;
+      a2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
+      __syncwarp();
+      issue(i + BULK);
+    }
   } else if constexpr (sizeof(TV) == 8 && SPLIT == 8) {
     // coarse levels (L2-resident FP64): warp wsub's slots wsub, wsub + 8, ...
     // stream through a 2-deep per-warp shared-memory ring (2,304 + 128 bytes
@@ -1032,6 +1077,7 @@ __global__ void __launch_bounds__(DP_SMOOTH_NT) k_mg_smooth_pf(int n, int S, con
 }
 
 // fine sweep ring filled by TMA bulk copies (depth 2; 0 = per-lane cp.async ring): in situ 24.7 -> 23.6 us
+static const int g_coarse_bulk = getenv("DP_COARSE_BULK") ? atoi(getenv("DP_COARSE_BULK")) : 1;
 static const int g_smooth_bulk = getenv("DP_SMOOTH_BULK") ? atoi(getenv("DP_SMOOTH_BULK")) : 2;
 static const int g_smooth_pf = getenv("DP_SMOOTH_PF") ? atoi(getenv("DP_SMOOTH_PF")) : 0;   // measured slower (25.6 vs 24.1 us in situ), off
 
@@ -1578,6 +1624,9 @@ static void smooth(dp_scene* s, const MGLevel& L, const TV* val, const TV* minv,
   else if (L.S >= 4 * 148)
     k_mg_smooth<TV, 1><<<grid_for((int64_t)L.S * 32, DP_SMOOTH_NT), DP_SMOOTH_NT, 0, s->stream>>>(
         L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x, xc, agg, omega, out, r_out, stop, alpha);
+  else if (sizeof(TV) == 8 && g_coarse_bulk)
+    k_mg_smooth<TV, 8, false, 2><<<L.S, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv,
+                                                             b, x, xc, agg, omega, out, r_out, stop, alpha);
   else
     k_mg_smooth<TV, 8><<<L.S, 256, 0, s->stream>>>(L.n, L.S, L.slice_base, L.slice_width, L.col, val, minv, b, x,
                                                    xc, agg, omega, out, r_out, stop, alpha);
@@ -1931,7 +1980,7 @@ static void launch_tail(dp_scene* s, const double* rf, const int* stop) {
     static double acc[9];
     static long cnt = 0;
     unsigned long long t[12];
-    cudaStreamSynchronize(s->stream);
+    host_sync(s);
     cudaMemcpyFromSymbol(t, g_tail_clk, sizeof(t));
     unsigned long long cy[12];
     cudaMemcpyFromSymbol(cy, g_tail_cyc, sizeof(cy));
@@ -1989,7 +2038,7 @@ static void launch_coarse_fused(dp_scene* s, const double* r0, const int* stop) 
     if (!dts) cudaMalloc(&dts, 64 * sizeof(unsigned long long));
     if (calls % 64 == 63) {
       unsigned long long h[64];
-      cudaStreamSynchronize(s->stream);
+      host_sync(s);
       cudaMemcpy(h, dts, sizeof(h), cudaMemcpyDeviceToHost);
       fprintf(stderr, "[mg-fused] L=%d phases(us):", a.L);
       for (int i = 1; i < 32 && h[i]; ++i) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);

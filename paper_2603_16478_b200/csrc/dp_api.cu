@@ -742,6 +742,7 @@ int dp_scene_create(const dp_scene_desc* d, dp_scene** out) {
   if (rc) { dp_scene_destroy(s); return rc; }
   if (cudaMallocHost(&s->h_esc, sizeof(EvalScalars)) != cudaSuccess ||
       cudaMallocHost(&s->h_ksc, sizeof(KrylovScalars)) != cudaSuccess ||
+      cudaMallocHost(&s->h_aux, 4 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&s->h_gsc, sizeof(GmresScalars)) != cudaSuccess) {
     dp_scene_destroy(s);
     set_error("cudaMallocHost failed");
@@ -806,6 +807,7 @@ int dp_scene_destroy(dp_scene* s) {
   for (void* p : ptrs) dfree(p);
   if (s->h_esc) cudaFreeHost(s->h_esc);
   if (s->h_ksc) cudaFreeHost(s->h_ksc);
+  if (s->h_aux) cudaFreeHost(s->h_aux);
   if (s->h_gsc) cudaFreeHost(s->h_gsc);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);

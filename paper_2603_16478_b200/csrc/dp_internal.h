@@ -272,6 +272,7 @@ struct dp_scene {
   dp::EvalScalars* esc = nullptr;
   dp::EvalScalars* h_esc = nullptr;     // pinned
   dp::KrylovScalars* h_ksc = nullptr;   // pinned
+  double* h_aux = nullptr;               // pinned: values read back with a later sync (|b|^2 of a solve)
   dp::GmresScalars* h_gsc = nullptr;    // pinned
   dp::Reduce red;
 

@@ -1187,6 +1187,32 @@ double device_norm2(dp_scene* s, const double* x) {
 }
 
 // true relative residual |b - A x| / |b| (synchronous)
+// |x|^2 -> *host (pinned) without a sync: the value is valid after the
+// caller's next host_sync (second reduction slot, see device_norm2)
+static void norm2_async(dp_scene* s, const double* x, double* host) {
+  const int n = 3 * s->V;
+  int nb = grid_for(n, kVT);
+  if (nb > 1024) nb = 1024;
+  double* res = s->red.partial + s->red.cap_blocks * s->red.width - 2;
+  k_norm2<<<nb, kVT, 0, s->stream>>>(n, x, s->red.partial, s->red.counter, res);
+  s->launches++;
+  cudaMemcpyAsync(host, res, sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+}
+
+// launch half of true_relres: r = b - A x and |r|^2 -> h_ksc->pad[1] (async)
+static void true_relres_launch(dp_scene* s, const double* val, const double* b, const double* x, double* r) {
+  const int nb = grid_for((int64_t)s->S * 32, 256);
+  double* res = s->red.partial + s->red.cap_blocks * s->red.width - 1;
+  if (val == s->val32_src && !s->val64_valid)   // FP32-only forward operator (EV_H32)
+    k_resid_true<float><<<nb, 256, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->col, s->val32, x,
+                                                   b, r, s->red.partial, s->red.counter, res);
+  else
+    k_resid_true<double><<<nb, 256, 0, s->stream>>>(s->V, s->S, s->slice_base, s->slice_width, s->col, val, x, b,
+                                                    r, s->red.partial, s->red.counter, res);
+  s->launches++;
+  cudaMemcpyAsync(&s->h_ksc->pad[1], res, sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+}
+
 static double true_relres(dp_scene* s, const double* val, const double* b, const double* x, double* r, double bnorm) {
   const int nb = grid_for((int64_t)s->S * 32, 256);
   double* res = s->red.partial + s->red.cap_blocks * s->red.width - 1;
@@ -2444,12 +2470,11 @@ int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x
   const int nbs = grid_for((int64_t)s->S * 32, 256);
   *iters = 0;
   *breakdown = 0;
-  double bnorm = sqrt(device_norm2(s, b));
-  if (bnorm == 0.0) {
-    cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
-    *relres = 0.0;
-    return 0;
-  }
+  // |b| comes back with the first sync of the solve (no sync of its own);
+  // a zero rhs runs no iteration (the stop test holds at init) and returns
+  // x = 0 once |b| is known
+  norm2_async(s, b, &s->h_aux[0]);
+  double bnorm = -1.0;
   const float* minv32 = nullptr;
   double* xa = nullptr;
   double omega = 0.0;
@@ -2465,7 +2490,14 @@ int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x
     // when it reduces the residual (else start from zero)
     launch_spmv(s, val, x0, bb);
     launch_axpy_to(s, bb, b, -1.0, bb);
-    rel = sqrt(device_norm2(s, bb)) / bnorm;
+    const double rg = sqrt(device_norm2(s, bb));   // this sync also brings |b|
+    bnorm = sqrt(s->h_aux[0]);
+    if (bnorm == 0.0) {
+      cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+      *relres = 0.0;
+      return 0;
+    }
+    rel = rg / bnorm;
     guess = rel < 1.0;
     if (guess) cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, s->stream);
     else rel = 1.0;
@@ -2491,12 +2523,18 @@ int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x
                                            omega, xa, max_iter - *iters);
     s->launches++;
     int done = 0, launched = 0, chunk = 4;
+    bool fused = false;   // Krylov scalars and the true residual came back in one sync
     GmGraph* gg = (g_use_graphs && !s->timing) ? pcg_graph(s, val, fp32) : nullptr;
     if (gg) {
-      // the whole solve on the device: one graph launch, one sync
+      // the whole solve on the device: one graph launch, then x += xc and the
+      // FP64 true residual queued behind it, one sync for all of it
       cudaGraphLaunch(gg->exec, s->stream);
-      read_ksc(s);
+      cudaMemcpyAsync(s->h_ksc, s->ksc, sizeof(KrylovScalars), cudaMemcpyDeviceToHost, s->stream);
+      launch_axpy_to(s, x, x, 1.0, xc);
+      true_relres_launch(s, val, b, x, bb);   // bb == s->tmp (the breakdown branch's buffer too)
+      host_sync(s);
       done = 1;
+      fused = true;
       s->launches += (int64_t)(gg->nodes / 2) * std::max(1, s->h_ksc->iters);
     }
     while (!done && *iters + launched < max_iter) {
@@ -2531,13 +2569,22 @@ int pcg_mg_solve_impl(dp_scene* s, const double* val, const double* b, double* x
       if (chunk < 16) chunk *= 2;
     }
     *iters += s->h_ksc->iters;
-    launch_axpy_to(s, x, x, 1.0, xc);
+    if (bnorm < 0.0) {   // first pass: |b| arrived with its sync
+      bnorm = sqrt(s->h_aux[0]);
+      if (bnorm == 0.0) {
+        cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+        *relres = 0.0;
+        return 0;
+      }
+    }
+    if (!fused) launch_axpy_to(s, x, x, 1.0, xc);
+    const double rel_f = fused ? sqrt(s->h_ksc->pad[1]) / bnorm : 0.0;
     if (s->h_ksc->done == 2) {
       *breakdown = 1;
-      *relres = true_relres(s, val, b, x, s->tmp, bnorm);
+      *relres = fused ? rel_f : true_relres(s, val, b, x, s->tmp, bnorm);
       return 2;
     }
-    rel = true_relres(s, val, b, x, bb, bnorm);
+    rel = fused ? rel_f : true_relres(s, val, b, x, bb, bnorm);
     if (rel <= rtol || *iters >= max_iter) break;
   }
   *relres = rel;

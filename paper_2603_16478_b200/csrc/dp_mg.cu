@@ -1937,10 +1937,12 @@ static int tail_cluster(size_t smem) {
   return ok;
 }
 
+static int g_tail_failed = 0;   // a cluster launch was refused: per-level V-cycle from then on
+
 // usable for the level pair (l, l+1) = (L-2, L-1)
 static bool tail_usable(const MG* mg, int la) {
   const int L = (int)mg->lv.size();
-  if (!(g_mg_tail && L >= 2 && la == L - 2 && la >= 1 && mg->nu == 1 && mg->gamma == 1 && mg->coarse_sweeps > 0 &&
+  if (!(g_mg_tail && !g_tail_failed && L >= 2 && la == L - 2 && la >= 1 && mg->nu == 1 && mg->gamma == 1 && mg->coarse_sweeps > 0 &&
         (mg->post == 1 || mg->symmetric_needed)))
     return false;
   const MGLevel &a = mg->lv[L - 2], &c = mg->lv[L - 1];
@@ -1949,7 +1951,8 @@ static bool tail_usable(const MG* mg, int la) {
   return smem <= 200 * 1024 && tail_cluster(smem) > 0;
 }
 
-static void launch_tail(dp_scene* s, const double* rf, const int* stop) {
+// false: the launch was refused (the caller runs the per-level kernels)
+static bool launch_tail(dp_scene* s, const double* rf, const int* stop) {
   MG* mg = s->mg;
   const int L = (int)mg->lv.size();
   MGLevel& a = mg->lv[L - 2];
@@ -1974,7 +1977,11 @@ static void launch_tail(dp_scene* s, const double* rf, const int* stop) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_mg_tail, A);
+  if (cudaLaunchKernelEx(&cfg, k_mg_tail, A) != cudaSuccess) {
+    cudaGetLastError();
+    g_tail_failed = 1;
+    return false;
+  }
   s->launches++;
   if (DP_MG_TAIL_TIMING && getenv("DP_MG_TAIL_DBG")) {
     static double acc[9];
@@ -2000,6 +2007,7 @@ static void launch_tail(dp_scene* s, const double* rf, const int* stop) {
                 cacc[1] / cnt, cacc[2] / cnt, cacc[3] / cnt, cacc[4] / cnt, cacc[5] / cnt, cacc[6] / cnt, cacc[7] / cnt);
     }
   }
+  return true;
 }
 
 static const int g_mg_fused_env = getenv("DP_MG_FUSED") ? atoi(getenv("DP_MG_FUSED")) : 0;
@@ -2097,8 +2105,9 @@ static void vcycle_level(dp_scene* s, int l, const TV* val, const TV* minv, cons
     smooth<TV>(s, L, val, minv, b, xa, nullptr, nullptr, om, nullptr, L.r, stop, 1.0);
     if (l == 0 && fused_usable(mg)) {
       launch_coarse_fused(s, L.r, stop);   // restriction to level 1 is its first phase
-    } else if (tail_usable(mg, l + 1)) {
-      launch_tail(s, L.r, stop);           // levels l+1 and l+2 in one cluster launch -> C.x
+    } else if (tail_usable(mg, l + 1) && launch_tail(s, L.r, stop)) {
+      // levels l+1 and l+2 in one cluster launch -> C.x (a refused launch
+      // falls through to the per-level kernels below)
     } else if (g_mg_rj0 && l + 1 == (int)mg->lv.size() - 1 && mg->coarse_sweeps > 0) {
       // coarsest level: the restriction is the first phase of its one-CTA solve
       k_mg_coarse_jacobi<<<1, 256, 0, s->stream>>>(C.n, C.S, C.slice_base, C.slice_width, C.col, C.val, C.minv, C.b,

@@ -109,6 +109,11 @@ CONFIGS = {
     "c2": dict(cells=(100, 100, 0), edge=0.01, fingers=False, eps_fb=1e-9, tol=1e-11, rollouts=1, cloth=True, steps=4,
                desc="20,000-triangle ARAP cloth (1 m, 0.3 kg/m^2) draping over a frictional sphere, "
                     "per-step control-force gradients (C2 without self-contact: none in the reference)"),
+    "c2fold": dict(cells=(40, 40, 0), edge=0.01, fingers=False, eps_fb=1e-9, tol=1e-10, rollouts=1, cloth=True,
+                   fold=120, h=0.005, comp=1e-4, steps=120,
+                   desc="3,200-triangle ARAP sheet (40 cm) on a frictionless ground, its right edge bound to "
+                        "targets that fold it over its centre line in 120 steps of 5 ms, self-contact on (C2 fold "
+                        "at reduced size: the 100 x 100 sheet stalls in the reference model's Newton)"),
     "c4": dict(cells=(8, 8, 520), edge=2.5e-3, fingers=False, eps_fb=1e-9, tol=1e-10, rollouts=1, trunk=True,
                steps=200, wall_gap=2e-3, cable_amp=1e-3,
                desc="199,680-tet NH trunk (2 x 2 x 130 cm) clamped at the top by stiff bindings, 4 cable "
@@ -154,6 +159,18 @@ def make_scene(cfg_or_n, fingers=None, eps_fb=None, E=E_YOUNG, mu=None):
         c = dict(cells=(n, n, n), edge=0.1 / n, fingers=True, eps_fb=1e-9 if n >= 40 else (1e-7 if n >= 20 else 1e-6),
                  schedule=(2e-5, None))
     nx, ny, nz = c["cells"]
+    if c.get("fold"):
+        # C2 fold (tools/c2_fold_explore.py): the bound right edge swings over
+        # the crease line x = size/2; self-contact between the two halves
+        size = nx * c["edge"]
+        v, t = ident.horizontal_sheet(nx, ny, c["edge"], origin=(0.0, 0.0, 5e-4))
+        right = np.nonzero(np.abs(v[:, 0] - size) < 1e-12)[0]
+        binds = [core.BindingSpec(int(i), v[i].copy(), c["comp"]) for i in right]
+        sc = core.Scene(v, t, core.lumped_masses(v, t, 0.3), [core.MaterialParams("arap", stiffness=50.0)] * len(t),
+                        colliders=[core.HalfSpace([0, 0, 1], 0.0, mu=0.0)], bindings=binds, h=c["h"],
+                        eps_fb=c["eps_fb"] if eps_fb is None else eps_fb, self_contact=True, self_mu=0.0)
+        sc._fold = (size, c["fold"])
+        return sc
     if c.get("cloth"):
         # horizontal sheet 0.5 mm above a sphere of radius 0.25
         v, t = ident.horizontal_sheet(nx, ny, c["edge"], origin=(0.0, 0.0, 0.2505))
@@ -221,6 +238,20 @@ def drive_cables(scene, k):
     return f
 
 
+def fold_targets(scene, k, lift=2e-3):
+    """C2 fold: targets of the bound edge at step k = that edge of the sheet
+    rigidly folded about x = size/2 by th(k) = pi min(1, (k+1)/fold), lifted
+    by `lift` near the crease (tools/c2_fold_explore.py)."""
+    size, fold = scene._fold
+    th = np.pi * min(1.0, (k + 1) / fold)
+    v = scene.vertices
+    xc = 0.5 * size
+    for b in scene.bindings:
+        x = v[b.vertex]
+        d = x[0] - xc
+        b.target = np.array([xc + d * np.cos(th), x[1], x[2] + d * np.sin(th) + lift * min(1.0, d / (0.1 * size))])
+
+
 def finger_offset(scene, k):
     """How far each finger has closed at finger index k (m)."""
     speed, hold = getattr(scene, "_finger_schedule", (2e-5, None))
@@ -232,6 +263,9 @@ def move_fingers(scene, k):
     every step as in contact.py:125-127); C4: cable forces."""
     if getattr(scene, "_cable_lines", None) is not None:
         drive_cables(scene, k)
+        return
+    if getattr(scene, "_fold", None) is not None:
+        fold_targets(scene, k)
         return
     if len(scene.colliders) < 3:
         return
@@ -899,7 +933,8 @@ def main():
               "material": ("arap stiffness=50" if cloth else
                            (f"neohookean E={E_YOUNG}(1+0.05 i) nu={NU}" if cdef.get("vary", "E") == "E" else
                             f"neohookean E={E_YOUNG} nu={NU}, target shift 1e-3 (1 + 0.1 i) per rollout i")),
-              "friction_mu": 0.3 if (cloth or cdef.get("trunk")) else cdef.get("mu", MU), "h": 0.01,
+              "friction_mu": (0.0 if cdef.get("fold") else 0.3) if (cloth or cdef.get("trunk")) else cdef.get("mu", MU),
+              "h": cdef.get("h", 0.01), "self_contact": bool(cdef.get("fold")),
               "finger_schedule": (f"close {FINGER_SPEED * 1e6:.0f} um/step up to finger index {FINGER_HOLD}, then "
                                   f"hold; every rollout starts at index {FINGER_K0}"
                                   if cdef.get("fingers") else None),

@@ -129,3 +129,33 @@ def test_stacked_cubes_step_no_interpenetration_and_fd_gradient(pkg):
     E0, eta = 2e4, 2e4 * 1e-3
     fd = (loss(E0 + eta) - loss(E0 - eta)) / (2 * eta)
     assert abs(g.dL_dE - fd) <= 1e-3 * abs(fd)
+
+
+def test_c2_fold_converges_with_self_contact(pkg):
+    """The bench's C2 fold (3,200-triangle ARAP sheet folded over its centre
+    line in 120 steps, bench.py CONFIGS['c2fold']): every step converges, the
+    folded halves end in hundreds of self contacts, and at the final state no
+    vertex lies behind its self-contact plane (planes from the oracle's
+    brute-force candidates at the last step's q_bar)."""
+    import sys
+    import os
+    import self_contact_oracle as SO
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_2603_16478_b200 import core, forward as fw
+    scene = bench.make_scene("c2fold")
+    sm = core.assemble_system_matrix(scene)
+    cfg = fw.ForwardConfig(tol=bench.CONFIGS["c2fold"]["tol"])
+    st = scene.rest_state()
+    rep = None
+    for k in range(bench.CONFIGS["c2fold"]["steps"]):
+        bench.move_fingers(scene, k)
+        st_prev = st
+        st, rep = fw.forward_step(scene, st, sm, cfg)
+        assert rep.converged, k
+    ncol = len(scene.colliders)
+    n_self = sum(1 for c in rep.cache.contacts if c.collider == ncol)
+    assert n_self > 100
+    tri, _, nrm, off = SO.self_candidates(st_prev.q, rep.cache.q_hat, scene.elements, scene.contact_activation)
+    _, gap = SO.active_self_contacts(tri, nrm, off, st.q, scene.contact_activation)
+    assert np.all(gap[tri >= 0] > 0.0)

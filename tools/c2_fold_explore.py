@@ -1,7 +1,7 @@
 """C2 fold exploration on the GPU: an ARAP cloth sheet on the ground, its
 right edge bound to targets that swing over the centre line (a half fold),
 with self-contact.  argv: JSON list of {n, steps, fold, eps, tol, mu, mus,
-comp, stiff}."""
+comp, stiff, h, max_iter, th0, lift}."""
 import json
 import os
 import sys
@@ -22,7 +22,7 @@ def fold_scene(d):
     right = np.nonzero(np.abs(v[:, 0] - size) < 1e-12)[0]
     binds = [core.BindingSpec(int(i), v[i].copy(), d.get("comp", 1e-6)) for i in right]
     sc = core.Scene(v, t, m, [core.MaterialParams("arap", stiffness=d.get("stiff", 50.0))] * len(t),
-                    colliders=[core.HalfSpace([0, 0, 1], 0.0, mu=d.get("mu", 0.0))], bindings=binds, h=0.01,
+                    colliders=[core.HalfSpace([0, 0, 1], 0.0, mu=d.get("mu", 0.0))], bindings=binds, h=d.get("h", 0.01),
                     eps_fb=d.get("eps", 1e-9), self_contact=True, self_mu=d.get("mus", 0.0))
     return sc, size
 
@@ -59,7 +59,7 @@ for d in json.loads(sys.argv[1]):
     th0 = d.get("th0", 0.0)
     if th0:
         st.q[:] = folded(sc.vertices, size, th0, d.get("lift", 2e-3)).reshape(-1)
-    cfg = fw.ForwardConfig(tol=d.get("tol", 1e-10))
+    cfg = fw.ForwardConfig(tol=d.get("tol", 1e-10), max_iter=d.get("max_iter", 100))
     its, t0, ok, nself = [], time.time(), True, []
     for k in range(d.get("steps", 60)):
         set_fold(sc, size, k, d.get("fold", 40), th0, d.get("lift", 2e-3))

@@ -25,8 +25,24 @@ std::recursive_mutex& api_mutex() {
   return mu;
 }
 
+// keeps the GPU busy for ~ns while the host queues a timed launch behind it
+__global__ void k_ktm_spin(long long ns) {
+  long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 void ktm_begin(dp_scene* s, int k) {
   if (!s->timing) return;
+  if (s->stream_drained) {
+    // right after a host wait the stream is empty: without this the begin
+    // event would fire at once and the interval would include the host's
+    // own launch latency for the kernel (not the kernel's duration)
+    k_ktm_spin<<<1, 1, 0, s->stream>>>(30000);
+    s->stream_drained = 0;
+  }
   dp_scene::KSlot& t = s->kslot[k];
   if (t.used == (int)t.a.size()) {
     if (t.used >= 8192) {   // bound the pool: resolve what is recorded so far

@@ -294,6 +294,7 @@ struct dp_scene {
   } kslot[8];
   int64_t launches = 0;
   int64_t host_syncs = 0;         // host waits on the scene stream (host_sync)
+  int stream_drained = 1;         // the host just waited on the stream (ktm_begin: GPU idle)
 
   // last assembled operator: symmetric flag
   int last_sym_fwd = 1, last_sym_adj = 1;
@@ -404,6 +405,7 @@ void ktm_flush(dp_scene* s);
 // Newton / line-search loop's round trips, dp_scene_host_sync_count)
 inline cudaError_t host_sync(dp_scene* s) {
   ++s->host_syncs;
+  s->stream_drained = 1;
   return cudaStreamSynchronize(s->stream);
 }
 

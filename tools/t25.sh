@@ -1,0 +1,11 @@
+# round-2 final artefacts (final code): GPU tests, driver bench command, reference arm, C1-C4 + C2 fold, launch list, smoke
+set -x
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/t25_gputests.log 2>&1; tail -2 gpurun_out/t25_gputests.log
+timeout 500 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/t25.json 2> gpurun_out/t25.err
+timeout 500 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > gpurun_out/t25_ref.json 2> gpurun_out/t25_ref.err
+for c in c1 c2 c3 c4; do timeout 600 python bench.py --config $c --warmup 3 --skip-insitu > gpurun_out/t25_$c.json 2> gpurun_out/t25_$c.err; done
+timeout 600 python bench.py --config c2fold --warmup 2 --skip-insitu --skip-cpu > gpurun_out/t25_c2fold.json 2> gpurun_out/t25_c2fold.err
+DP_GRAPHS=0 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv \
+  --log-file gpurun_out/t25_launches.csv python bench.py --steps 20 --warmup 0 --warmup-seconds 0 --skip-cpu --skip-e2e --skip-insitu \
+  > gpurun_out/t25_ncu.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/t25_smoke.log 2>&1; tail -1 gpurun_out/t25_smoke.log

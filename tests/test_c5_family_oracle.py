@@ -47,3 +47,26 @@ def test_finger_schedule_is_independent_of_warmup():
     assert np.allclose(d[:bench.FINGER_HOLD], bench.FINGER_SPEED)
     assert np.all(d[bench.FINGER_HOLD:] == 0.0)
     assert bench.FINGER_K0 == 0
+
+
+def test_c2_fold_scene_and_targets():
+    """bench.py's C2 fold: a 40 x 40 sheet with self-contact, its right edge
+    bound; the edge targets are that edge rigidly folded about x = size/2 by
+    pi (k+1)/fold - vertical at mid-fold, mirrored onto the left half (lifted
+    by 2 mm) at the end - and the frictionless ground is the only collider."""
+    import bench
+    sc = bench.make_scene("c2fold")
+    c = bench.CONFIGS["c2fold"]
+    size = c["cells"][0] * c["edge"]
+    assert sc.self_contact and sc.h == c["h"] and len(sc.colliders) == 1 and sc.colliders[0].mu == 0.0
+    assert len(sc.bindings) == c["cells"][1] + 1
+    edge = np.array([sc.vertices[b.vertex] for b in sc.bindings])
+    assert np.allclose(edge[:, 0], size)
+    bench.move_fingers(sc, c["fold"] // 2 - 1)
+    mid = np.array([b.target for b in sc.bindings])
+    assert np.allclose(mid[:, 0], size / 2, atol=1e-12)
+    assert np.allclose(mid[:, 2], edge[:, 2] + size / 2 + 2e-3)
+    bench.move_fingers(sc, c["fold"] - 1)
+    end = np.array([b.target for b in sc.bindings])
+    assert np.allclose(end[:, 0], 0.0, atol=1e-12) and np.allclose(end[:, 1], edge[:, 1])
+    assert np.allclose(end[:, 2], edge[:, 2] + 2e-3, atol=1e-12)

@@ -1604,24 +1604,10 @@ __global__ void __launch_bounds__(kVT) k_gm_start(double reorth_thr, int V, cons
   }
 }
 
-// back substitution H[:used,:used] y = g[:used] of a finished cycle on the
-// device (one thread, the host loop's order and rounding: no FMA
-// contraction), so x is updated without a host round trip
-__global__ void k_gm_backsub(const GmresScalars* gs, double* y) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const int used = gs->used;
-  for (int i = used - 1; i >= 0; --i) {
-    double acc = gs->g[i];
-    for (int k = i + 1; k < used; ++k) acc = __dsub_rn(acc, __dmul_rn(gs->H[(size_t)k * kGM1 + i], y[k]));
-    y[i] = __ddiv_rn(acc, gs->H[(size_t)i * kGM1 + i]);
-  }
-}
-
 // x += sum_i y_i v_i   (or x = sum when accumulate == 0)
 template <typename TB>
 __global__ void k_gm_combine(int n, int used, const double* __restrict__ y, const TB* __restrict__ Vb, size_t ld,
-                             double* __restrict__ x, int accumulate, const GmresScalars* gs = nullptr) {
-  if (gs) used = gs->used;   // the cycle's column count, read on the device
+                             double* __restrict__ x, int accumulate) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     double acc = 0.0;
     for (int i = 0; i < used; ++i) acc += y[i] * (double)Vb[(size_t)i * ld + k];
@@ -2073,11 +2059,11 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
     }
     s->launches++;
     if (gg) {
-      // the whole cycle on the device: one graph launch; the back
-      // substitution, the x update and the true residual are queued behind
-      // it (below) and come back with ONE sync
+      // the whole cycle on the device: one graph launch, one sync
       cudaGraphLaunch(gg->exec, s->stream);
       cudaMemcpyAsync(s->h_gsc, s->gsc, gsc_bytes, cudaMemcpyDeviceToHost, s->stream);
+      host_sync(s);
+      s->launches += (int64_t)gg->nodes * std::max(1, s->h_gsc->used);
     } else {
       // host-driven columns, polled every 8
       bool stop = false;
@@ -2091,23 +2077,6 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
         stop = s->h_gsc->done || !s->h_gsc->active;
       }
     }
-    // back substitution on the device, x += (M^-1) V y with the device's
-    // column count (0 columns: x += 0), then the true residual: one sync
-    k_gm_backsub<<<1, 32, 0, s->stream>>>(s->gsc, y_dev);
-    if (zb) k_gm_combine<double><<<nbg, kGT, 0, s->stream>>>(n, 0, y_dev, s->gm_Z, ld, x, 1, s->gsc);
-    else if (lowp) k_gm_combine<float><<<nbg, kGT, 0, s->stream>>>(n, 0, y_dev, reinterpret_cast<const float*>(Vb), ld, t, 0, s->gsc);
-    else k_gm_combine<double><<<nbg, kGT, 0, s->stream>>>(n, 0, y_dev, Vb, ld, left ? x : t, left ? 1 : 0, s->gsc);
-    if (left || zb) {
-    } else if (use_mg) {
-      mg_apply(s, val, t, z, nullptr);
-      launch_axpy_to(s, x, x, 1.0, z);
-    } else {
-      k_minv_axpy<<<grid_for(V, 256), 256, 0, s->stream>>>(V, s->minv, t, x);
-    }
-    s->launches += 3;
-    true_relres_launch(s, val, b, x, r);
-    host_sync(s);
-    if (gg) s->launches += (int64_t)gg->nodes * std::max(1, s->h_gsc->used);
     if (bnorm < 0.0) {   // first cycle: |b| arrived with its sync
       bnorm = sqrt(s->h_aux[0]);
       if (bnorm == 0.0) {
@@ -2116,10 +2085,32 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
         return 0;
       }
     }
-    const int used = s->h_gsc->used;
+    const GmresScalars* hg = s->h_gsc;
+    const int used = hg->used;
     *iters += used;
     total = *iters;
-    rel = sqrt(s->h_ksc->pad[1]) / bnorm;
+    if (used > 0) {
+      // back substitution H[:used,:used] y = g[:used]; x += (M^-1) V y
+      double y[kMaxRestart];
+      for (int i = used - 1; i >= 0; --i) {
+        double acc = hg->g[i];
+        for (int k = i + 1; k < used; ++k) acc -= hg->H[(size_t)k * kGM1 + i] * y[k];
+        y[i] = acc / hg->H[(size_t)i * kGM1 + i];
+      }
+      cudaMemcpyAsync(y_dev, y, sizeof(double) * used, cudaMemcpyHostToDevice, s->stream);
+      if (zb) k_gm_combine<double><<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, s->gm_Z, ld, x, 1);
+      else if (lowp) k_gm_combine<float><<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, reinterpret_cast<const float*>(Vb), ld, t, 0);
+      else k_gm_combine<double><<<nbg, kGT, 0, s->stream>>>(n, used, y_dev, Vb, ld, left ? x : t, left ? 1 : 0);
+      if (left || zb) {
+      } else if (use_mg) {
+        mg_apply(s, val, t, z, nullptr);
+        launch_axpy_to(s, x, x, 1.0, z);
+      } else {
+        k_minv_axpy<<<grid_for(V, 256), 256, 0, s->stream>>>(V, s->minv, t, x);
+      }
+      s->launches += 2;
+    }
+    rel = true_relres(s, val, b, x, r, bnorm);
     have_rel = true;
     if (rel <= rtol) break;
     if (used == 0) break;

@@ -1985,24 +1985,16 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
   *iters = 0;
   // x = 0, or the caller's initial guess (use_x0) when it beats x = 0
   if (!use_x0) cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
-  // |b| comes back with the first sync of the solve (no sync of its own); a
-  // zero rhs returns x = 0 once it is known
-  norm2_async(s, b, &s->h_aux[0]);
-  double bnorm = -1.0;
+  const double bnorm = sqrt(device_norm2(s, b));
+  if (bnorm == 0.0) {
+    cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+    *relres = 0.0;
+    return 0;
+  }
   bool x_zero = !use_x0;
-  if (use_x0) {
-    true_relres_launch(s, val, b, x, s->kr);
-    host_sync(s);
-    bnorm = sqrt(s->h_aux[0]);
-    if (bnorm == 0.0) {
-      cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
-      *relres = 0.0;
-      return 0;
-    }
-    if (sqrt(s->h_ksc->pad[1]) / bnorm >= 1.0) {
-      cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
-      x_zero = true;
-    }
+  if (use_x0 && true_relres(s, val, b, x, s->kr, bnorm) >= 1.0) {
+    cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
+    x_zero = true;
   }
   // nmb = |b| (right) or |M^-1 b| (left, the reference's normalisation)
   if (left && use_mg) {
@@ -2075,14 +2067,6 @@ int gmres_solve(dp_scene* s, const double* val, const double* b, double* x, doub
         cudaMemcpyAsync(s->h_gsc, s->gsc, gsc_bytes, cudaMemcpyDeviceToHost, s->stream);
         host_sync(s);
         stop = s->h_gsc->done || !s->h_gsc->active;
-      }
-    }
-    if (bnorm < 0.0) {   // first cycle: |b| arrived with its sync
-      bnorm = sqrt(s->h_aux[0]);
-      if (bnorm == 0.0) {
-        cudaMemsetAsync(x, 0, sizeof(double) * n, s->stream);
-        *relres = 0.0;
-        return 0;
       }
     }
     const GmresScalars* hg = s->h_gsc;

@@ -456,6 +456,51 @@ __device__ __forceinline__ void inv3(const double a[9], double o[9]) {
   o[8] = (a[0] * a[4] - a[1] * a[3]) * id;
 }
 
+// The same product with an 8-lane group per coarse slot (4 slots per warp):
+// most coarse slots gather a few dozen fine blocks, so the 9-value
+// reduction over 8 lanes (3 shuffle rounds) replaces the 5-round warp tree
+// that dominated the warp-per-slot kernel.  Component-major layouts only.
+template <class TF>
+__global__ void __launch_bounds__(256) k_mg_galerkin8(int n, const int* __restrict__ slice_base,
+                                                      const int* __restrict__ diag_slot,
+                                                      const int* __restrict__ gal_ptr, const int* __restrict__ gal,
+                                                      const TF* __restrict__ valf, double* __restrict__ valc,
+                                                      double* __restrict__ minv, const int* __restrict__ slot_row,
+                                                      int64_t NS) {
+  const int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int g = threadIdx.x & 7;
+  const bool live = slot < NS;
+  const int t0 = live ? gal_ptr[slot] : 0, t1 = live ? gal_ptr[slot + 1] : 0;
+  double b[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int t = t0 + g; t < t1; t += 8) {
+    const TF* src = valf + gal[t];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) b[c] += (double)src[c * kSlice];
+  }
+#pragma unroll
+  for (int c = 0; c < 9; ++c) {
+    b[c] += __shfl_xor_sync(0xffffffffu, b[c], 4);
+    b[c] += __shfl_xor_sync(0xffffffffu, b[c], 2);
+    b[c] += __shfl_xor_sync(0xffffffffu, b[c], 1);
+  }
+  if (!live || t0 == t1) return;   // padding keeps the zero block from setup
+  const int ln = (int)(slot % kSlice);
+  double* dst = valc + (size_t)(slot - ln) * 9 + ln;
+  // lanes 0..7 of the group write components g and g + 8
+  double v = 0.0;
+#pragma unroll
+  for (int c = 0; c < 9; ++c) v = (g == c) ? b[c] : v;
+  dst[g * kSlice] = v;
+  if (g == 0) dst[8 * kSlice] = b[8];
+  const int row = slot_row[slot];
+  if (g == 0 && row < n && slot == diag_slot[row]) {
+    double o[9];
+    inv3(b, o);
+#pragma unroll
+    for (int c = 0; c < 9; ++c) minv[(size_t)c * n + row] = o[c];
+  }
+}
+
 // coarse operator: val_c[slot] = sum of the fine blocks in its gather list
 // (one warp per coarse slot, lanes over contributions); block-Jacobi inverse
 // of the diagonal slots.
@@ -1078,6 +1123,7 @@ __global__ void __launch_bounds__(DP_SMOOTH_NT) k_mg_smooth_pf(int n, int S, con
 
 // fine sweep ring filled by TMA bulk copies (depth 2; 0 = per-lane cp.async ring): in situ 24.7 -> 23.6 us
 static const int g_coarse_bulk = getenv("DP_COARSE_BULK") ? atoi(getenv("DP_COARSE_BULK")) : 1;
+static const int g_gal8 = getenv("DP_GAL8") ? atoi(getenv("DP_GAL8")) : 1;
 static const int g_smooth_bulk = getenv("DP_SMOOTH_BULK") ? atoi(getenv("DP_SMOOTH_BULK")) : 2;
 static const int g_smooth_pf = getenv("DP_SMOOTH_PF") ? atoi(getenv("DP_SMOOTH_PF")) : 0;   // measured slower (25.6 vs 24.1 us in situ), off
 
@@ -1531,7 +1577,10 @@ void mg_assemble(dp_scene* s, const double* val) {
   const double* vf = nullptr;
   for (size_t l = 1; l < mg->lv.size(); ++l) {
     MGLevel& L = mg->lv[l];
-    if (l == 1)
+    if (l == 1 && g_gal8 && DP_VAL32_PACKED == 0)
+      k_mg_galerkin8<float><<<grid_for(L.NS * 8, 256), 256, 0, s->stream>>>(
+          L.n, L.slice_base, L.diag_slot, L.gal_ptr, L.gal, s->val32, L.val, L.minv, L.slot_row, L.NS);
+    else if (l == 1)
       k_mg_galerkin<float, DP_VAL32_PACKED ? 1 : kSlice><<<grid_for(L.NS * 32, 256), 256, 0, s->stream>>>(
           L.n, L.S, L.slice_base, L.slice_width, L.diag_slot, L.gal_ptr, L.gal, s->val32, L.val, L.minv, L.slot_row,
           L.NS, DP_VAL32_PACKED == 2 ? s->val32 + (size_t)s->NS * 8 : nullptr);

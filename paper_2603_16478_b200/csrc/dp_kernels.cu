@@ -517,6 +517,11 @@ void launch_elements(dp_scene* s, const double* q, int mode, int* status) {
 
 constexpr int kVT = 256;
 
+#ifndef DP_RES_GROUP
+#define DP_RES_GROUP 8
+#endif
+constexpr int kResG = DP_RES_GROUP;   // fe loads in flight per row (measured 4 -> 8)
+
 // one row of the momentum residual (momentum_residual, forward.py:101-110):
 // M (q - q_hat) + element contributions (incidence order, 4 loads in flight)
 // + bindings + contact forces; shared by the full residual and the
@@ -538,12 +543,12 @@ __device__ __forceinline__ void residual_row(int i, const double* __restrict__ m
     // before the in-order accumulation)
     int k = inc_ptr[i];
     const int k1 = inc_ptr[i + 1];
-    for (; k + 4 <= k1; k += 4) {
-      double f[4][4];
+    for (; k + kResG <= k1; k += kResG) {
+      double f[kResG][4];
 #pragma unroll
-      for (int g = 0; g < 4; ++g) ld256(fe + (size_t)(k + g) * kFeS, f[g]);
+      for (int g = 0; g < kResG; ++g) ld256(fe + (size_t)(k + g) * kFeS, f[g]);
 #pragma unroll
-      for (int g = 0; g < 4; ++g) { r0 += f[g][0]; r1 += f[g][1]; r2 += f[g][2]; }
+      for (int g = 0; g < kResG; ++g) { r0 += f[g][0]; r1 += f[g][1]; r2 += f[g][2]; }
     }
     for (; k < k1; ++k) {
       double f[4];

@@ -774,17 +774,21 @@ __global__ void __launch_bounds__(256) k_assemble(int V, int S, const int* __res
       const float* hs32 = reinterpret_cast<const float*>(H) + (size_t)ri.x * 8;
       const float* ht32 = reinterpret_cast<const float*>(Ht) + ri.x;
       for (; t + ASM_CHUNK <= n; t += ASM_CHUNK) {
-        double src[ASM_CHUNK][9];
+        // the group's blocks held as floats (half the registers of doubles),
+        // widened exactly when accumulated
+        float fs[ASM_CHUNK][9];
 #pragma unroll
         for (int g = 0; g < ASM_CHUNK; ++g) {
-          float f[8];
-          ld256f(hs32 + (size_t)(t + g) * 8, f);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) src[g][c] = f[c];
-          src[g][8] = __ldg(ht32 + t + g);
+          ld256f(hs32 + (size_t)(t + g) * 8, fs[g]);
+          fs[g][8] = __ldg(ht32 + t + g);
         }
 #pragma unroll
-        for (int g = 0; g < ASM_CHUNK; ++g) acc_block(b, src[g], tr);
+        for (int g = 0; g < ASM_CHUNK; ++g) {
+          double src[9];
+#pragma unroll
+          for (int c = 0; c < 9; ++c) src[c] = fs[g][c];
+          acc_block(b, src, tr);
+        }
       }
       for (; t < n; ++t) {
         double src[9];

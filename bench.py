@@ -109,6 +109,10 @@ CONFIGS = {
     "c2": dict(cells=(100, 100, 0), edge=0.01, fingers=False, eps_fb=1e-9, tol=1e-11, rollouts=1, cloth=True, steps=4,
                desc="20,000-triangle ARAP cloth (1 m, 0.3 kg/m^2) draping over a frictional sphere, "
                     "per-step control-force gradients (C2 without self-contact: none in the reference)"),
+    "c2drape": dict(cells=(100, 100, 0), edge=0.01, fingers=False, eps_fb=1e-9, tol=1e-11, rollouts=1, cloth=True,
+                    h=0.0025, steps=48,
+                    desc="C2 drape at h = 2.5 ms: the 20,000-triangle cloth over the frictional sphere for 48 steps "
+                         "(0.12 s; at h = 10 ms the reference model's Newton stalls at step 4-6)"),
     "c2fold": dict(cells=(40, 40, 0), edge=0.01, fingers=False, eps_fb=1e-9, tol=1e-10, rollouts=1, cloth=True,
                    fold=120, h=0.005, comp=1e-4, steps=120,
                    desc="3,200-triangle ARAP sheet (40 cm) on a frictionless ground, its right edge bound to "
@@ -177,7 +181,7 @@ def make_scene(cfg_or_n, fingers=None, eps_fb=None, E=E_YOUNG, mu=None):
         mats = [core.MaterialParams("arap", stiffness=50.0)] * len(t)
         cx, cy = nx * c["edge"] / 2, ny * c["edge"] / 2
         cols = [core.HalfSpace([0, 0, 1], 0.0, mu=0.3), core.Sphere([cx, cy, 0.0], 0.25, mu=0.3)]
-        return core.Scene(v, t, core.lumped_masses(v, t, 0.3), mats, colliders=cols, h=0.01,
+        return core.Scene(v, t, core.lumped_masses(v, t, 0.3), mats, colliders=cols, h=c.get("h", 0.01),
                           eps_fb=c["eps_fb"] if eps_fb is None else eps_fb)
     if c.get("trunk"):
         return make_trunk(c, E)
